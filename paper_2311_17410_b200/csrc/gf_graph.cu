@@ -1,0 +1,926 @@
+// gf_graph.cu -- device block store: create/grow, batch append (K1), deletes, exports.
+//
+// K1 replaces DynamicGraph.add_edges / _append_edge / node_t_max
+// (reference storage.py:382-477).  The reference appends edge by edge; here a
+// whole batch is appended with sorts and scans, reproducing the reference's
+// state exactly (same block handles, capacities, links, slot order, ids):
+//   events (edge j, endpoint side) -> stable radix sort by node -> per-node
+//   segments -> chronology check (serial resolve only if a batch could reject)
+//   -> ids by scan -> per-segment block plan (capacity law with the live
+//   degree at allocation) -> new blocks sorted by the event that triggers them
+//   (= the reference's allocation order, so handles match) -> slot bases by
+//   scan in handle order -> metadata/directory/slot writes.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "gf_graph.cuh"
+
+using namespace gf;
+
+namespace {
+
+struct IngestCounters {
+  long long minv, maxv;   // node id range of the batch
+  long long viol;         // 1 if the batch may reject an edge
+  long long num_segs;     // distinct stored endpoints
+  long long n_acc;        // accepted edges
+  long long new_blocks;   // blocks to allocate
+  long long new_slots;    // slots to allocate
+  long long dir_need;     // directory entries to allocate
+  long long max_eid;      // max preassigned accepted id
+};
+
+template <class T>
+gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
+  T* q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, sizeof(T) * (size_t)std::max<int64_t>(new_cap, 1), s);
+  if (e != cudaSuccess) return fail(GF_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
+  if (p && keep > 0) GF_CUDA(cudaMemcpyAsync(q, p, sizeof(T) * (size_t)keep, cudaMemcpyDeviceToDevice, s));
+  if (p) cudaFreeAsync(p, s);
+  p = q;
+  return GF_OK;
+}
+
+__global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tail, int64_t* nb, int64_t* deg,
+                             uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap) {
+  for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi; v += (int64_t)gridDim.x * blockDim.x) {
+    head[v] = GF_NO_BLOCK;
+    tail[v] = GF_NO_BLOCK;
+    nb[v] = 0;
+    deg[v] = 0;
+    valid[v] = 1;
+    nslots[v] = 0;
+    doff[v] = -1;
+    dcap[v] = 0;
+  }
+}
+
+__global__ void k_minmax(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n,
+                         IngestCounters* c) {
+  long long mn = LLONG_MAX, mx = LLONG_MIN;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    long long a = src[i], b = dst[i];
+    mn = min(mn, min(a, b));
+    mx = max(mx, max(a, b));
+  }
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&c->minv, mn);
+    atomicMax(&c->maxv, mx);
+  }
+}
+
+// one event per (edge, stored endpoint), in the reference's append order
+__global__ void k_make_events(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n, int directed,
+                              uint32_t* keys, uint32_t* vals) {
+  int64_t E = directed ? n : 2 * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = directed ? e : (e >> 1);
+    int side = directed ? 0 : (int)(e & 1);
+    keys[e] = (uint32_t)(side ? dst[j] : src[j]);
+    vals[e] = (uint32_t)e;
+  }
+}
+
+__device__ __forceinline__ int64_t ev_edge(uint32_t ev, int directed) { return directed ? (int64_t)ev : (int64_t)(ev >> 1); }
+
+__device__ __forceinline__ int64_t node_tmax(const int64_t* tail, const int64_t* bsize, const int64_t* btmax, int64_t v) {
+  int64_t t = tail[v];
+  if (t == GF_NO_BLOCK || bsize[t] == 0) return GF_TS_MIN;  // storage.py:382-390
+  return btmax[t];
+}
+
+__global__ void k_heads(const uint32_t* __restrict__ keys, int64_t E, int32_t* heads) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x)
+    heads[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// seg_id = inclusive_scan(heads) - 1; record segment starts, detect possible rejections
+__global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl,
+                           int64_t E, int directed, const int64_t* __restrict__ ts, const int64_t* tail, const int64_t* bsize,
+                           const int64_t* btmax, int64_t* seg_start, IngestCounters* c) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = incl[i] - 1;
+    bool head = (i == 0) || keys[i] != keys[i - 1];
+    int64_t t = ts[ev_edge(vals[i], directed)];
+    bool viol;
+    if (head) {
+      seg_start[s] = i;
+      viol = t < node_tmax(tail, bsize, btmax, keys[i]);
+    } else {
+      viol = t < ts[ev_edge(vals[i - 1], directed)];
+    }
+    if (viol) atomicOr((unsigned long long*)&c->viol, 1ull);
+    if (i == E - 1) c->num_segs = s + 1;
+  }
+}
+
+__global__ void k_accept_all(uint8_t* acc, int64_t n, const IngestCounters* c) {
+  if (c->viol) return;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
+}
+
+__global__ void k_tmax_init(int64_t* tm, int64_t num_nodes, const int64_t* tail, const int64_t* bsize, const int64_t* btmax,
+                            const IngestCounters* c) {
+  if (!c->viol) return;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < num_nodes; v += (int64_t)gridDim.x * blockDim.x)
+    tm[v] = node_tmax(tail, bsize, btmax, v);
+}
+
+// Sequential chronology resolve (storage.py:426-437): only when a batch may reject.
+__global__ void k_accept_serial(const int64_t* src, const int64_t* dst, const int64_t* ts, int64_t n, int directed,
+                                int64_t* tm, uint8_t* acc, const IngestCounters* c) {
+  if (!c->viol || threadIdx.x || blockIdx.x) return;
+  for (int64_t j = 0; j < n; j++) {
+    int64_t s = src[j], d = dst[j], t = ts[j];
+    bool ok = t >= tm[s] && (directed || t >= tm[d]);
+    acc[j] = ok;
+    if (ok) {
+      tm[s] = t;
+      if (!directed) tm[d] = t;
+    }
+  }
+}
+
+__global__ void k_keep(const uint32_t* __restrict__ vals, int64_t E, int directed, const uint8_t* __restrict__ acc,
+                       int64_t* keep) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x)
+    keep[i] = acc[ev_edge(vals[i], directed)];
+  if (blockIdx.x == 0 && threadIdx.x == 0) keep[E] = 0;
+}
+
+__global__ void k_eids(const uint8_t* __restrict__ acc, const int64_t* __restrict__ rank, int64_t n, int64_t next_id,
+                       const int64_t* __restrict__ eids_in, int64_t* out_eids, IngestCounters* c) {
+  long long mx = LLONG_MIN;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = -1;
+    if (acc[j]) {
+      e = eids_in ? eids_in[j] : next_id + rank[j];
+      mx = max(mx, (long long)e);
+    }
+    out_eids[j] = e;
+    if (j == n - 1) c->n_acc = rank[j] + acc[j];
+  }
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx != LLONG_MIN) atomicMax(&c->max_eid, mx);
+}
+
+// compacted accepted events (segment-major, arrival order inside a segment)
+__global__ void k_compact(const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl, const int64_t* __restrict__ cpos,
+                          const int64_t* __restrict__ keep, const int64_t* __restrict__ seg_start, int64_t E,
+                          const IngestCounters* c, uint32_t* ce_ev, int64_t* ce_pend, int32_t* ce_seg) {
+  int64_t nseg = c->num_segs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    int32_t s = incl[i] - 1;
+    int64_t end = (s + 1 < nseg) ? seg_start[s + 1] : E;
+    int64_t p = cpos[i];
+    ce_ev[p] = vals[i];
+    ce_pend[p] = end - i;  // pending count incl. later rejected events (storage.py:417-447)
+    ce_seg[p] = s;
+  }
+}
+
+__device__ __forceinline__ int64_t sizing_cap(int kind, int64_t tau, int64_t param, int64_t degree, int64_t pending) {
+  if (kind == GF_SIZING_FIXED) return param;                // storage.py:102-103
+  if (kind == GF_SIZING_BATCH) return pending > 1 ? pending : 1;  // storage.py:116-117
+  int64_t d = degree > 1 ? degree : 1;                      // storage.py:88-89
+  return d < tau ? d : tau;
+}
+
+struct SegPlan {
+  int64_t* acc_cnt;   // accepted events per segment
+  int64_t* cstart;    // start in the compacted event list
+  int64_t* fill;      // events that go into the current tail
+  int64_t* tail_size; // tail size before the batch
+  int64_t* nb_new;    // new blocks (E+1, zero padded)
+  int64_t* slots_new; // new slots (E+1)
+  int64_t* dir_new;   // new directory capacity (E+1)
+};
+
+__global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
+                       const int64_t* __restrict__ cpos, const int64_t* __restrict__ ce_pend, int64_t E,
+                       const IngestCounters* c, const int64_t* tail, const int64_t* bsize, const int64_t* bcap,
+                       const int64_t* degree, const int64_t* num_blocks, const int64_t* dir_cap, int kind, int64_t tau,
+                       int64_t param, SegPlan P) {
+  int64_t nseg = c->num_segs;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t st = seg_start[s], en = (s + 1 < nseg) ? seg_start[s + 1] : E;
+    int64_t cs = cpos[st], cnt = cpos[en] - cs;
+    int64_t v = keys[st];
+    P.acc_cnt[s] = cnt;
+    P.cstart[s] = cs;
+    int64_t t = tail[v];
+    int64_t fill = 0, tsz = 0;
+    if (t != GF_NO_BLOCK) {
+      tsz = bsize[t];
+      fill = min(bcap[t] - tsz, cnt);
+    }
+    P.fill[s] = fill;
+    P.tail_size[s] = tsz;
+    int64_t deg = degree[v] + fill, rem = cnt - fill, used = fill, blocks = 0, slots = 0;
+    while (rem > 0) {
+      int64_t cap = sizing_cap(kind, tau, param, deg, ce_pend[cs + used]);
+      int64_t take = min(cap, rem);
+      blocks++;
+      slots += cap;
+      deg += take;
+      used += take;
+      rem -= take;
+    }
+    P.nb_new[s] = blocks;
+    P.slots_new[s] = slots;
+    int64_t need = num_blocks[v] + blocks;
+    int64_t dc = dir_cap[v];
+    if (need > dc) {
+      int64_t nc = 8;
+      while (nc < need) nc <<= 1;
+      P.dir_new[s] = nc;
+    } else {
+      P.dir_new[s] = 0;
+    }
+  }
+}
+
+__global__ void k_totals(const int64_t* blkoff, const int64_t* slotsoff, const int64_t* diroff, int64_t E, IngestCounters* c) {
+  if (threadIdx.x || blockIdx.x) return;
+  c->new_blocks = blkoff[E];
+  c->new_slots = slotsoff[E];
+  c->dir_need = diroff[E];
+}
+
+struct Recs {
+  int64_t* first;   // segment-local accepted rank of the block's first event
+  int64_t* count;   // events placed in the block
+  int64_t* cap;     // capacity
+  int32_t* seg;     // owning segment
+  uint32_t* key;    // original event index of the first event = allocation order
+  uint32_t* idx;    // identity values for the sort
+  int64_t* handle;  // assigned handle
+};
+
+__global__ void k_enumerate(const int64_t* __restrict__ ce_pend, const uint32_t* __restrict__ ce_ev, const IngestCounters* c,
+                            const int64_t* __restrict__ blkoff, const int64_t* __restrict__ keys_node_of_seg_unused,
+                            SegPlan P, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
+                            const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R) {
+  int64_t nseg = c->num_segs;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t nb = P.nb_new[s];
+    if (!nb) continue;
+    int64_t v = keys[seg_start[s]];
+    int64_t cs = P.cstart[s], cnt = P.acc_cnt[s], fill = P.fill[s];
+    int64_t deg = degree[v] + fill, used = fill, rem = cnt - fill;
+    int64_t r = blkoff[s];
+    while (rem > 0) {
+      int64_t cap = sizing_cap(kind, tau, param, deg, ce_pend[cs + used]);
+      int64_t take = min(cap, rem);
+      R.first[r] = used;
+      R.count[r] = take;
+      R.cap[r] = cap;
+      R.seg[r] = (int32_t)s;
+      R.key[r] = ce_ev[cs + used];
+      R.idx[r] = (uint32_t)r;
+      r++;
+      deg += take;
+      used += take;
+      rem -= take;
+    }
+  }
+}
+
+__global__ void k_assign_handles(const uint32_t* __restrict__ perm, int64_t nrec, int64_t blk_used, const int64_t* rcap,
+                                 int64_t* handle, int64_t* cap_sorted) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t rec = perm[r];
+    handle[rec] = blk_used + r;
+    cap_sorted[r] = rcap[rec];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cap_sorted[nrec] = 0;
+}
+
+struct BlockArrays {
+  int64_t *cap, *size, *tmin, *tmax, *prev, *next, *base;
+};
+
+__global__ void k_write_blocks(const uint32_t* __restrict__ perm, int64_t nrec, int64_t blk_used, int64_t slots_used,
+                               const int64_t* __restrict__ base_scan, Recs R, const int64_t* __restrict__ blkoff, SegPlan P,
+                               const uint32_t* __restrict__ ce_ev, const uint32_t* __restrict__ keys,
+                               const int64_t* __restrict__ seg_start, const int64_t* tail, const int64_t* __restrict__ ts,
+                               int directed, BlockArrays B) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t rec = perm[r];
+    int64_t h = blk_used + r;
+    int32_t s = R.seg[rec];
+    int64_t k = rec - blkoff[s], nb = P.nb_new[s];
+    int64_t cs = P.cstart[s];
+    int64_t f = R.first[rec], cnt = R.count[rec];
+    B.cap[h] = R.cap[rec];
+    B.size[h] = cnt;
+    B.tmin[h] = ts[ev_edge(ce_ev[cs + f], directed)];
+    B.tmax[h] = ts[ev_edge(ce_ev[cs + f + cnt - 1], directed)];
+    B.base[h] = slots_used + base_scan[r];
+    int64_t v = keys[seg_start[s]];
+    B.prev[h] = (k == 0) ? tail[v] : R.handle[rec - 1];
+    B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : R.handle[rec + 1];
+  }
+}
+
+struct NodeArrays {
+  int64_t *head, *tail, *num_blocks, *degree, *nslots, *dir_off, *dir_cap;
+};
+struct DirArrays {
+  int64_t *tmin, *cum, *base;
+};
+
+__global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
+                           SegPlan P, const int64_t* __restrict__ blkoff, const int64_t* __restrict__ diroff, int64_t dir_used,
+                           Recs R, const uint32_t* __restrict__ ce_ev, const int64_t* __restrict__ ts, int directed,
+                           NodeArrays N, BlockArrays B, DirArrays D) {
+  int64_t nseg = c->num_segs;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t cnt = P.acc_cnt[s];
+    if (!cnt) continue;
+    int64_t v = keys[seg_start[s]];
+    int64_t t = N.tail[v], fill = P.fill[s], nb = P.nb_new[s], cs = P.cstart[s];
+    int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v];
+    if (t != GF_NO_BLOCK && fill > 0) {
+      B.size[t] = P.tail_size[s] + fill;
+      B.tmax[t] = ts[ev_edge(ce_ev[cs + fill - 1], directed)];
+    }
+    if (nb > 0) {
+      int64_t h0 = R.handle[blkoff[s]];
+      if (t == GF_NO_BLOCK) N.head[v] = h0;
+      else B.next[t] = h0;
+      N.tail[v] = R.handle[blkoff[s] + nb - 1];
+      // block directory: grow (copy) if needed, then append the new blocks
+      if (P.dir_new[s] > 0) {
+        int64_t no = dir_used + diroff[s], oo = N.dir_off[v];
+        for (int64_t b = 0; b < nb_old; b++) {
+          D.tmin[no + b] = D.tmin[oo + b];
+          D.cum[no + b] = D.cum[oo + b];
+          D.base[no + b] = D.base[oo + b];
+        }
+        N.dir_off[v] = no;
+        N.dir_cap[v] = P.dir_new[s];
+      }
+      int64_t d0 = N.dir_off[v] + nb_old;
+      for (int64_t k = 0; k < nb; k++) {
+        int64_t rec = blkoff[s] + k, h = R.handle[rec];
+        D.tmin[d0 + k] = B.tmin[h];
+        D.cum[d0 + k] = ns_old + R.first[rec];
+        D.base[d0 + k] = B.base[h];
+      }
+    }
+    N.num_blocks[v] = nb_old + nb;
+    N.degree[v] += cnt;
+    N.nslots[v] = ns_old + cnt;
+  }
+}
+
+__global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restrict__ ce_seg, const uint32_t* __restrict__ ce_ev,
+                                const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start, SegPlan P,
+                                const int64_t* __restrict__ blkoff, Recs R, const int64_t* tail_before_unused,
+                                const int64_t* __restrict__ bbase, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                                const int64_t* __restrict__ ts, const int64_t* __restrict__ eids, int directed,
+                                const int64_t* __restrict__ old_tail, Slot* slots) {
+  int64_t nacc_ev = 0;
+  {
+    int64_t nseg = c->num_segs;
+    nacc_ev = P.cstart[nseg - 1] + P.acc_cnt[nseg - 1];
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nacc_ev; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = ce_seg[i];
+    int64_t r = i - P.cstart[s];
+    uint32_t ev = ce_ev[i];
+    int64_t j = ev_edge(ev, directed);
+    int side = directed ? 0 : (int)(ev & 1);
+    int64_t v = keys[seg_start[s]];
+    int64_t pos;
+    int64_t fill = P.fill[s];
+    if (r < fill) {
+      pos = bbase[old_tail[s]] + P.tail_size[s] + r;
+    } else {
+      int64_t lo = blkoff[s], hi = blkoff[s] + P.nb_new[s];  // last rec with first <= r
+      while (hi - lo > 1) {
+        int64_t m = (lo + hi) >> 1;
+        if (R.first[m] <= r) lo = m;
+        else hi = m;
+      }
+      pos = bbase[R.handle[lo]] + (r - R.first[lo]);
+    }
+    Slot sl;
+    sl.ts = ts[j];
+    sl.eid = eids[j];
+    sl.nbr = (int32_t)(side ? src[j] : dst[j]);
+    sl.owner = (int32_t)v;
+    sl.valid = 1;
+    sl.pad = 0;
+    slots[pos] = sl;
+  }
+}
+
+__global__ void k_old_tail(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
+                           const int64_t* tail, int64_t* old_tail) {
+  int64_t nseg = c->num_segs;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x)
+    old_tail[s] = tail[keys[seg_start[s]]];
+}
+
+template <class F>
+gf_status cub_call(F f, cudaStream_t s) {
+  size_t bytes = 0;
+  GF_CUDA(f((void*)nullptr, bytes));
+  Scratch tmp(s);
+  GF_TRY(tmp.alloc(bytes));
+  GF_CUDA(f(tmp.p, bytes));
+  return GF_OK;
+}
+
+int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 32 && ((int64_t)1 << b) < n) b++;
+  return b;
+}
+
+gf_status ensure_nodes(gf_graph* g, int64_t need, cudaStream_t s) {
+  if (need <= g->num_nodes) return GF_OK;
+  if (need > ((int64_t)1 << 31)) return fail(GF_EINVAL, "node ids must be < 2^31");
+  if (need > g->node_cap) {
+    int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, g->node_cap * 2));
+    int64_t k = g->num_nodes;
+    GF_TRY(grow_array(g->head, k, nc, s));
+    GF_TRY(grow_array(g->tail, k, nc, s));
+    GF_TRY(grow_array(g->num_blocks, k, nc, s));
+    GF_TRY(grow_array(g->degree, k, nc, s));
+    GF_TRY(grow_array(g->node_valid, k, nc, s));
+    GF_TRY(grow_array(g->nslots, k, nc, s));
+    GF_TRY(grow_array(g->dir_off, k, nc, s));
+    GF_TRY(grow_array(g->dir_cap, k, nc, s));
+    g->node_cap = nc;
+  }
+  int64_t cnt = need - g->num_nodes;
+  GF_LAUNCH(k_init_nodes, grid_for(cnt, 256, 4096), 256, 0, s, g->num_nodes, need, g->head, g->tail, g->num_blocks,
+            g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap);
+  g->num_nodes = need;
+  return GF_OK;
+}
+
+gf_status ensure_blocks(gf_graph* g, int64_t need, cudaStream_t s) {
+  if (need <= g->blk_cap) return GF_OK;
+  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, g->blk_cap * 2));
+  int64_t k = g->blk_used;
+  GF_TRY(grow_array(g->bcap, k, nc, s));
+  GF_TRY(grow_array(g->bsize, k, nc, s));
+  GF_TRY(grow_array(g->btmin, k, nc, s));
+  GF_TRY(grow_array(g->btmax, k, nc, s));
+  GF_TRY(grow_array(g->bprev, k, nc, s));
+  GF_TRY(grow_array(g->bnext, k, nc, s));
+  GF_TRY(grow_array(g->bbase, k, nc, s));
+  g->blk_cap = nc;
+  return GF_OK;
+}
+
+gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
+  if (need <= g->slot_cap) return GF_OK;
+  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(4096, g->slot_cap + g->slot_cap / 2));
+  int64_t old = g->slot_cap;
+  GF_TRY(grow_array(g->slots, g->slots_used, nc, s));
+  // unused capacity slots must read as invalid (delete scans the whole pool)
+  GF_CUDA(cudaMemsetAsync(g->slots + old, 0, sizeof(Slot) * (size_t)(nc - old), s));
+  g->slot_cap = nc;
+  return GF_OK;
+}
+
+gf_status ensure_dir(gf_graph* g, int64_t need, cudaStream_t s) {
+  if (need <= g->dir_cap_total) return GF_OK;
+  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(4096, g->dir_cap_total * 2));
+  GF_TRY(grow_array(g->dtmin, g->dir_used, nc, s));
+  GF_TRY(grow_array(g->dcum, g->dir_used, nc, s));
+  GF_TRY(grow_array(g->dbase, g->dir_used, nc, s));
+  g->dir_cap_total = nc;
+  return GF_OK;
+}
+
+gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, const int64_t* ts, int64_t n,
+                         const int64_t* eids_in, int64_t* out_eids, int64_t* h_rej, cudaStream_t s) {
+  if (h_rej) *h_rej = 0;
+  if (n == 0) return GF_OK;
+  if (n < 0 || n >= ((int64_t)1 << 30)) return fail(GF_EINVAL, "batch size must be in [0, 2^30)");
+  const int dir = g->directed;
+  const int64_t E = dir ? n : 2 * n;
+
+  Scratch cbuf(s);
+  GF_TRY(cbuf.alloc(sizeof(IngestCounters)));
+  IngestCounters* dc = cbuf.as<IngestCounters>();
+  IngestCounters hc;
+  memset(&hc, 0, sizeof(hc));
+  hc.minv = LLONG_MAX;
+  hc.maxv = LLONG_MIN;
+  hc.max_eid = LLONG_MIN;
+  GF_CUDA(cudaMemcpyAsync(dc, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+  GF_LAUNCH(k_minmax, grid_for(n, 256, 2 * num_sms()), 256, 0, s, src, dst, n, dc);
+  GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+  if (hc.minv < 0) return fail(GF_EINVAL, "node ids must be non-negative");  // storage.py:408-409
+  GF_TRY(ensure_nodes(g, hc.maxv + 1, s));                                  // storage.py:410-412
+
+  // ---- scratch --------------------------------------------------------------
+  Scratch sb(s);
+  Arena A;
+  size_t need = 0;
+  {
+    Arena probe;
+    probe.take<uint32_t>(E); probe.take<uint32_t>(E); probe.take<uint32_t>(E); probe.take<uint32_t>(E);
+    probe.take<int32_t>(E); probe.take<int32_t>(E); probe.take<int64_t>(E + 1);
+    probe.take<uint8_t>(n); probe.take<int64_t>(n + 1); probe.take<int64_t>(g->num_nodes);
+    probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1);
+    probe.take<uint32_t>(E); probe.take<int64_t>(E); probe.take<int32_t>(E);
+    for (int q = 0; q < 7; q++) probe.take<int64_t>(E + 1);
+    probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1);
+    need = probe.off + 4096;
+  }
+  GF_TRY(sb.alloc(need));
+  A.base = sb.as<char>();
+  uint32_t* keys_in = A.take<uint32_t>(E);
+  uint32_t* keys = A.take<uint32_t>(E);
+  uint32_t* vals_in = A.take<uint32_t>(E);
+  uint32_t* vals = A.take<uint32_t>(E);
+  int32_t* heads = A.take<int32_t>(E);
+  int32_t* incl = A.take<int32_t>(E);
+  int64_t* seg_start = A.take<int64_t>(E + 1);
+  uint8_t* acc = A.take<uint8_t>(n);
+  int64_t* rank = A.take<int64_t>(n + 1);
+  int64_t* tm = A.take<int64_t>(g->num_nodes);
+  int64_t* keep = A.take<int64_t>(E + 1);
+  int64_t* cpos = A.take<int64_t>(E + 1);
+  uint32_t* ce_ev = A.take<uint32_t>(E);
+  int64_t* ce_pend = A.take<int64_t>(E);
+  int32_t* ce_seg = A.take<int32_t>(E);
+  SegPlan P;
+  P.acc_cnt = A.take<int64_t>(E + 1);
+  P.cstart = A.take<int64_t>(E + 1);
+  P.fill = A.take<int64_t>(E + 1);
+  P.tail_size = A.take<int64_t>(E + 1);
+  P.nb_new = A.take<int64_t>(E + 1);
+  P.slots_new = A.take<int64_t>(E + 1);
+  P.dir_new = A.take<int64_t>(E + 1);
+  int64_t* blkoff = A.take<int64_t>(E + 1);
+  int64_t* slotsoff = A.take<int64_t>(E + 1);
+  int64_t* diroff = A.take<int64_t>(E + 1);
+  int64_t* old_tail = A.take<int64_t>(E + 1);
+
+  const int T = 256;
+  const int64_t G = 8 * num_sms();
+  GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in);
+  int endbit = bits_for(g->num_nodes);
+  GF_TRY(cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s);
+  }, s));
+  GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
+  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, heads, incl, (int)E, s); }, s));
+  GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
+            seg_start, dc);
+  // chronology: accept all unless some stored endpoint sees a decreasing timestamp
+  GF_LAUNCH(k_accept_all, grid_for(n, T, G), T, 0, s, acc, n, dc);
+  GF_LAUNCH(k_tmax_init, grid_for(g->num_nodes, T, G), T, 0, s, tm, g->num_nodes, g->tail, g->bsize, g->btmax, dc);
+  GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
+  // edge ids by scan (storage.py:438-442)
+  GF_TRY(cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, acc, rank, (int)n, s);
+  }, s));
+  GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, g->next_edge_id, eids_in, out_eids, dc);
+  GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep);
+  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, keep, cpos, (int)(E + 1), s); }, s));
+  GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
+  GF_CUDA(cudaMemsetAsync(P.nb_new, 0, sizeof(int64_t) * (E + 1), s));
+  GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
+  GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
+  GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
+            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P);
+  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.nb_new, blkoff, (int)(E + 1), s); }, s));
+  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.slots_new, slotsoff, (int)(E + 1), s); }, s));
+  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.dir_new, diroff, (int)(E + 1), s); }, s));
+  GF_LAUNCH(k_totals, 1, 1, 0, s, blkoff, slotsoff, diroff, E, dc);
+  GF_LAUNCH(k_old_tail, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, g->tail, old_tail);
+  GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+
+  const int64_t nrec = hc.new_blocks;
+  GF_TRY(ensure_blocks(g, g->blk_used + nrec, s));
+  GF_TRY(ensure_slots(g, g->slots_used + hc.new_slots, s));
+  GF_TRY(ensure_dir(g, g->dir_used + hc.dir_need, s));
+
+  Scratch rb(s);
+  Arena RA;
+  {
+    Arena probe;
+    for (int q = 0; q < 3; q++) probe.take<int64_t>(nrec + 1);
+    probe.take<int32_t>(nrec); probe.take<uint32_t>(nrec); probe.take<uint32_t>(nrec); probe.take<uint32_t>(nrec);
+    probe.take<uint32_t>(nrec); probe.take<int64_t>(nrec + 1); probe.take<int64_t>(nrec + 1); probe.take<int64_t>(nrec + 1);
+    GF_TRY(rb.alloc(probe.off + 4096));
+  }
+  RA.base = rb.as<char>();
+  Recs R;
+  R.first = RA.take<int64_t>(nrec + 1);
+  R.count = RA.take<int64_t>(nrec + 1);
+  R.cap = RA.take<int64_t>(nrec + 1);
+  R.seg = RA.take<int32_t>(nrec);
+  R.key = RA.take<uint32_t>(nrec);
+  R.idx = RA.take<uint32_t>(nrec);
+  uint32_t* key_sorted = RA.take<uint32_t>(nrec);
+  uint32_t* perm = RA.take<uint32_t>(nrec);
+  R.handle = RA.take<int64_t>(nrec + 1);
+  int64_t* cap_sorted = RA.take<int64_t>(nrec + 1);
+  int64_t* base_scan = RA.take<int64_t>(nrec + 1);
+
+  if (nrec > 0) {
+    GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
+              g->degree, g->sizing_kind, g->tau, g->sizing_param, R);
+    int kb = bits_for(E + 1);
+    GF_TRY(cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, R.key, key_sorted, R.idx, perm, (int)nrec, 0, kb, s);
+    }, s));
+    GF_LAUNCH(k_assign_handles, grid_for(nrec, T, G), T, 0, s, perm, nrec, g->blk_used, R.cap, R.handle, cap_sorted);
+    GF_TRY(cub_call([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, cap_sorted, base_scan, (int)(nrec + 1), s);
+    }, s));
+    BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
+    GF_LAUNCH(k_write_blocks, grid_for(nrec, T, G), T, 0, s, perm, nrec, g->blk_used, g->slots_used, base_scan, R,
+              blkoff, P, ce_ev, keys, seg_start, g->tail, ts, dir, B);
+  }
+  if (hc.n_acc > 0) {
+    BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
+    NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap};
+    DirArrays D{g->dtmin, g->dcum, g->dbase};
+    GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
+              dir, N, B, D);
+    GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
+              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots);
+  }
+  g->blk_used += nrec;
+  g->slots_used += hc.new_slots;
+  g->dir_used += hc.dir_need;
+  if (eids_in) {
+    if (hc.n_acc > 0 && hc.max_eid + 1 > g->next_edge_id) g->next_edge_id = hc.max_eid + 1;
+  } else {
+    g->next_edge_id += hc.n_acc;
+  }
+  g->total_edges_inserted += hc.n_acc;
+  if (h_rej) *h_rej = n - hc.n_acc;
+  GF_CUDA(cudaGetLastError());
+  return GF_OK;
+}
+
+// ---- deletes (storage.py:479-512) ------------------------------------------
+__global__ void k_delete_scan(Slot* slots, int64_t nslots, const int64_t* __restrict__ wanted, int64_t nw, int64_t* degree,
+                              uint8_t* hit) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x) {
+    Slot sl = slots[i];
+    if (!sl.valid) continue;
+    int64_t lo = 0, hi = nw;
+    while (lo < hi) {
+      int64_t m = (lo + hi) >> 1;
+      if (wanted[m] < sl.eid) lo = m + 1;
+      else hi = m;
+    }
+    if (lo < nw && wanted[lo] == sl.eid) {
+      slots[i].valid = 0;
+      atomicAdd((unsigned long long*)&degree[sl.owner], (unsigned long long)(-1LL));
+      hit[lo] = 1;
+    }
+  }
+}
+
+__global__ void k_count_hits(const uint8_t* hit, int64_t n, long long* out) {
+  long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) c += hit[i];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long*)out, (unsigned long long)c);
+}
+
+__global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bbase, const int64_t* __restrict__ offs,
+                               int64_t h0, int64_t nblk, int64_t* nbr, int64_t* eid, int64_t* ts, uint8_t* valid) {
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    int64_t o = offs[b], cnt = offs[b + 1] - o, base = bbase[h0 + b];
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      Slot sl = slots[base + i];
+      nbr[o + i] = sl.nbr;
+      eid[o + i] = sl.eid;
+      ts[o + i] = sl.ts;
+      valid[o + i] = (uint8_t)(sl.valid != 0);
+    }
+  }
+}
+
+void free_graph(gf_graph* g) {
+  void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
+                g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dtmin, g->dcum, g->dbase,
+                g->slots};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+}
+
+}  // namespace
+
+extern "C" {
+
+gf_status gf_graph_create(int directed, int64_t tau, int sizing_kind, int64_t sizing_param, int device, gf_graph** out) {
+  if (!out) return fail(GF_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (sizing_kind == GF_SIZING_ADAPTIVE && tau < 1) return fail(GF_EINVAL, "tau must be >= 1");  // storage.py:85-86, 314-315
+  if (sizing_kind == GF_SIZING_FIXED && sizing_param < 1) return fail(GF_EINVAL, "block size must be >= 1");
+  if (sizing_kind < 0 || sizing_kind > 2) return fail(GF_EINVAL, "unknown sizing kind");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(GF_ECUDA, "no CUDA device available");
+  if (device < 0 || device >= ndev) return fail(GF_EINVAL, "bad device ordinal");
+  gf_graph* g = new gf_graph();
+  g->device = device;
+  g->directed = directed ? 1 : 0;
+  g->tau = tau;
+  g->sizing_kind = sizing_kind;
+  g->sizing_param = sizing_param;
+  *out = g;
+  return GF_OK;
+}
+
+gf_status gf_graph_destroy(gf_graph* g) {
+  if (!g) return GF_OK;
+  DeviceGuard dg(g->device);
+  cudaDeviceSynchronize();
+  free_graph(g);
+  delete g;
+  return GF_OK;
+}
+
+gf_status gf_graph_reserve(gf_graph* g, int64_t nodes, int64_t blocks, int64_t slots, void* stream) {
+  if (!g) return fail(GF_EINVAL, "graph is NULL");
+  DeviceGuard dg(g->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nodes > g->node_cap) {
+    int64_t k = g->num_nodes, nc = nodes;
+    GF_TRY(grow_array(g->head, k, nc, s));
+    GF_TRY(grow_array(g->tail, k, nc, s));
+    GF_TRY(grow_array(g->num_blocks, k, nc, s));
+    GF_TRY(grow_array(g->degree, k, nc, s));
+    GF_TRY(grow_array(g->node_valid, k, nc, s));
+    GF_TRY(grow_array(g->nslots, k, nc, s));
+    GF_TRY(grow_array(g->dir_off, k, nc, s));
+    GF_TRY(grow_array(g->dir_cap, k, nc, s));
+    g->node_cap = nc;
+  }
+  GF_TRY(ensure_blocks(g, blocks, s));
+  GF_TRY(ensure_slots(g, slots, s));
+  GF_TRY(ensure_dir(g, blocks * 2, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
+}
+
+gf_status gf_graph_add_edges(gf_graph* g, const int64_t* d_src, const int64_t* d_dst, const int64_t* d_ts, int64_t n,
+                             const int64_t* d_eids_in, int64_t* d_out_eids, int64_t* h_out_rejected, void* stream) {
+  if (!g) return fail(GF_EINVAL, "graph is NULL");
+  if (n > 0 && (!d_src || !d_dst || !d_ts || !d_out_eids)) return fail(GF_EINVAL, "NULL input array");
+  DeviceGuard dg(g->device);
+  return add_edges_impl(g, d_src, d_dst, d_ts, n, d_eids_in, d_out_eids, h_out_rejected, (cudaStream_t)stream);
+}
+
+gf_status gf_graph_delete_edges(gf_graph* g, const int64_t* d_eids, int64_t n, int64_t* h_out_deleted, void* stream) {
+  if (!g) return fail(GF_EINVAL, "graph is NULL");
+  if (h_out_deleted) *h_out_deleted = 0;
+  if (n <= 0 || g->slots_used == 0) return GF_OK;
+  DeviceGuard dg(g->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch sb(s);
+  Arena A;
+  {
+    Arena probe;
+    probe.take<int64_t>(n); probe.take<uint8_t>(n); probe.take<long long>(1);
+    GF_TRY(sb.alloc(probe.off + 1024));
+  }
+  A.base = sb.as<char>();
+  int64_t* sorted = A.take<int64_t>(n);
+  uint8_t* hit = A.take<uint8_t>(n);
+  long long* cnt = A.take<long long>(1);
+  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, d_eids, sorted, (int)n, 0, 64, s); }, s));
+  GF_CUDA(cudaMemsetAsync(hit, 0, n, s));
+  GF_CUDA(cudaMemsetAsync(cnt, 0, sizeof(long long), s));
+  GF_LAUNCH(k_delete_scan, grid_for(g->slots_used, 256, 16 * num_sms()), 256, 0, s, g->slots, g->slots_used, sorted, n,
+            g->degree, hit);
+  GF_LAUNCH(k_count_hits, grid_for(n, 256, 4 * num_sms()), 256, 0, s, hit, n, cnt);
+  long long h = 0;
+  GF_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+  if (h > 0) g->any_deleted = 1;
+  if (h_out_deleted) *h_out_deleted = h;
+  return GF_OK;
+}
+
+gf_status gf_graph_delete_node(gf_graph* g, int64_t node, int* h_out_deleted, void* stream) {
+  if (!g) return fail(GF_EINVAL, "graph is NULL");
+  if (h_out_deleted) *h_out_deleted = 0;
+  if (node < 0 || node >= g->num_nodes) return GF_OK;
+  DeviceGuard dg(g->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t v = 0;
+  GF_CUDA(cudaMemcpyAsync(&v, g->node_valid + node, 1, cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+  if (!v) return GF_OK;
+  GF_CUDA(cudaMemsetAsync(g->node_valid + node, 0, 1, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+  g->any_deleted = 1;
+  if (h_out_deleted) *h_out_deleted = 1;
+  return GF_OK;
+}
+
+gf_status gf_graph_get_info(gf_graph* g, gf_graph_info* out) {
+  if (!g || !out) return fail(GF_EINVAL, "NULL argument");
+  out->num_nodes = g->num_nodes;
+  out->num_block_handles = g->blk_used;
+  out->live_blocks = g->blk_used;
+  out->slots_allocated = g->slots_used;
+  out->next_edge_id = g->next_edge_id;
+  out->total_edges_inserted = g->total_edges_inserted;
+  out->any_deleted = g->any_deleted;
+  out->directed = g->directed;
+  out->tau = g->tau;
+  out->sizing_kind = g->sizing_kind;
+  out->sizing_param = g->sizing_param;
+  out->device_bytes = g->node_cap * (8 * 7 + 1) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * 3 +
+                      g->slot_cap * (int64_t)sizeof(Slot);
+  return GF_OK;
+}
+
+gf_status gf_graph_export_nodes(gf_graph* g, int64_t* h_head, int64_t* h_tail, int64_t* h_num_blocks, int64_t* h_degree,
+                                uint8_t* h_node_valid, void* stream) {
+  if (!g) return fail(GF_EINVAL, "graph is NULL");
+  DeviceGuard dg(g->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t n = (size_t)g->num_nodes;
+  if (n) {
+    if (h_head) GF_CUDA(cudaMemcpyAsync(h_head, g->head, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_tail) GF_CUDA(cudaMemcpyAsync(h_tail, g->tail, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_num_blocks) GF_CUDA(cudaMemcpyAsync(h_num_blocks, g->num_blocks, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_degree) GF_CUDA(cudaMemcpyAsync(h_degree, g->degree, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_node_valid) GF_CUDA(cudaMemcpyAsync(h_node_valid, g->node_valid, n, cudaMemcpyDeviceToHost, s));
+  }
+  GF_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
+}
+
+gf_status gf_graph_export_blocks(gf_graph* g, int64_t* h_capacity, int64_t* h_size, int64_t* h_tmin, int64_t* h_tmax,
+                                 int64_t* h_prev, int64_t* h_next, void* stream) {
+  if (!g) return fail(GF_EINVAL, "graph is NULL");
+  DeviceGuard dg(g->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t n = (size_t)g->blk_used;
+  if (n) {
+    if (h_capacity) GF_CUDA(cudaMemcpyAsync(h_capacity, g->bcap, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_size) GF_CUDA(cudaMemcpyAsync(h_size, g->bsize, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_tmin) GF_CUDA(cudaMemcpyAsync(h_tmin, g->btmin, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_tmax) GF_CUDA(cudaMemcpyAsync(h_tmax, g->btmax, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_prev) GF_CUDA(cudaMemcpyAsync(h_prev, g->bprev, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (h_next) GF_CUDA(cudaMemcpyAsync(h_next, g->bnext, 8 * n, cudaMemcpyDeviceToHost, s));
+  }
+  GF_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
+}
+
+gf_status gf_graph_export_slots(gf_graph* g, int64_t h0, int64_t h1, int64_t* h_offsets, int64_t* h_nbr, int64_t* h_eid,
+                                int64_t* h_ts, uint8_t* h_valid, void* stream) {
+  if (!g || !h_offsets) return fail(GF_EINVAL, "NULL argument");
+  if (h0 < 0 || h1 < h0 || h1 > g->blk_used) return fail(GF_EINVAL, "bad handle range");
+  DeviceGuard dg(g->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nb = h1 - h0;
+  std::vector<int64_t> sz(nb);
+  if (nb) GF_CUDA(cudaMemcpyAsync(sz.data(), g->bsize + h0, 8 * nb, cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+  h_offsets[0] = 0;
+  for (int64_t i = 0; i < nb; i++) h_offsets[i + 1] = h_offsets[i] + sz[i];
+  int64_t tot = h_offsets[nb];
+  if (tot == 0) return GF_OK;
+  Scratch sb(s);
+  Arena A;
+  GF_TRY(sb.alloc((size_t)(nb + 1) * 8 + (size_t)tot * 25 + 4096));
+  A.base = sb.as<char>();
+  int64_t* d_off = A.take<int64_t>(nb + 1);
+  int64_t* d_nbr = A.take<int64_t>(tot);
+  int64_t* d_eid = A.take<int64_t>(tot);
+  int64_t* d_ts = A.take<int64_t>(tot);
+  uint8_t* d_valid = A.take<uint8_t>(tot);
+  GF_CUDA(cudaMemcpyAsync(d_off, h_offsets, 8 * (nb + 1), cudaMemcpyHostToDevice, s));
+  GF_LAUNCH(k_gather_slots, (int)std::min<int64_t>(nb, 65535), 256, 0, s, g->slots, g->bbase, d_off, h0, nb, d_nbr, d_eid,
+            d_ts, d_valid);
+  if (h_nbr) GF_CUDA(cudaMemcpyAsync(h_nbr, d_nbr, 8 * tot, cudaMemcpyDeviceToHost, s));
+  if (h_eid) GF_CUDA(cudaMemcpyAsync(h_eid, d_eid, 8 * tot, cudaMemcpyDeviceToHost, s));
+  if (h_ts) GF_CUDA(cudaMemcpyAsync(h_ts, d_ts, 8 * tot, cudaMemcpyDeviceToHost, s));
+  if (h_valid) GF_CUDA(cudaMemcpyAsync(h_valid, d_valid, tot, cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
+}
+
+}  // extern "C"

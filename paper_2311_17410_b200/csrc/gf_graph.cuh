@@ -1,0 +1,65 @@
+// gf_graph.cuh -- device-resident block store (reference storage.py DynamicGraph).
+//
+// HBM layout:
+//   node table  (SoA, indexed by node id)      head, tail, num_blocks, degree (int64), node_valid (u8),
+//                                              nslots (list end position), dir_off / dir_cap (block directory)
+//   block arena (SoA, indexed by block handle) capacity, size, tmin, tmax, prev, next (int64, FastTier
+//                                              columns storage.py:147-152) + base (slot-pool offset)
+//   block directory (per node, contiguous)     tmin, cum (list position of first slot), base -- one entry
+//                                              per block, head..tail, so the sampler can binary-search
+//                                              blocks instead of chasing prev pointers
+//   slot pool  (AoS, 32 B per slot)            Slot{ts, eid, nbr, owner, valid}; block h owns
+//                                              [base[h], base[h] + capacity[h])
+#pragma once
+
+#include "gf_common.cuh"
+
+struct gf_graph {
+  int device = 0;
+  int directed = 0;
+  int64_t tau = 48;
+  int sizing_kind = GF_SIZING_ADAPTIVE;
+  int64_t sizing_param = 0;
+
+  int64_t num_nodes = 0, node_cap = 0;
+  int64_t blk_used = 0, blk_cap = 0;
+  int64_t slots_used = 0, slot_cap = 0;
+  int64_t dir_used = 0, dir_cap_total = 0;
+  int64_t next_edge_id = 0, total_edges_inserted = 0;
+  int any_deleted = 0;
+
+  // node table
+  int64_t *head = nullptr, *tail = nullptr, *num_blocks = nullptr, *degree = nullptr;
+  uint8_t* node_valid = nullptr;
+  int64_t *nslots = nullptr, *dir_off = nullptr, *dir_cap = nullptr;
+  // block arena
+  int64_t *bcap = nullptr, *bsize = nullptr, *btmin = nullptr, *btmax = nullptr, *bprev = nullptr,
+          *bnext = nullptr, *bbase = nullptr;
+  // block directory pool
+  int64_t *dtmin = nullptr, *dcum = nullptr, *dbase = nullptr;
+  // slot pool
+  gf::Slot* slots = nullptr;
+};
+
+namespace gf {
+
+// read-only view passed to sampling kernels
+struct GraphView {
+  const uint8_t* node_valid;
+  const int64_t* num_blocks;
+  const int64_t* nslots;
+  const int64_t* dir_off;
+  const int64_t* dtmin;
+  const int64_t* dcum;
+  const int64_t* dbase;
+  const Slot* slots;
+  int64_t num_nodes;
+  int any_deleted;
+};
+
+inline GraphView view_of(const gf_graph* g) {
+  return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off, g->dtmin,
+                   g->dcum,       g->dbase,      g->slots,  g->num_nodes, g->any_deleted};
+}
+
+}  // namespace gf
