@@ -62,6 +62,11 @@ const char* gf_last_error(void);
 const char* gf_version(void);
 /* number of kernels this process has launched through the library */
 uint64_t gf_launch_count(void);
+/* Per-kernel CUDA-event timing of every library launch (off by default;
+ * enabling clears previous records).  gf_profile_summary writes one line per
+ * kernel: "name<TAB>launches<TAB>total_ms" (synchronises the device). */
+void gf_profile_enable(int on);
+gf_status gf_profile_summary(char* buf, int64_t len);
 
 /* ---- hop seeds -------------------------------------------------------- */
 /* sampling.py:135-137 hop_seed(seed, hop) = SeedSequence([seed, hop]).generate_state(1, u64)[0] */

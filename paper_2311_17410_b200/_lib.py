@@ -40,6 +40,8 @@ _SIGS = {
     "gf_last_error": (ctypes.c_char_p, []),
     "gf_version": (ctypes.c_char_p, []),
     "gf_launch_count": (c_u64, []),
+    "gf_profile_enable": (None, [c_int]),
+    "gf_profile_summary": (c_int, [ctypes.c_char_p, c_i64]),
     "gf_hop_seed": (c_u64, [c_u64, c_u64]),
     "gf_child_key": (c_u64, [c_u64, c_u64]),
     "gf_graph_create": (c_int, [c_int, c_i64, c_int, c_i64, c_int, ctypes.POINTER(c_vp)]),
@@ -137,3 +139,18 @@ def stream_ptr(stream=None) -> int:
 
 def launch_count() -> int:
     return int(load().gf_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    load().gf_profile_enable(1 if on else 0)
+
+
+def profile_summary() -> dict[str, tuple[int, float]]:
+    """{kernel name: (launches, total ms)} from CUDA events around every library launch."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(load().gf_profile_summary(buf, len(buf)))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split("\t")
+        out[name] = (int(cnt), float(ms))
+    return out

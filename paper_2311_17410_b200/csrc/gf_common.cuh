@@ -35,14 +35,23 @@ uint64_t seed_sequence_2(uint64_t a, uint64_t b);
     if (_s != GF_OK) return _s;   \
   } while (0)
 
-// launch + count + check
-#define GF_LAUNCH(kernel, grid, block, smem, stream, ...)                  \
-  do {                                                                     \
-    if ((grid) > 0) {                                                      \
-      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);          \
-      ::gf::g_launches.fetch_add(1, std::memory_order_relaxed);            \
-      GF_CUDA(cudaGetLastError());                                         \
-    }                                                                      \
+// optional per-launch CUDA-event profiling (gf_profile_enable)
+extern std::atomic<int> g_profile;
+cudaEvent_t prof_start(cudaStream_t s);
+void prof_stop(const char* name, cudaStream_t s, cudaEvent_t e0);
+
+// launch + count + (optional) profile + check
+#define GF_LAUNCH(kernel, grid, block, smem, stream, ...)                        \
+  do {                                                                           \
+    if ((grid) > 0) {                                                            \
+      cudaEvent_t _gf_e0 = nullptr;                                              \
+      if (::gf::g_profile.load(std::memory_order_relaxed))                       \
+        _gf_e0 = ::gf::prof_start(stream);                                       \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                \
+      ::gf::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
+      if (_gf_e0) ::gf::prof_stop(#kernel, stream, _gf_e0);                      \
+      GF_CUDA(cudaGetLastError());                                               \
+    }                                                                            \
   } while (0)
 
 struct DeviceGuard {

@@ -348,7 +348,9 @@ gf_status layer_impl(gf_graph* g, const QueryIn& Q, int64_t* d_offsets, int64_t*
   int64_t* counts = A.take<int64_t>(Q.n);
   GraphView G = view_of(g);
   GF_LAUNCH(k_sample_count, grid_warps(Q.n), THREADS, 0, s, G, Q, S, counts);
+  cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, (int)Q.n, s); }, s));
+  if (e0) prof_stop("cub_scan_offsets", s, e0);
   GF_CUDA(cudaMemcpyAsync(h_total, d_offsets + Q.n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
   if (*h_total > out_cap) return fail(GF_ERANGE, "output buffer too small");
