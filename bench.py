@@ -1,0 +1,497 @@
+"""Benchmark: sampled edges/s (2-hop fanout 10, recent + uniform) and ingest edges/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config gdelt|reddit|wiki]
+
+Workload (BASELINE.json metric, configs[3] at N GPUs; fits one B200):
+GDELT-shaped synthetic stream -- 17,000 nodes, 191,000,000 directed edges,
+tau 8192, power-law destinations and sources (skew 2.2), 175,200 time ticks
+ -- drawn on the GPU with the reference generator's law
+(paper_2311_17410_b200/synth.py), ingested in 100K-edge batches
+through gf_graph_add_edges.  One step = sample_khop over R = 2^20 roots per
+GPU (the last edges' src+dst at their own timestamps, harness.py:542-545)
+with fanouts [10, 10], once with the recent and once with the uniform policy.
+value = sampled edges (all hops, both policies, all ranks) / max-over-ranks
+device time.  Multi-GPU: every rank holds a full replica (each new batch is
+assembled with an NCCL all-gather of per-rank shards) and samples its own
+2^20 roots with key base rank*2^20 (weak scaling, no data-path collective).
+
+--impl reference times the reference algorithm on the host: the CPU oracle's
+faithful restatement of sample_khop (oracle/gf_oracle.c, all host threads)
+on a bounded root sample of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: nodes, edges, directed, tau, skew, src_skew, span, roots per GPU
+    "gdelt": dict(nodes=17_000, edges=191_000_000, directed=True, tau=8192, skew=2.2, src_skew=2.2, span=175_200,
+                  roots=1 << 20, label="GDELT-shaped TGN 2-hop f10 (17K nodes, 191M edges, directed, tau 8192)"),
+    "reddit": dict(nodes=11_000, edges=672_000, directed=False, tau=48, skew=2.2, src_skew=None, span=2_592_000,
+                   roots=1 << 16, label="REDDIT-shaped TGAT 2-hop f10 (11K nodes, 672K edges, undirected, tau 48)"),
+    "wiki": dict(nodes=9_000, edges=157_000, directed=False, tau=48, skew=2.2, src_skew=None, span=2_592_000,
+                 roots=8_000, label="WIKI-shaped (9K nodes, 157K edges, undirected, tau 48)"),
+}
+FANOUTS = [10, 10]
+POLICIES = ("recent", "uniform")
+INGEST_BATCH = 100_000
+# algorithmic bytes per query / per sampled edge
+BYTES_PER_QUERY = 65
+BYTES_PER_EDGE = 50
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = [r for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in rows for n, v in zip(names, r[2:6]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def make_stream(cfg, device):
+    from paper_2311_17410_b200.synth import generate_synthetic_device
+
+    return generate_synthetic_device(cfg["nodes"], cfg["edges"], cfg["skew"], cfg["span"], seed=0,
+                                     src_skew=cfg["src_skew"], device=device)
+
+
+def roots_for_rank(src, dst, ts, R, rank):
+    """Latest R/2 edges for this rank: src+dst at their own timestamps (harness.py:542-545)."""
+    import torch
+
+    half = R // 2
+    e = src.numel()
+    lo, hi = e - (rank + 1) * half, e - rank * half
+    roots = torch.cat([src[lo:hi], dst[lo:hi]]).contiguous()
+    rts = torch.cat([ts[lo:hi], ts[lo:hi]]).contiguous()
+    return roots, rts
+
+
+def build_graph(cfg, src, dst, ts, world, rank, device):
+    """Ingest the stream in 100K-edge batches; N>1: each batch is all-gathered from per-rank shards."""
+    import torch
+
+    import paper_2311_17410_b200 as gf
+
+    g = gf.DynamicGraph(directed=cfg["directed"], tau=cfg["tau"], device=device)
+    n = src.numel()
+    slots = n * (1 if cfg["directed"] else 2)
+    g.reserve(cfg["nodes"], cfg["nodes"] * 16 + slots // max(1, cfg["tau"]) + 1024,
+              slots + min(cfg["nodes"] * cfg["tau"], slots // 2))
+    if world > 1:
+        import torch.distributed as dist
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for lo in range(0, n, INGEST_BATCH):
+        hi = min(n, lo + INGEST_BATCH)
+        if world > 1:
+            b = hi - lo
+            per = (b + world - 1) // world
+            pad = per * world
+            shard = torch.zeros((3, per), dtype=torch.int64, device=device)
+            s_lo, s_hi = lo + rank * per, min(hi, lo + (rank + 1) * per)
+            if s_hi > s_lo:
+                shard[0, : s_hi - s_lo] = src[s_lo:s_hi]
+                shard[1, : s_hi - s_lo] = dst[s_lo:s_hi]
+                shard[2, : s_hi - s_lo] = ts[s_lo:s_hi]
+            full = torch.empty((world, 3, per), dtype=torch.int64, device=device)
+            dist.all_gather_into_tensor(full, shard)
+            batch = full.permute(1, 0, 2).reshape(3, pad)[:, :b]
+            g.add_edges_arrays(batch[0].contiguous(), batch[1].contiguous(), batch[2].contiguous())
+        else:
+            g.add_edges_arrays(src[lo:hi], dst[lo:hi], ts[lo:hi])
+    e1.record()
+    torch.cuda.synchronize()
+    return g, e0.elapsed_time(e1)
+
+
+def run_step(g, roots, rts, R_base):
+    import paper_2311_17410_b200 as gf
+
+    edges = 0
+    queries = 0
+    out = []
+    for pol in POLICIES:
+        s = gf.sample_khop_device(g, roots, rts, FANOUTS, gf.SamplingPolicy(pol), seed=0, root_key_base=R_base)
+        for lay in s.layers:
+            edges += int(lay.neighbors.numel())
+            queries += int(lay.source_nodes.numel())
+        out.append(s)
+    return edges, queries, out
+
+
+def cpu_oracle_graph(cfg, src, dst, ts):
+    """Build the oracle (reference restatement) graph on the host; returns (graph, ingest edges/s)."""
+    from oracle import OracleGraph
+
+    s, d, t = src.cpu().numpy(), dst.cpu().numpy(), ts.cpu().numpy()
+    o = OracleGraph(cfg["directed"], cfg["tau"])
+    t0 = time.perf_counter()
+    for lo in range(0, len(s), INGEST_BATCH):
+        o.add_edges(s[lo:lo + INGEST_BATCH], d[lo:lo + INGEST_BATCH], t[lo:lo + INGEST_BATCH])
+    return o, len(s) / (time.perf_counter() - t0)
+
+
+def cpu_sample_rate(o, roots, rts, faithful: bool, budget_s: float, chunk: int, threads: int):
+    """Time the oracle's sample_khop (recent + uniform) over successive root chunks until budget_s."""
+    edges, used, t_total = 0, 0, 0.0
+    pos = 0
+    while t_total < budget_s and pos < len(roots):
+        r, t = roots[pos:pos + chunk], rts[pos:pos + chunk]
+        t0 = time.perf_counter()
+        for pol in POLICIES:
+            lays = o.sample_khop(r, t, FANOUTS, pol, seed=0, root_key_base=pos, threads=threads, faithful=faithful)
+            edges += sum(len(lay[3]) for lay in lays)
+        t_total += time.perf_counter() - t0
+        used += len(r)
+        pos += chunk
+    return edges / t_total if t_total else 0.0, used, edges, t_total
+
+
+def load_traffic() -> dict:
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
+
+
+def bench_ours(args, cfg, world, rank, local):
+    import torch
+
+    import paper_2311_17410_b200 as gf
+    from paper_2311_17410_b200 import _lib
+
+    device = torch.device("cuda", local)
+    R = cfg["roots"] if args.roots is None else args.roots
+    src, dst, ts = make_stream(cfg, device)
+    torch.cuda.synchronize()
+    g, ingest_ms = build_graph(cfg, src, dst, ts, world, rank, device)
+    roots, rts = roots_for_rank(src, dst, ts, R, rank)
+    key_base = rank * R
+
+    for _ in range(args.warmup):
+        run_step(g, roots, rts, key_base)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches0 = _lib.launch_count()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    edges = queries = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e, q, _ = run_step(g, roots, rts, key_base)
+            edges += e
+            queries += q
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms_local = ev0.elapsed_time(ev1)
+    launches = _lib.launch_count() - launches0
+    ms = max_over_ranks(ms_local, world)
+    total_edges = sum_over_ranks(edges, world)
+    value = total_edges / (ms / 1e3)
+
+    # per-kernel shares (separate profiled pass, same workload)
+    _lib.profile_enable(True)
+    e_p, q_p, _ = run_step(g, roots, rts, key_base)
+    prof = _lib.profile_summary()
+    _lib.profile_enable(False)
+    # algorithmic bytes: count kernel 65 B/query, write kernel 50 B/sampled edge
+    alg = {"k_sample_count": BYTES_PER_QUERY * q_p, "k_sample_write": BYTES_PER_EDGE * e_p}
+    pk = peaks()
+    kernels = {}
+    tot_ms = sum(v[1] for v in prof.values())
+    for name, (cnt, kms) in prof.items():
+        short = name.split("(")[0]
+        kernels[short] = {"launches": cnt, "ms": round(kms, 4), "share": round(kms / tot_ms, 4) if tot_ms else None}
+        if short in alg and kms > 0:
+            kernels[short]["achieved_gbs"] = round(alg[short] / (kms / 1e3) / 1e9, 1)
+    dom = max(((k, v) for k, v in kernels.items() if k in alg), key=lambda kv: kv[1]["ms"])
+    dom_name, dom_v = dom
+    achieved = alg[dom_name] / (dom_v["ms"] / 1e3) / 1e9
+    traffic = load_traffic().get(dom_name)
+    pipe_ms = sum(v[1] for k, v in prof.items() if k.split("(")[0] in ("k_sample_count", "k_sample_write",
+                                                                          "cub_scan_offsets"))
+    pipe_gbs = (BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p) / (pipe_ms / 1e3) / 1e9 if pipe_ms else None
+
+    # e2e through the public API with host (pinned) buffers: H2D roots, sample, D2H every layer
+    e2e = None
+    if not args.no_e2e:
+        roots_h = roots.cpu().pin_memory()
+        rts_h = rts.cpu().pin_memory()
+        _, _, outs = run_step(g, roots, rts, key_base)
+        host_bufs = []
+        bo = 0
+        for s in outs:
+            for lay in s.layers:
+                for t in (lay.offsets, lay.neighbors, lay.edge_ids, lay.timestamps):
+                    host_bufs.append(torch.empty(t.numel() + (1 << 20), dtype=torch.int64).pin_memory())
+        sampler = {p: gf.TemporalSampler(g, FANOUTS, p, seed=0) for p in POLICIES}
+        torch.cuda.synchronize()
+        barrier(world)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_edges = 0
+        a0.record(stream)
+        for _ in range(args.steps):
+            bi = bo = 0
+            k = 0
+            for p in POLICIES:
+                r_d = roots_h.to(device, non_blocking=True)
+                t_d = rts_h.to(device, non_blocking=True)
+                bi += 2 * roots_h.numel() * 8
+                s = sampler[p].sample(r_d, t_d, root_key_base=key_base)
+                for lay in s.layers:
+                    e2e_edges += int(lay.neighbors.numel())
+                    for t in (lay.offsets, lay.neighbors, lay.edge_ids, lay.timestamps):
+                        hb = host_bufs[k]
+                        k += 1
+                        hb[: t.numel()].copy_(t, non_blocking=True)
+                        bo += t.numel() * 8
+        a1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        e2e_ms = max_over_ranks(a0.elapsed_time(a1), world)
+        e2e_total = sum_over_ranks(e2e_edges, world)
+        e2e = {"value": round(e2e_total / (e2e_ms / 1e3), 1), "unit": "sampled edges/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo}
+
+    ingest_eps = cfg["edges"] / (max_over_ranks(ingest_ms, world) / 1e3)
+    info = g.info()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, src, dst, ts, roots, rts, args)
+
+    if rank == 0:
+        line = {
+            "metric": "sampled edges/sec (2-hop fanout 10, recent+uniform) at 1/2/4/8 B200; edges/sec ingest",
+            "value": round(value, 1),
+            "unit": "sampled edges/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "int64",
+            "data": "synthetic (reference generator law, drawn on device; seed 0)",
+            "config": {
+                "workload": cfg["label"],
+                "nodes": cfg["nodes"], "edges": cfg["edges"], "directed": cfg["directed"], "tau": cfg["tau"],
+                "fanouts": FANOUTS, "policies": list(POLICIES), "roots_per_gpu": R,
+                "roots": "latest R/2 edges per rank, src+dst at own ts (harness.py:542-545)",
+                "ingest_batch": INGEST_BATCH,
+                "l2": "no flush: slot pool %.1f GB >> 126 MB L2" % (info.slots_allocated * 32 / 1e9),
+                "parallelism": f"replicas x{world}, root sharding (dp{world})",
+            },
+            "ingest": {"value": round(ingest_eps, 1), "unit": "edges/s",
+                       "note": "100K-edge batches through gf_graph_add_edges, device events; N>1 includes the NCCL all-gather"},
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
+                         "peak_source": pk["source"],
+                         "alg_bytes": f"{BYTES_PER_QUERY} B/query (count), {BYTES_PER_EDGE} B/sampled edge (write)",
+                         "pipeline_gbs": round(pipe_gbs, 1) if pipe_gbs else None,
+                         "pipeline_frac": round(pipe_gbs / pk["hbm_gbs"], 4) if pipe_gbs else None},
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, src, dst, ts, roots, rts, args):
+    threads = os.cpu_count() or 1
+    o, cpu_ingest = cpu_oracle_graph(cfg, src, dst, ts)
+    r, t = roots.cpu().numpy(), rts.cpu().numpy()
+    rate, used, edges, secs = cpu_sample_rate(o, r, t, True, args.cpu_budget, 16, threads)
+    frate, fused, fedges, fsecs = cpu_sample_rate(o, r, t, False, min(5.0, args.cpu_budget), 2048, threads)
+    return {"value": round(rate, 1), "unit": "sampled edges/s", "cores": threads, "kind": "port",
+            "sample": f"faithful C restatement of the reference sample_khop (candidate collection as "
+                      f"sampling.py:145-182) on the same graph: first {used} of the {len(r)} roots, recent+uniform "
+                      f"2-hop f10, {edges} edges in {secs:.1f}s",
+            "ingest_edges_per_s": round(cpu_ingest, 1),
+            "ingest_note": "oracle add_edges, 1 core (the reference add_edges is a serial loop)",
+            "fast_port": {"value": round(frate, 1), "cores": threads,
+                          "sample": f"early-exit C port (same output): {fused} roots, {fedges} edges in {fsecs:.1f}s"}}
+
+
+def bench_reference(args, cfg, world, rank, local):
+    """--impl reference: the reference algorithm (faithful oracle port) on host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import torch
+
+    device = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
+    src, dst, ts = make_stream(cfg, device)
+    R = cfg["roots"] if args.roots is None else args.roots
+    roots, rts = roots_for_rank(src, dst, ts, R, 0)
+    o, cpu_ingest = cpu_oracle_graph(cfg, src, dst, ts)
+    r, t = roots.cpu().numpy(), rts.cpu().numpy()
+    threads = os.cpu_count() or 1
+    chunk = args.ref_chunk
+    pos = 0
+    for _ in range(args.warmup):
+        cpu_sample_rate(o, r[pos:pos + chunk], t[pos:pos + chunk], True, 1e9, chunk, threads)
+        pos += chunk
+    edges, secs = 0, 0.0
+    for _ in range(args.steps):
+        _, _, e, s = cpu_sample_rate(o, r[pos:pos + chunk], t[pos:pos + chunk], True, 1e9, chunk, threads)
+        edges += e
+        secs += s
+        pos += chunk
+    value = edges / secs if secs else 0.0
+    line = {
+        "impl": "reference",
+        "metric": "sampled edges/sec (2-hop fanout 10, recent+uniform) at 1/2/4/8 B200; edges/sec ingest",
+        "value": round(value, 1), "unit": "sampled edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(secs * 1e3 / max(args.steps, 1), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic (same stream as --impl ours)",
+        "config": {"workload": cfg["label"], "fanouts": FANOUTS, "policies": list(POLICIES), "roots_per_step": chunk,
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(value, 1), "unit": "sampled edges/s", "cores": threads, "kind": "port",
+                         "sample": f"{chunk} roots per step of the same root set, faithful restatement of the "
+                                   f"reference sample_khop (oracle/gf_oracle.c)"},
+        "ingest": {"value": round(cpu_ingest, 1), "unit": "edges/s", "note": "oracle add_edges, 1 core"},
+        "e2e": {"value": round(value, 1), "unit": "sampled edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="gdelt")
+    ap.add_argument("--roots", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-chunk", type=int, default=16)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        bench_reference(args, cfg, world, rank, local)
+    else:
+        bench_ours(args, cfg, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -362,6 +362,10 @@ class DynamicGraph:
         return int(b["tmax"][tail]) if b["size"][tail] else TS_MIN
 
     # -- mutation -----------------------------------------------------------------
+    def reserve(self, nodes: int, blocks: int, slots: int) -> None:
+        """Pre-size the device node table, block arena and slot pool (they also grow on demand)."""
+        check(load().gf_graph_reserve(self._h, int(nodes), int(blocks), int(slots), stream_ptr()))
+
     def add_edges_arrays(self, src, dst, ts, edge_ids=None, stream=None):
         """Batch append from arrays or CUDA tensors; returns (eids tensor, n_rejected).
 
