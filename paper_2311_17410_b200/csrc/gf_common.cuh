@@ -54,11 +54,14 @@ void prof_stop(const char* name, cudaStream_t s, cudaEvent_t e0);
     }                                                                            \
   } while (0)
 
+inline void init_device_pool(int dev);
+
 struct DeviceGuard {
   int prev = 0;
   explicit DeviceGuard(int dev) {
     cudaGetDevice(&prev);
     if (prev != dev) cudaSetDevice(dev);
+    init_device_pool(dev);
   }
   ~DeviceGuard() {
     int cur = 0;
@@ -66,6 +69,20 @@ struct DeviceGuard {
     if (cur != prev) cudaSetDevice(prev);
   }
 };
+
+// Keep freed stream-ordered scratch mapped (the default pool would return it to
+// the OS at every synchronise, making each per-call cudaMallocAsync a remap).
+inline void init_device_pool(int dev) {
+  static std::atomic<uint64_t> done{0};
+  uint64_t bit = 1ull << (dev & 63);
+  if (done.load() & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.fetch_or(bit);
+}
 
 inline int num_sms() {
   static int n = 0;

@@ -91,7 +91,7 @@ struct QueryScratch {
 };
 
 // ---- pass A: window search + counts --------------------------------------------
-__global__ void __launch_bounds__(THREADS) k_sample_count(GraphView G, QueryIn Q, QueryScratch S, int64_t* counts) {
+__global__ void __launch_bounds__(THREADS, 4) k_sample_count(GraphView G, QueryIn Q, QueryScratch S, int64_t* counts) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -191,7 +191,7 @@ __device__ __forceinline__ const Slot* slot_at(const GraphView& G, int64_t d0, i
 }
 
 // ---- pass B: selection + CSR write ---------------------------------------------
-__global__ void __launch_bounds__(THREADS) k_sample_write(GraphView G, QueryIn Q, QueryScratch S, LayerOut O) {
+__global__ void __launch_bounds__(THREADS, 4) k_sample_write(GraphView G, QueryIn Q, QueryScratch S, LayerOut O) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
