@@ -44,7 +44,7 @@ gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
 }
 
 __global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tail, int64_t* nb, int64_t* deg,
-                             uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap) {
+                             uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap, uint8_t* nflags) {
   for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi; v += (int64_t)gridDim.x * blockDim.x) {
     head[v] = GF_NO_BLOCK;
     tail[v] = GF_NO_BLOCK;
@@ -54,6 +54,7 @@ __global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tai
     nslots[v] = 0;
     doff[v] = -1;
     dcap[v] = 0;
+    nflags[v] = 0;
   }
 }
 
@@ -207,7 +208,7 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
                        const int64_t* __restrict__ cpos, const int64_t* __restrict__ ce_pend, int64_t E,
                        const IngestCounters* c, const int64_t* tail, const int64_t* bsize, const int64_t* bcap,
                        const int64_t* degree, const int64_t* num_blocks, const int64_t* dir_cap, int kind, int64_t tau,
-                       int64_t param, SegPlan P) {
+                       int64_t param, SegPlan P, const int64_t* nslots, uint8_t* nflags) {
   int64_t nseg = c->num_segs;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     int64_t st = seg_start[s], en = (s + 1 < nseg) ? seg_start[s + 1] : E;
@@ -235,6 +236,9 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
     }
     P.nb_new[s] = blocks;
     P.slots_new[s] = slots;
+    // a block allocated while live degree != slots written (a deletion happened) or by
+    // batch sizing leaves the closed-form position -> block law (SizingLaw)
+    if (blocks > 0 && (kind == GF_SIZING_BATCH || degree[v] != nslots[v])) nflags[v] |= 1;
     int64_t need = num_blocks[v] + blocks;
     int64_t dc = dir_cap[v];
     if (need > dc) {
@@ -387,7 +391,7 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
                                 const int64_t* __restrict__ blkoff, Recs R, const int64_t* tail_before_unused,
                                 const int64_t* __restrict__ bbase, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
                                 const int64_t* __restrict__ ts, const int64_t* __restrict__ eids, int directed,
-                                const int64_t* __restrict__ old_tail, Slot* slots) {
+                                const int64_t* __restrict__ old_tail, Slot* slots, int64_t* sts, int64_t* fts) {
   int64_t nacc_ev = 0;
   {
     int64_t nseg = c->num_segs;
@@ -421,6 +425,8 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
     sl.valid = 1;
     sl.pad = 0;
     slots[pos] = sl;
+    sts[pos] = sl.ts;
+    if ((pos & (FENCE - 1)) == 0) fts[pos / FENCE] = sl.ts;
   }
 }
 
@@ -461,11 +467,12 @@ gf_status ensure_nodes(gf_graph* g, int64_t need, cudaStream_t s) {
     GF_TRY(grow_array(g->nslots, k, nc, s));
     GF_TRY(grow_array(g->dir_off, k, nc, s));
     GF_TRY(grow_array(g->dir_cap, k, nc, s));
+    GF_TRY(grow_array(g->nflags, k, nc, s));
     g->node_cap = nc;
   }
   int64_t cnt = need - g->num_nodes;
   GF_LAUNCH(k_init_nodes, grid_for(cnt, 256, 4096), 256, 0, s, g->num_nodes, need, g->head, g->tail, g->num_blocks,
-            g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap);
+            g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags);
   g->num_nodes = need;
   return GF_OK;
 }
@@ -490,6 +497,8 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
   int64_t nc = std::max<int64_t>(need, std::max<int64_t>(4096, g->slot_cap + g->slot_cap / 2));
   int64_t old = g->slot_cap;
   GF_TRY(grow_array(g->slots, g->slots_used, nc, s));
+  GF_TRY(grow_array(g->sts, g->slots_used, nc, s));
+  GF_TRY(grow_array(g->fts, (g->slots_used + FENCE - 1) / FENCE, nc / FENCE + 1, s));
   // unused capacity slots must read as invalid (delete scans the whole pool)
   GF_CUDA(cudaMemsetAsync(g->slots + old, 0, sizeof(Slot) * (size_t)(nc - old), s));
   g->slot_cap = nc;
@@ -601,7 +610,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
   GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
   GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
-            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P);
+            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots, g->nflags);
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.nb_new, blkoff, (int)(E + 1), s); }, s));
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.slots_new, slotsoff, (int)(E + 1), s); }, s));
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.dir_new, diroff, (int)(E + 1), s); }, s));
@@ -660,7 +669,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
               dir, N, B, D);
     GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
-              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots);
+              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
   }
   g->blk_used += nrec;
   g->slots_used += hc.new_slots;
@@ -720,7 +729,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dtmin, g->dcum, g->dbase,
-                g->slots};
+                g->slots, g->sts, g->fts, g->nflags};
   for (void* p : ps)
     if (p) cudaFree(p);
 }
@@ -771,6 +780,7 @@ gf_status gf_graph_reserve(gf_graph* g, int64_t nodes, int64_t blocks, int64_t s
     GF_TRY(grow_array(g->nslots, k, nc, s));
     GF_TRY(grow_array(g->dir_off, k, nc, s));
     GF_TRY(grow_array(g->dir_cap, k, nc, s));
+    GF_TRY(grow_array(g->nflags, k, nc, s));
     g->node_cap = nc;
   }
   GF_TRY(ensure_blocks(g, blocks, s));
@@ -849,8 +859,8 @@ gf_status gf_graph_get_info(gf_graph* g, gf_graph_info* out) {
   out->tau = g->tau;
   out->sizing_kind = g->sizing_kind;
   out->sizing_param = g->sizing_param;
-  out->device_bytes = g->node_cap * (8 * 7 + 1) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * 3 +
-                      g->slot_cap * (int64_t)sizeof(Slot);
+  out->device_bytes = g->node_cap * (8 * 7 + 2) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * 3 +
+                      g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8;
   return GF_OK;
 }
 

@@ -10,6 +10,10 @@
 //                                              blocks instead of chasing prev pointers
 //   slot pool  (AoS, 32 B per slot)            Slot{ts, eid, nbr, owner, valid}; block h owns
 //                                              [base[h], base[h] + capacity[h])
+//   sts        (int64 per slot)                dense copy of the slot timestamps (window reads)
+//   fts        (int64 per 32 slots)            fence index: fts[i] = ts of pool slot 32*i, a sorted
+//                                              subsequence of every block's timestamps (L2-sized)
+//   nflags     (u8 per node)                   bit 0: block list not on the sizing law's closed form
 #pragma once
 
 #include "gf_common.cuh"
@@ -32,6 +36,7 @@ struct gf_graph {
   int64_t *head = nullptr, *tail = nullptr, *num_blocks = nullptr, *degree = nullptr;
   uint8_t* node_valid = nullptr;
   int64_t *nslots = nullptr, *dir_off = nullptr, *dir_cap = nullptr;
+  uint8_t* nflags = nullptr;
   // block arena
   int64_t *bcap = nullptr, *bsize = nullptr, *btmin = nullptr, *btmax = nullptr, *bprev = nullptr,
           *bnext = nullptr, *bbase = nullptr;
@@ -39,9 +44,34 @@ struct gf_graph {
   int64_t *dtmin = nullptr, *dcum = nullptr, *dbase = nullptr;
   // slot pool
   gf::Slot* slots = nullptr;
+  int64_t* sts = nullptr;
+  int64_t* fts = nullptr;
 };
 
 namespace gf {
+
+constexpr int FENCE = 32;  // pool slots per fence entry
+
+// Closed-form block index of a list position for nodes whose blocks follow
+// the sizing law exactly (no deletion before an allocation, no offload):
+// adaptive caps are min(max(cum_b, 1), tau) (storage.py:88-89, degree ==
+// slots written), so cum_b = 2^(b-1) up to the first b = m with
+// 2^(b-1) >= tau, then grows by tau; fixed caps give cum_b = b * size.
+struct SizingLaw {
+  int kind;
+  int64_t tau, size, m, cum_m;
+};
+
+inline SizingLaw sizing_law(int kind, int64_t tau, int64_t param) {
+  SizingLaw L{kind, tau, param, 0, 0};
+  if (kind == GF_SIZING_ADAPTIVE) {
+    int64_t b = 1;
+    while ((1ll << (b - 1)) < tau) b++;
+    L.m = b;
+    L.cum_m = 1ll << (b - 1);
+  }
+  return L;
+}
 
 // read-only view passed to sampling kernels
 struct GraphView {
@@ -53,13 +83,18 @@ struct GraphView {
   const int64_t* dcum;
   const int64_t* dbase;
   const Slot* slots;
+  const int64_t* sts;
+  const int64_t* fts;
+  const uint8_t* nflags;
   int64_t num_nodes;
   int any_deleted;
+  SizingLaw law;
 };
 
 inline GraphView view_of(const gf_graph* g) {
-  return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off, g->dtmin,
-                   g->dcum,       g->dbase,      g->slots,  g->num_nodes, g->any_deleted};
+  return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off, g->dtmin, g->dcum, g->dbase, g->slots,
+                   g->sts,        g->fts,        g->nflags, g->num_nodes, g->any_deleted,
+                   sizing_law(g->sizing_kind, g->tau, g->sizing_param)};
 }
 
 }  // namespace gf
