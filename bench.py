@@ -306,7 +306,7 @@ def bench_ours(args, cfg, world, rank, local):
     prof = _lib.profile_summary()
     _lib.profile_enable(False)
     # algorithmic bytes: count kernel 65 B/query, write kernel 50 B/sampled edge
-    alg = {"k_sample_hop": BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p}
+    alg = {"k_count_fast": BYTES_PER_QUERY * q_p, "k_write_fast": BYTES_PER_EDGE * e_p}
     pk = peaks()
     kernels = {}
     tot_ms = sum(v[1] for v in prof.values())
@@ -319,7 +319,8 @@ def bench_ours(args, cfg, world, rank, local):
     dom_name, dom_v = dom
     achieved = alg[dom_name] / (dom_v["ms"] / 1e3) / 1e9
     traffic = load_traffic().get(dom_name)
-    pipe_ms = sum(v[1] for k, v in prof.items() if k.split("(")[0] in ("k_sample_hop", "k_zero_total"))
+    pipe_ms = sum(v[1] for k, v in prof.items() if k.split("(")[0] in ("k_count_fast", "k_write_fast", "k_total",
+                                                                          "cub_scan_offsets"))
     pipe_gbs = (BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p) / (pipe_ms / 1e3) / 1e9 if pipe_ms else None
 
     # e2e through the public API with host (pinned) buffers: H2D roots, sample, D2H every layer
@@ -397,7 +398,7 @@ def bench_ours(args, cfg, world, rank, local):
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
                          "peak_source": pk["source"],
-                         "alg_bytes": f"{BYTES_PER_QUERY} B/query + {BYTES_PER_EDGE} B/sampled edge (SURVEY.md 8(d))",
+                         "alg_bytes": f"count kernel {BYTES_PER_QUERY} B/query, write kernel {BYTES_PER_EDGE} B/sampled edge (SURVEY.md 8(d))",
                          "pipeline_gbs": round(pipe_gbs, 1) if pipe_gbs else None,
                          "pipeline_frac": round(pipe_gbs / pk["hbm_gbs"], 4) if pipe_gbs else None},
             "kernels": kernels,

@@ -44,7 +44,8 @@ gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
 }
 
 __global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tail, int64_t* nb, int64_t* deg,
-                             uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap, uint8_t* nflags) {
+                             uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap, uint8_t* nflags,
+                             int64_t* nrec) {
   for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi; v += (int64_t)gridDim.x * blockDim.x) {
     head[v] = GF_NO_BLOCK;
     tail[v] = GF_NO_BLOCK;
@@ -55,6 +56,11 @@ __global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tai
     doff[v] = -1;
     dcap[v] = 0;
     nflags[v] = 0;
+    int64_t* r = nrec + v * NREC;
+    r[0] = -1;
+    r[1] = 0;
+    r[2] = NREC_VALID;
+    r[3] = r[4] = r[5] = r[6] = r[7] = 0;
   }
 }
 
@@ -336,6 +342,9 @@ __global__ void k_write_blocks(const uint32_t* __restrict__ perm, int64_t nrec, 
 
 struct NodeArrays {
   int64_t *head, *tail, *num_blocks, *degree, *nslots, *dir_off, *dir_cap;
+  const uint8_t* valid;
+  const uint8_t* nflags;
+  int64_t* nrec;
 };
 struct DirArrays {
   int64_t *tmin, *cum, *base;
@@ -383,8 +392,19 @@ __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__
     N.num_blocks[v] = nb_old + nb;
     N.degree[v] += cnt;
     N.nslots[v] = ns_old + cnt;
+    int64_t tl = N.tail[v], doff = N.dir_off[v], nbt = nb_old + nb;
+    int64_t* r = N.nrec + v * NREC;
+    r[0] = doff;
+    r[1] = ns_old + cnt;
+    r[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
+    r[3] = D.cum[doff];
+    r[4] = D.cum[doff + nbt - 1];
+    r[5] = B.base[tl];
+    r[6] = B.tmin[tl];
   }
 }
+
+__global__ void k_noderec_invalidate(int64_t* nrec, int64_t v) { nrec[v * NREC + 2] &= ~NREC_VALID; }
 
 __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restrict__ ce_seg, const uint32_t* __restrict__ ce_ev,
                                 const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start, SegPlan P,
@@ -468,11 +488,12 @@ gf_status ensure_nodes(gf_graph* g, int64_t need, cudaStream_t s) {
     GF_TRY(grow_array(g->dir_off, k, nc, s));
     GF_TRY(grow_array(g->dir_cap, k, nc, s));
     GF_TRY(grow_array(g->nflags, k, nc, s));
+    GF_TRY(grow_array(g->nrec, k * NREC, nc * NREC, s));
     g->node_cap = nc;
   }
   int64_t cnt = need - g->num_nodes;
   GF_LAUNCH(k_init_nodes, grid_for(cnt, 256, 4096), 256, 0, s, g->num_nodes, need, g->head, g->tail, g->num_blocks,
-            g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags);
+            g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
   g->num_nodes = need;
   return GF_OK;
 }
@@ -664,7 +685,8 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   }
   if (hc.n_acc > 0) {
     BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
-    NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap};
+    NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid, g->nflags,
+                 g->nrec};
     DirArrays D{g->dtmin, g->dcum, g->dbase};
     GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
               dir, N, B, D);
@@ -729,7 +751,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dtmin, g->dcum, g->dbase,
-                g->slots, g->sts, g->fts, g->nflags};
+                g->slots, g->sts, g->fts, g->nflags, g->nrec};
   for (void* p : ps)
     if (p) cudaFree(p);
 }
@@ -781,6 +803,7 @@ gf_status gf_graph_reserve(gf_graph* g, int64_t nodes, int64_t blocks, int64_t s
     GF_TRY(grow_array(g->dir_off, k, nc, s));
     GF_TRY(grow_array(g->dir_cap, k, nc, s));
     GF_TRY(grow_array(g->nflags, k, nc, s));
+    GF_TRY(grow_array(g->nrec, k * NREC, nc * NREC, s));
     g->node_cap = nc;
   }
   GF_TRY(ensure_blocks(g, blocks, s));
@@ -840,6 +863,7 @@ gf_status gf_graph_delete_node(gf_graph* g, int64_t node, int* h_out_deleted, vo
   GF_CUDA(cudaStreamSynchronize(s));
   if (!v) return GF_OK;
   GF_CUDA(cudaMemsetAsync(g->node_valid + node, 0, 1, s));
+  GF_LAUNCH(k_noderec_invalidate, 1, 1, 0, s, g->nrec, node);
   GF_CUDA(cudaStreamSynchronize(s));
   g->any_deleted = 1;
   if (h_out_deleted) *h_out_deleted = 1;

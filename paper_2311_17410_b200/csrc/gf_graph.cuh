@@ -37,6 +37,7 @@ struct gf_graph {
   uint8_t* node_valid = nullptr;
   int64_t *nslots = nullptr, *dir_off = nullptr, *dir_cap = nullptr;
   uint8_t* nflags = nullptr;
+  int64_t* nrec = nullptr;  // packed 64-byte sampler record per node (NodeRec)
   // block arena
   int64_t *bcap = nullptr, *bsize = nullptr, *btmin = nullptr, *btmax = nullptr, *bprev = nullptr,
           *bnext = nullptr, *bbase = nullptr;
@@ -51,6 +52,14 @@ struct gf_graph {
 namespace gf {
 
 constexpr int FENCE = 32;  // pool slots per fence entry
+
+// NodeRec: one 64-byte line per node, everything a sampler query needs first
+// (one coalesced load by 8 lanes): word 0 dir_off, 1 nslots (list end),
+// 2 num_blocks | valid << 32 | irregular << 33, 3 first live list position,
+// 4 tail block cum, 5 tail block slot base, 6 tail block tmin, 7 reserved.
+constexpr int NREC = 8;
+constexpr int64_t NREC_VALID = 1ll << 32;
+constexpr int64_t NREC_IRREG = 1ll << 33;
 
 // Closed-form block index of a list position for nodes whose blocks follow
 // the sizing law exactly (no deletion before an allocation, no offload):
@@ -86,6 +95,7 @@ struct GraphView {
   const int64_t* sts;
   const int64_t* fts;
   const uint8_t* nflags;
+  const int64_t* nrec;
   int64_t num_nodes;
   int any_deleted;
   SizingLaw law;
@@ -93,7 +103,7 @@ struct GraphView {
 
 inline GraphView view_of(const gf_graph* g) {
   return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off, g->dtmin, g->dcum, g->dbase, g->slots,
-                   g->sts,        g->fts,        g->nflags, g->num_nodes, g->any_deleted,
+                   g->sts,        g->fts,        g->nflags, g->nrec,      g->num_nodes, g->any_deleted,
                    sizing_law(g->sizing_kind, g->tau, g->sizing_param)};
 }
 

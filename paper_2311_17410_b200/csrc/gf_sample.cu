@@ -1,26 +1,33 @@
-// gf_sample.cu -- temporal k-hop sampler (K2 + K3), one fused kernel per hop.
+// gf_sample.cu -- temporal k-hop sampler (K2 window search + selection, K3 CSR output).
 //
 // Replaces sample_layer / _sample_one / _collect_candidates / _select and the
 // sample_khop hop loop (reference sampling.py:145-299).
 //
-// One warp per (source, window) query.  Timestamps never decrease along a
-// node's block list (storage.py:426-437 rejects out-of-order edges), so the
-// in-window candidates of a query are one contiguous run [lo, hi) of list
-// positions.  The warp finds hi (and lo when t_start > TS_MIN) with 32-ary
-// ballot searches that probe the newest entries first: over the node's block
-// directory (block tmin), then over the fence index of the boundary block,
-// then one 32-timestamp window of the dense ts array.  This replaces the
-// reference's tail->head block walk with block skipping (sampling.py:157-172).
+// Timestamps never decrease along a node's block list (storage.py:426-437
+// rejects out-of-order edges), so the in-window candidates of a query are one
+// contiguous run [lo, hi) of list positions.  Finding hi replaces the
+// reference's tail->head block walk with block skipping (sampling.py:157-172):
+//   1. the node's 64-byte NodeRec (one load) -- if the tail block's tmin is
+//      below t_end the boundary is in the tail block (the common case for
+//      recent roots), else a 32-ary search over the node's block directory;
+//   2. a 32-ary search over the block's fence index (every 32nd timestamp,
+//      L2-resident), newest fences probed first;
+//   3. one 32-timestamp window of the dense ts array.
+// Selection:
 //   recent:     the k newest valid candidates, newest first (sampling.py:188-190) -- bit-exact.
 //   uniform/tw: k distinct candidates by Floyd's algorithm on a Philox4x32-10 stream
-//               keyed by (hop seed, query key); statistically checked against the reference.
-// CSR output (K3) is produced in the same kernel: each CTA claims a tile of
-// queries in order, counts its samples, and obtains its output offset with a
-// decoupled look-back over the preceding tiles' published counts; it then
-// writes its samples.  Hop totals stay on the device, so a whole sample_khop
-// is a fixed sequence of launches with one host synchronisation at the end.
+//               keyed by (hop seed, query key); positions map to slots by the
+//               sizing law's closed form (or the directory for irregular lists).
+// Output (K3): a count pass, a device scan, and a write pass; hop totals stay
+// on the device so a k-hop call is a fixed launch sequence with one host
+// synchronisation at the end.
+//
+// Fast path (no deletions ever applied): 8-lane groups, 4 queries in flight
+// per warp; each lane issues 4 independent loads per search step, so a group
+// still performs 32-ary searches.  General path (after deletions): one warp
+// per query, scanning candidate validity (valid edge and valid neighbour,
+// sampling.py:178).
 #include <cub/cub.cuh>
-#include <cuda/atomic>
 
 #include <algorithm>
 #include <vector>
@@ -31,76 +38,51 @@ using namespace gf;
 
 namespace {
 
-constexpr int WARPS = 8;
-constexpr int THREADS = WARPS * 32;
-constexpr int QW = 4;              // queries per warp per tile
-constexpr int TQ = WARPS * QW;     // queries per tile (== 32: one per lane of the scanning warp)
-static_assert(TQ == 32, "tile scan assumes 32 queries per tile");
+constexpr int THREADS = 256;
+constexpr int G = 8;   // lanes per query group (fast path)
+constexpr int V = 4;   // loads per lane per search step: G * V = 32-ary search
 
-constexpr unsigned long long FLAG_A = 1ull << 62;  // tile aggregate published
-constexpr unsigned long long FLAG_P = 2ull << 62;  // tile inclusive prefix published
-constexpr unsigned long long VAL_MASK = (1ull << 62) - 1;
-
-__device__ __forceinline__ bool node_ok(const GraphView& G, int64_t v) {
-  return v >= 0 && v < G.num_nodes && G.node_valid[v];
-}
-
-// number of timestamps < x in the block whose slots are sts[base, base + size)
-__device__ __forceinline__ int64_t block_lower_bound(const GraphView& G, int64_t base, int64_t size, int64_t x) {
-  const int lane = lane_id();
-  int64_t seg_lo, seg_hi;
-  int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;  // fences inside the block
-  if (size <= FENCE || f0 > f1) {
-    seg_lo = base;
-    seg_hi = base + size;
-  } else {
-    int64_t j = warp_lower_bound(G.fts + f0, 1, f1 - f0 + 1, x);  // fences < x
-    if (j == 0) {
-      seg_lo = base;
-      seg_hi = f0 * FENCE;
-    } else {
-      seg_lo = (f0 + j - 1) * FENCE;
-      seg_hi = min(seg_lo + FENCE, base + size);
-    }
-  }
-  // seg length <= 2 * FENCE - 1 only when size <= FENCE... otherwise <= FENCE
-  int64_t cnt = 0;
-  for (int64_t p0 = seg_lo; p0 < seg_hi; p0 += 32) {
-    int64_t p = p0 + lane;
-    bool lt = p < seg_hi && __ldg(G.sts + p) < x;
-    unsigned m = __ballot_sync(0xffffffffu, lt);
-    cnt += __popc(m);
-    if (m != 0xffffffffu) break;
-  }
-  return seg_lo - base + cnt;
-}
-
-struct Bound {
-  int64_t pos;  // list position (count of slots with ts < x)
-  int64_t blk;  // directory index of the block holding pos - 1 (or -1)
+struct QueryIn {
+  const int64_t* src;
+  const int64_t* t_start;  // NULL => TS_MIN
+  const int64_t* t_end;
+  const uint64_t* keys;    // NULL => key_base + q
+  uint64_t key_base;
+  int64_t n;               // query count when n_dev == NULL
+  const int64_t* n_dev;    // device-resident query count (previous hop's total)
+  int64_t fanout;
+  int policy;
+  int64_t delta;
+  uint64_t seed;
 };
 
-// list position of the first slot with ts >= x, and the block holding the slot before it
-__device__ __forceinline__ Bound list_lower_bound(const GraphView& G, int64_t d0, int64_t nb, int64_t ns_end, int64_t x) {
-  int64_t B = warp_lower_bound(G.dtmin + d0, 1, nb, x);  // blocks with tmin < x
-  if (B == 0) return Bound{__ldg(G.dcum + d0), -1};
-  int64_t b = B - 1;
-  int64_t cum = __ldg(G.dcum + d0 + b);
-  int64_t size = (b == nb - 1) ? (ns_end - cum) : (__ldg(G.dcum + d0 + b + 1) - cum);
-  int64_t in = block_lower_bound(G, __ldg(G.dbase + d0 + b), size, x);
-  // in >= 1 because tmin_b < x; the slot before the boundary is in block b
-  return Bound{cum + in, b};
-}
+// per-query state between the count and write passes
+struct QState {
+  int64_t* lo;
+  int64_t* hi;
+  int64_t* slot;  // pool index of the slot at list position hi - 1
+  int64_t* cum;   // list position of the first slot of that block
+  int64_t* d0;    // directory offset
+  int64_t* meta;  // block index of hi-1 (low 32) | num_blocks << 32 | irregular << 63
+  int64_t* nv;    // candidates the selection runs over
+};
 
-// directory index of the block holding list position p
-__device__ __forceinline__ int64_t block_of(const GraphView& G, bool regular, int64_t d0, int64_t nb, int64_t p) {
-  if (regular) {
-    const SizingLaw& L = G.law;
-    if (L.kind == GF_SIZING_FIXED) return p / L.size;
-    if (p >= L.cum_m) return L.m + (p - L.cum_m) / L.tau;
-    return p == 0 ? 0 : 64 - __clzll(p);
-  }
-  return upper_bound_seq(G.dcum + d0, nb, p) - 1;
+struct LayerOut {
+  const int64_t* offsets;
+  int64_t* nbr;
+  int64_t* eid;
+  int64_t* ts;
+  uint64_t* keys;  // optional child keys
+  int64_t cap;
+  int* overflow;
+};
+
+__device__ __forceinline__ int64_t query_count(const QueryIn& Q) { return Q.n_dev ? *Q.n_dev : Q.n; }
+
+__device__ __forceinline__ int64_t t_start_of(const QueryIn& Q, int64_t q, int64_t te) {
+  int64_t tsr = Q.t_start ? Q.t_start[q] : GF_TS_MIN;
+  if (Q.policy == GF_POLICY_TIME_WINDOW) tsr = (te < GF_TS_MIN + Q.delta) ? GF_TS_MIN : te - Q.delta;  // sampling.py:202-203
+  return tsr;
 }
 
 __device__ __forceinline__ Slot load_slot(const Slot* p) {
@@ -116,337 +98,494 @@ __device__ __forceinline__ Slot load_slot(const Slot* p) {
   return s;
 }
 
-__device__ __forceinline__ bool slot_ok(const GraphView& G, const Slot& s) {
-  return s.valid && G.node_valid[s.nbr];
+__device__ __forceinline__ void store_out(const LayerOut& O, int64_t at, const Slot& s, uint64_t qkey, int64_t i) {
+  if (at >= O.cap) {
+    *O.overflow = 1;
+    return;
+  }
+  __stcs((long long*)O.nbr + at, (long long)s.nbr);
+  __stcs((long long*)O.eid + at, (long long)s.eid);
+  __stcs((long long*)O.ts + at, (long long)s.ts);
+  if (O.keys) __stcs((long long*)O.keys + at, (long long)child_key(qkey, (uint64_t)i));
 }
+
+// closed-form block index of a list position for regular lists (SizingLaw)
+__device__ __forceinline__ int64_t law_block(const SizingLaw& L, int64_t p) {
+  if (L.kind == GF_SIZING_FIXED) return p / L.size;
+  if (p >= L.cum_m) return L.m + (p - L.cum_m) / L.tau;
+  return p == 0 ? 0 : 64 - __clzll(p);
+}
+
+// ============================ group-of-8 fast path ===========================
+
+struct Grp {
+  int gl;          // lane within the group
+  int gbase;       // first lane of the group
+  unsigned mask;   // group lanes
+};
+
+__device__ __forceinline__ Grp make_grp() {
+  int lane = threadIdx.x & 31;
+  Grp g;
+  g.gl = lane & (G - 1);
+  g.gbase = lane & ~(G - 1);
+  g.mask = ((1u << G) - 1) << g.gbase;
+  return g;
+}
+
+__device__ __forceinline__ int gcount(const Grp& g, bool p) {
+  return __popc(__ballot_sync(g.mask, p) & g.mask);
+}
+
+template <class T>
+__device__ __forceinline__ T gbcast(const Grp& g, T v, int src) {
+  return __shfl_sync(g.mask, v, g.gbase + src);
+}
+
+// number of elements < x in the sorted a[0], a[stride], ..., a[(n-1)*stride];
+// 32 probes per step (V loads per lane), the newest 32 first
+__device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __restrict__ a, int64_t stride, int64_t n,
+                                                 int64_t x) {
+  int64_t lo = 0, hi = n;
+  if (n > 32) {
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (n - 32 + g.gl * V + j) * stride) < x);
+    if (c > 0) return n - 32 + c;
+    hi = n - 32;
+  }
+  while (hi - lo > 32) {
+    int64_t step = (hi - lo + 31) / 32;
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < V; j++) {
+      int64_t p = lo + (int64_t)(g.gl * V + j) * step;
+      c += gcount(g, p < hi && __ldg(a + p * stride) < x);
+    }
+    if (c == 0) return lo;
+    int64_t plast = lo + (int64_t)(c - 1) * step;
+    int64_t nh = plast + step;
+    lo = plast + 1;
+    if (nh < hi) hi = nh;
+  }
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < V; j++) {
+    int64_t p = lo + g.gl * V + j;
+    c += gcount(g, p < hi && __ldg(a + p * stride) < x);
+  }
+  return lo + c;
+}
+
+// timestamps < x inside the block whose slots are sts[base, base + size)
+__device__ __forceinline__ int64_t g_block_lower_bound(const Grp& g, const GraphView& GV, int64_t base, int64_t size,
+                                                       int64_t x) {
+  int64_t seg_lo = base, seg_hi = base + size;
+  if (size > FENCE) {
+    int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;
+    int64_t j = g_lower_bound(g, GV.fts + f0, 1, f1 - f0 + 1, x);
+    if (j == 0) {
+      seg_hi = f0 * FENCE;
+    } else {
+      seg_lo = (f0 + j - 1) * FENCE;
+      seg_hi = min(seg_lo + FENCE, base + size);
+    }
+  }
+  int c = 0;  // window of <= 32 timestamps
+#pragma unroll
+  for (int j = 0; j < V; j++) {
+    int64_t p = seg_lo + g.gl * V + j;
+    c += gcount(g, p < seg_hi && __ldg(GV.sts + p) < x);
+  }
+  return seg_lo - base + c;
+}
+
+struct NodeView {
+  int64_t d0, ns, nb, first, tcum, tbase, ttmin;
+  bool valid, irregular;
+};
+
+__device__ __forceinline__ NodeView load_node(const Grp& g, const GraphView& GV, int64_t v) {
+  int64_t w = __ldg(GV.nrec + v * NREC + g.gl);
+  NodeView N;
+  N.d0 = gbcast(g, w, 0);
+  N.ns = gbcast(g, w, 1);
+  int64_t w2 = gbcast(g, w, 2);
+  N.first = gbcast(g, w, 3);
+  N.tcum = gbcast(g, w, 4);
+  N.tbase = gbcast(g, w, 5);
+  N.ttmin = gbcast(g, w, 6);
+  N.nb = w2 & 0xffffffffll;
+  N.valid = (w2 & NREC_VALID) != 0;
+  N.irregular = (w2 & NREC_IRREG) != 0;
+  return N;
+}
+
+struct Bnd {
+  int64_t pos, blk, cum, base;  // boundary position; block holding pos-1 with its cum/base
+};
+
+__device__ __forceinline__ Bnd g_list_lower_bound(const Grp& g, const GraphView& GV, const NodeView& N, int64_t x) {
+  int64_t b, cum, base, size;
+  if (N.ttmin < x) {  // boundary inside the tail block
+    b = N.nb - 1;
+    cum = N.tcum;
+    base = N.tbase;
+    size = N.ns - N.tcum;
+  } else {
+    int64_t B = g_lower_bound(g, GV.dtmin + N.d0, 1, N.nb - 1, x);  // non-tail blocks with tmin < x
+    if (B == 0) return Bnd{N.first, -1, 0, 0};
+    b = B - 1;
+    cum = __ldg(GV.dcum + N.d0 + b);
+    size = __ldg(GV.dcum + N.d0 + b + 1) - cum;
+    base = __ldg(GV.dbase + N.d0 + b);
+  }
+  return Bnd{cum + g_block_lower_bound(g, GV, base, size, x), b, cum, base};
+}
+
+__global__ void __launch_bounds__(THREADS) k_count_fast(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
+  const Grp g = make_grp();
+  const int64_t n = query_count(Q);
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t q = gid; q < cap_q; q += ngroups) {
+    if (q >= n) {
+      if (g.gl == 0) counts[q] = 0;
+      continue;
+    }
+    int64_t v = Q.src[q];
+    int64_t te = Q.t_end[q];
+    int64_t lo = 0, hi = 0, k = 0;
+    Bnd h{0, -1, 0, 0};
+    NodeView N{0, 0, 0, 0, 0, 0, 0, false, false};
+    if (v >= 0 && v < GV.num_nodes) N = load_node(g, GV, v);
+    if (N.valid && N.nb > 0) {  // sampling.py:153-155
+      h = g_list_lower_bound(g, GV, N, te);
+      int64_t tsr = t_start_of(Q, q, te);
+      lo = (tsr == GF_TS_MIN) ? N.first : g_list_lower_bound(g, GV, N, tsr).pos;
+      hi = h.pos > lo ? h.pos : lo;
+      k = min(hi - lo, Q.fanout);
+    }
+    if (g.gl == 0) {
+      counts[q] = k;
+      if (k > 0) {
+        S.lo[q] = lo;
+        S.hi[q] = hi;
+        S.slot[q] = h.base + (hi - 1 - h.cum);
+        S.cum[q] = h.cum;
+        S.d0[q] = N.d0;
+        S.meta[q] = (h.blk & 0xffffffffll) | (N.nb << 32) | (N.irregular ? (1ll << 62) : 0);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q, QState S, LayerOut O) {
+  const Grp g = make_grp();
+  const int64_t n = query_count(Q);
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t q = gid; q < n; q += ngroups) {
+    const int64_t out = O.offsets[q];
+    const int64_t k = O.offsets[q + 1] - out;
+    if (k == 0) continue;
+    const int64_t lo = S.lo[q], hi = S.hi[q], nv = hi - lo;
+    const uint64_t qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
+    if (Q.policy == GF_POLICY_RECENT || k == nv) {
+      // newest first: positions hi-1, hi-2, ... (sampling.py:188-190)
+      int64_t slot_hi = S.slot[q], cum = S.cum[q];
+      int64_t inblk = hi - cum;  // candidates inside the block holding hi-1
+      for (int64_t r0 = 0; r0 < k; r0 += G * 2) {
+        Slot s0, s1;
+        int64_t r_a = r0 + g.gl, r_b = r0 + G + g.gl;
+        // both loads in flight before either store
+        bool a_ok = r_a < k, b_ok = r_b < k;
+        if (a_ok && r_a < inblk) s0 = load_slot(GV.slots + slot_hi - r_a);
+        if (b_ok && r_b < inblk) s1 = load_slot(GV.slots + slot_hi - r_b);
+        if ((a_ok && r_a >= inblk) || (b_ok && r_b >= inblk)) {
+          // crosses into earlier blocks (rare): locate by directory
+          int64_t d0 = S.d0[q];
+          int64_t nb = S.meta[q] >> 32 & 0x3fffffff;
+          if (a_ok && r_a >= inblk) {
+            int64_t p = hi - 1 - r_a;
+            int64_t b = upper_bound_seq(GV.dcum + d0, nb, p) - 1;
+            s0 = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b)));
+          }
+          if (b_ok && r_b >= inblk) {
+            int64_t p = hi - 1 - r_b;
+            int64_t b = upper_bound_seq(GV.dcum + d0, nb, p) - 1;
+            s1 = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b)));
+          }
+        }
+        if (a_ok) store_out(O, out + r_a, s0, qkey, r_a);
+        if (b_ok) store_out(O, out + r_b, s1, qkey, r_b);
+      }
+      continue;
+    }
+    // uniform / time_window with k < nv: Floyd's algorithm, draws i = gl*V + j
+    const int64_t meta = S.meta[q], d0 = S.d0[q];
+    const bool irregular = (meta >> 62) & 1;
+    const int64_t nb = meta >> 32 & 0x3fffffff;
+    if (k <= G * V) {
+      int64_t t[V], sel[V];
+#pragma unroll
+      for (int j = 0; j < V; j += 2) {
+        int64_t i = g.gl * V + j;
+        // one Philox call yields draws i and i+1 (i even)
+        uint32_t c[4] = {(uint32_t)(i >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+        philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
+        uint64_t r0 = (uint64_t)c[0] | ((uint64_t)c[1] << 32), r1 = (uint64_t)c[2] | ((uint64_t)c[3] << 32);
+        t[j] = (int64_t)bounded64(r0, (uint64_t)(nv - k + i + 1));
+        t[j + 1] = (int64_t)bounded64(r1, (uint64_t)(nv - k + i + 2));
+        sel[j] = sel[j + 1] = -1;
+      }
+#pragma unroll
+      for (int i = 0; i < G * V; i++) {
+        if (i < k) {
+          int64_t ti = gbcast(g, t[i % V], i / V);
+          bool dup = false;
+#pragma unroll
+          for (int j = 0; j < V; j++) dup |= (g.gl * V + j < i) && sel[j] == ti;
+          dup = gcount(g, dup) > 0;
+          if (g.gl == i / V) sel[i % V] = dup ? (nv - k + i) : ti;
+        }
+      }
+      Slot sl[V];
+      int64_t idx[V];
+#pragma unroll
+      for (int j = 0; j < V; j++) {
+        idx[j] = g.gl * V + j;
+        if (idx[j] < k) {
+          int64_t p = lo + sel[j];
+          int64_t b = irregular ? upper_bound_seq(GV.dcum + d0, nb, p) - 1 : law_block(GV.law, p);
+          sl[j] = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b)));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < V; j++)
+        if (idx[j] < k) store_out(O, out + idx[j], sl[j], qkey, idx[j]);
+      continue;
+    }
+    // large fanout: keep the Floyd set in the output's eid column while drawing
+    if (out + k > O.cap) {
+      if (g.gl == 0) *O.overflow = 1;
+      continue;
+    }
+    int64_t* setv = O.eid + out;
+    for (int64_t i = 0; i < k; i++) {
+      int64_t j = nv - k + i;
+      int64_t ti = (int64_t)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
+      bool dup = false;
+      for (int64_t c0 = 0; c0 < i; c0 += G) {
+        int64_t c = c0 + g.gl;
+        if (gcount(g, c < i && setv[c] == ti) > 0) dup = true;
+      }
+      __syncwarp(g.mask);
+      if (g.gl == 0) setv[i] = dup ? j : ti;
+      __syncwarp(g.mask);
+    }
+    for (int64_t i0 = 0; i0 < k; i0 += G) {
+      int64_t i = i0 + g.gl;
+      int64_t rk = (i < k) ? setv[i] : -1;
+      __syncwarp(g.mask);
+      if (i < k) {
+        int64_t p = lo + rk;
+        int64_t b = irregular ? upper_bound_seq(GV.dcum + d0, nb, p) - 1 : law_block(GV.law, p);
+        store_out(O, out + i, load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b))), qkey, i);
+      }
+      __syncwarp(g.mask);
+    }
+  }
+}
+
+// ========================== general path (deletions) =========================
+
+__device__ __forceinline__ bool node_ok(const GraphView& G_, int64_t v) {
+  return v >= 0 && v < G_.num_nodes && G_.node_valid[v];
+}
+
+__device__ __forceinline__ bool slot_ok(const GraphView& G_, const Slot& s) { return s.valid && G_.node_valid[s.nbr]; }
 
 __device__ __forceinline__ int nth_set_bit(unsigned m, int n) {  // 0-based
   for (int i = 0; i < n; i++) m &= m - 1;
   return __ffs(m) - 1;
 }
 
-struct HopArgs {
-  GraphView G;
-  const int64_t* src;
-  const int64_t* t_start;  // NULL => TS_MIN
-  const int64_t* t_end;
-  const uint64_t* keys;    // NULL => key_base + q
-  uint64_t key_base;
-  int64_t n;               // query count when n_dev == NULL
-  const int64_t* n_dev;    // device query count (previous hop's total)
-  int64_t fanout;
-  int policy;
-  int64_t delta;
-  uint64_t seed;
-  int64_t* offsets;        // n + 1
-  int64_t* nbr;
-  int64_t* eid;
-  int64_t* ts;
-  uint64_t* out_keys;      // optional child keys
-  int64_t out_cap;
-  unsigned long long* tile_state;
-  unsigned int* tile_counter;
-  int64_t* total;          // this hop's total (device)
-  int* overflow;           // set when a write would exceed out_cap
-};
-
-__device__ __forceinline__ void emit(const HopArgs& A, int64_t at, const Slot& s, uint64_t qkey, int64_t i) {
-  if (at >= A.out_cap) {
-    *A.overflow = 1;
-    return;
-  }
-  __stcs((long long*)A.nbr + at, (long long)s.nbr);
-  __stcs((long long*)A.eid + at, (long long)s.eid);
-  __stcs((long long*)A.ts + at, (long long)s.ts);
-  if (A.out_keys) __stcs((long long*)A.out_keys + at, (long long)child_key(qkey, (uint64_t)i));
-}
-
-// ---- phase 1: window search + candidate count ---------------------------------
-struct QState {
-  int64_t lo, hi, nv, k;
-  int64_t blk;  // block holding hi - 1
-};
-
-__device__ __forceinline__ QState search_query(const HopArgs& A, int64_t q) {
-  const GraphView& G = A.G;
+// timestamps < x in the block whose slots are sts[base, base + size)
+__device__ __forceinline__ int64_t w_block_lower_bound(const GraphView& GV, int64_t base, int64_t size, int64_t x) {
   const int lane = lane_id();
-  QState S{0, 0, 0, 0, -1};
-  int64_t v = A.src[q];
-  if (!node_ok(G, v)) return S;  // sampling.py:153-155
-  int64_t nb = G.num_blocks[v];
-  if (nb == 0) return S;
-  int64_t te = A.t_end[q];
-  int64_t tsr = A.t_start ? A.t_start[q] : GF_TS_MIN;
-  if (A.policy == GF_POLICY_TIME_WINDOW) tsr = (te < GF_TS_MIN + A.delta) ? GF_TS_MIN : te - A.delta;  // sampling.py:202-203
-  int64_t d0 = G.dir_off[v], ns = G.nslots[v];
-  Bound h = list_lower_bound(G, d0, nb, ns, te);
-  int64_t lo = (tsr == GF_TS_MIN) ? __ldg(G.dcum + d0) : list_lower_bound(G, d0, nb, ns, tsr).pos;
-  if (h.pos <= lo) {
-    S.lo = S.hi = lo;
-    return S;
-  }
-  S.lo = lo;
-  S.hi = h.pos;
-  S.blk = h.blk;
-  if (!G.any_deleted) {
-    S.nv = h.pos - lo;
-  } else {
-    // valid candidates only (valid edge && valid neighbour, sampling.py:178); recent needs <= fanout
-    int64_t limit = (A.policy == GF_POLICY_RECENT) ? A.fanout : INT64_MAX;
-    int64_t b = h.blk, p = h.pos, cnt = 0;
-    while (p > lo && cnt < limit) {
-      int64_t cum = __ldg(G.dcum + d0 + b);
-      int64_t cst = max(max(cum, lo), p - 32);
-      int64_t pos = p - 1 - lane;
-      bool ok = false;
-      if (pos >= cst) ok = slot_ok(G, load_slot(G.slots + __ldg(G.dbase + d0 + b) + (pos - cum)));
-      cnt += __popc(__ballot_sync(0xffffffffu, ok));
-      p = cst;
-      if (p == cum) b--;
-    }
-    S.nv = cnt < limit ? cnt : limit;
-  }
-  S.k = S.nv < A.fanout ? S.nv : A.fanout;
-  return S;
-}
-
-// ---- phase 2: selection + write -------------------------------------------------
-__device__ __forceinline__ void emit_query(const HopArgs& A, int64_t q, const QState& S, int64_t out) {
-  const GraphView& G = A.G;
-  const int lane = lane_id();
-  const int64_t k = S.k;
-  int64_t v = A.src[q];
-  int64_t d0 = G.dir_off[v], nb = G.num_blocks[v];
-  uint64_t qkey = A.keys ? A.keys[q] : A.key_base + (uint64_t)q;
-  const int64_t lo = S.lo, hi = S.hi, nv = S.nv;
-  if (A.policy == GF_POLICY_RECENT || k == nv) {
-    // newest first: the first k valid candidates walking back from hi - 1
-    const unsigned lt = (1u << lane) - 1u;
-    int64_t b = S.blk, p = hi, done = 0;
-    while (done < k && p > lo) {
-      int64_t cum = __ldg(G.dcum + d0 + b);
-      int64_t cst = max(max(cum, lo), p - 32);
-      int64_t pos = p - 1 - lane;
-      bool ok = false;
-      Slot s;
-      if (pos >= cst) {
-        s = load_slot(G.slots + __ldg(G.dbase + d0 + b) + (pos - cum));
-        ok = G.any_deleted ? slot_ok(G, s) : true;
-      }
-      unsigned m = __ballot_sync(0xffffffffu, ok);
-      int64_t r = done + __popc(m & lt);
-      if (ok && r < k) emit(A, out + r, s, qkey, r);
-      done += __popc(m);
-      p = cst;
-      if (p == cum) b--;
-    }
-    return;
-  }
-  const bool regular = !(G.nflags[v] & 1);
-  if (k <= 32) {
-    // Floyd: draw t_i in [0, nv-k+i] (independent draws, one per lane), then dedupe in order
-    int64_t t = 0;
-    if (lane < k) t = (int64_t)bounded64(rand64(A.seed, qkey, (uint64_t)lane), (uint64_t)(nv - k + lane + 1));
-    int64_t mine = -1;
-    for (int i = 0; i < (int)k; i++) {
-      int64_t ti = __shfl_sync(0xffffffffu, t, i);
-      bool dup = __ballot_sync(0xffffffffu, lane < i && mine == ti) != 0;
-      if (lane == i) mine = dup ? (nv - k + i) : ti;
-    }
-    if (!G.any_deleted) {
-      if (lane < k) {
-        int64_t p = lo + mine;
-        int64_t b = block_of(G, regular, d0, nb, p);
-        emit(A, out + lane, load_slot(G.slots + __ldg(G.dbase + d0 + b) + (p - __ldg(G.dcum + d0 + b))), qkey, lane);
-      }
+  int64_t seg_lo = base, seg_hi = base + size;
+  if (size > FENCE) {
+    int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;
+    int64_t j = warp_lower_bound(GV.fts + f0, 1, f1 - f0 + 1, x);
+    if (j == 0) {
+      seg_hi = f0 * FENCE;
     } else {
-      // chronological valid rank -> position: forward scan over [lo, hi)
-      int64_t b = block_of(G, false, d0, nb, lo);
-      int64_t p = lo, rank0 = 0;
-      while (p < hi) {
-        int64_t cum = __ldg(G.dcum + d0 + b);
-        int64_t bend = (b == nb - 1) ? G.nslots[v] : __ldg(G.dcum + d0 + b + 1);
-        int64_t cen = min(min(bend, hi), p + 32);
-        int64_t pos = p + lane;
-        Slot s;
-        s.ts = 0; s.eid = 0; s.nbr = 0;
+      seg_lo = (f0 + j - 1) * FENCE;
+      seg_hi = min(seg_lo + FENCE, base + size);
+    }
+  }
+  int64_t p = seg_lo + lane;
+  return seg_lo - base + __popc(__ballot_sync(0xffffffffu, p < seg_hi && __ldg(GV.sts + p) < x));
+}
+
+struct WBound {
+  int64_t pos, blk;
+};
+
+__device__ __forceinline__ WBound w_list_lower_bound(const GraphView& GV, int64_t d0, int64_t nb, int64_t ns_end, int64_t x) {
+  int64_t B = warp_lower_bound(GV.dtmin + d0, 1, nb, x);
+  if (B == 0) return WBound{__ldg(GV.dcum + d0), -1};
+  int64_t b = B - 1;
+  int64_t cum = __ldg(GV.dcum + d0 + b);
+  int64_t size = (b == nb - 1) ? (ns_end - cum) : (__ldg(GV.dcum + d0 + b + 1) - cum);
+  return WBound{cum + w_block_lower_bound(GV, __ldg(GV.dbase + d0 + b), size, x), b};
+}
+
+__global__ void __launch_bounds__(THREADS) k_count_general(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = query_count(Q);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = warp; q < cap_q; q += nwarps) {
+    if (q >= n) {
+      if (lane == 0) counts[q] = 0;
+      continue;
+    }
+    int64_t v = Q.src[q];
+    int64_t lo = 0, hi = 0, nv = 0, k = 0, blk = -1;
+    if (node_ok(GV, v) && GV.num_blocks[v] > 0) {
+      int64_t nb = GV.num_blocks[v], d0 = GV.dir_off[v], ns = GV.nslots[v];
+      int64_t te = Q.t_end[q], tsr = t_start_of(Q, q, te);
+      WBound h = w_list_lower_bound(GV, d0, nb, ns, te);
+      lo = (tsr == GF_TS_MIN) ? __ldg(GV.dcum + d0) : w_list_lower_bound(GV, d0, nb, ns, tsr).pos;
+      hi = h.pos > lo ? h.pos : lo;
+      blk = h.blk;
+      if (hi > lo) {
+        // valid candidates (sampling.py:178); recent needs at most `fanout`
+        int64_t limit = (Q.policy == GF_POLICY_RECENT) ? Q.fanout : INT64_MAX;
+        int64_t b = blk, p = hi, cnt = 0;
+        while (p > lo && cnt < limit) {
+          int64_t cum = __ldg(GV.dcum + d0 + b);
+          int64_t cst = max(max(cum, lo), p - 32);
+          int64_t pos = p - 1 - lane;
+          bool ok = false;
+          if (pos >= cst) ok = slot_ok(GV, load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (pos - cum)));
+          cnt += __popc(__ballot_sync(0xffffffffu, ok));
+          p = cst;
+          if (p == cum) b--;
+        }
+        nv = cnt < limit ? cnt : limit;
+        k = nv < Q.fanout ? nv : Q.fanout;
+      }
+    }
+    if (lane == 0) {
+      counts[q] = k;
+      S.lo[q] = lo;
+      S.hi[q] = hi;
+      S.nv[q] = nv;
+      S.meta[q] = blk;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(THREADS) k_write_general(GraphView GV, QueryIn Q, QState S, LayerOut O) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = query_count(Q);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = warp; q < n; q += nwarps) {
+    const int64_t out = O.offsets[q];
+    const int64_t k = O.offsets[q + 1] - out;
+    if (k == 0) continue;
+    int64_t v = Q.src[q];
+    int64_t d0 = GV.dir_off[v], nb = GV.num_blocks[v];
+    uint64_t qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
+    const int64_t lo = S.lo[q], hi = S.hi[q], nv = S.nv[q];
+    if (Q.policy == GF_POLICY_RECENT || k == nv) {
+      const unsigned lt = (1u << lane) - 1u;
+      int64_t b = S.meta[q], p = hi, done = 0;
+      while (done < k && p > lo) {
+        int64_t cum = __ldg(GV.dcum + d0 + b);
+        int64_t cst = max(max(cum, lo), p - 32);
+        int64_t pos = p - 1 - lane;
         bool ok = false;
-        if (pos < cen) {
-          s = load_slot(G.slots + __ldg(G.dbase + d0 + b) + (pos - cum));
-          ok = slot_ok(G, s);
+        Slot s;
+        if (pos >= cst) {
+          s = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (pos - cum));
+          ok = slot_ok(GV, s);
         }
         unsigned m = __ballot_sync(0xffffffffu, ok);
-        int c = __popc(m);
-        bool here = lane < k && mine >= rank0 && mine < rank0 + c;
-        int srcl = here ? nth_set_bit(m, (int)(mine - rank0)) : lane;
-        Slot t2;
-        t2.ts = __shfl_sync(0xffffffffu, s.ts, srcl);
-        t2.eid = __shfl_sync(0xffffffffu, s.eid, srcl);
-        t2.nbr = __shfl_sync(0xffffffffu, s.nbr, srcl);
-        if (here) emit(A, out + lane, t2, qkey, lane);
-        rank0 += c;
-        p = cen;
-        if (p == bend) b++;
+        int64_t r = done + __popc(m & lt);
+        if (ok && r < k) store_out(O, out + r, s, qkey, r);
+        done += __popc(m);
+        p = cst;
+        if (p == cum) b--;
       }
+      continue;
     }
-    return;
-  }
-  // large fanout: keep the Floyd set in the output's eid column while drawing
-  if (out + k > A.out_cap) {
-    if (lane == 0) *A.overflow = 1;
-    return;
-  }
-  int64_t* sel = A.eid + out;
-  for (int64_t i = 0; i < k; i++) {
-    int64_t j = nv - k + i;
-    int64_t ti = (int64_t)bounded64(rand64(A.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
-    bool dup = false;
-    for (int64_t c0 = 0; c0 < i; c0 += 32) {
-      int64_t c = c0 + lane;
-      if (__ballot_sync(0xffffffffu, c < i && sel[c] == ti)) dup = true;
+    // Floyd's k-of-nv over the chronological valid ranks, then rank -> position scans
+    if (out + k > O.cap) {
+      if (lane == 0) *O.overflow = 1;
+      continue;
     }
-    __syncwarp();
-    if (lane == 0) sel[i] = dup ? j : ti;
-    __syncwarp();
-  }
-  for (int64_t i0 = 0; i0 < k; i0 += 32) {
-    int64_t i = i0 + lane;
-    int64_t rk = (i < k) ? sel[i] : -1;
-    __syncwarp();
-    if (!G.any_deleted) {
-      if (i < k) {
-        int64_t p = lo + rk;
-        int64_t b = block_of(G, regular, d0, nb, p);
-        emit(A, out + i, load_slot(G.slots + __ldg(G.dbase + d0 + b) + (p - __ldg(G.dcum + d0 + b))), qkey, i);
+    int64_t* setv = O.eid + out;
+    for (int64_t i = 0; i < k; i++) {
+      int64_t j = nv - k + i;
+      int64_t ti = (int64_t)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
+      bool dup = false;
+      for (int64_t c0 = 0; c0 < i; c0 += 32) {
+        int64_t c = c0 + lane;
+        if (__ballot_sync(0xffffffffu, c < i && setv[c] == ti)) dup = true;
       }
-    } else {
-      for (int l = 0; l < 32 && i0 + l < k; l++) {
-        int64_t want = __shfl_sync(0xffffffffu, rk, l);
-        int64_t p = lo, seen = 0;
-        int64_t b = block_of(G, false, d0, nb, lo);
-        while (p < hi) {
-          int64_t cum = __ldg(G.dcum + d0 + b);
-          int64_t bend = (b == nb - 1) ? G.nslots[v] : __ldg(G.dcum + d0 + b + 1);
-          int64_t cen = min(min(bend, hi), p + 32);
-          int64_t pos = p + lane;
-          Slot s;
-          s.ts = 0; s.eid = 0; s.nbr = 0;
-          bool ok = false;
-          if (pos < cen) {
-            s = load_slot(G.slots + __ldg(G.dbase + d0 + b) + (pos - cum));
-            ok = slot_ok(G, s);
-          }
-          unsigned m = __ballot_sync(0xffffffffu, ok);
-          int c = __popc(m);
-          if (want < seen + c) {
-            int srcl = nth_set_bit(m, (int)(want - seen));
-            Slot t2;
-            t2.ts = __shfl_sync(0xffffffffu, s.ts, srcl);
-            t2.eid = __shfl_sync(0xffffffffu, s.eid, srcl);
-            t2.nbr = __shfl_sync(0xffffffffu, s.nbr, srcl);
-            if (lane == 0) emit(A, out + i0 + l, t2, qkey, i0 + l);
-            break;
-          }
-          seen += c;
-          p = cen;
-          if (p == bend) b++;
-        }
-      }
+      __syncwarp();
+      if (lane == 0) setv[i] = dup ? j : ti;
+      __syncwarp();
     }
-    __syncwarp();
+    // one forward pass over [lo, hi): a selected chronological valid rank r is
+    // replaced by ~position (negative, so it cannot match again) when reached
+    int64_t b = upper_bound_seq(GV.dcum + d0, nb, lo) - 1;
+    int64_t p = lo, rank0 = 0;
+    while (p < hi) {
+      int64_t cum = __ldg(GV.dcum + d0 + b);
+      int64_t bend = (b == nb - 1) ? GV.nslots[v] : __ldg(GV.dcum + d0 + b + 1);
+      int64_t cen = min(min(bend, hi), p + 32);
+      int64_t pos = p + lane;
+      bool ok = pos < cen && slot_ok(GV, load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (pos - cum)));
+      unsigned m = __ballot_sync(0xffffffffu, ok);
+      int c = __popc(m);
+      for (int64_t i0 = 0; i0 < k; i0 += 32) {
+        int64_t i = i0 + lane;
+        int64_t want = (i < k) ? setv[i] : -1;
+        if (want >= rank0 && want < rank0 + c) setv[i] = ~(p + nth_set_bit(m, (int)(want - rank0)));
+      }
+      __syncwarp();
+      rank0 += c;
+      p = cen;
+      if (p == bend) b++;
+    }
+    for (int64_t i = lane; i < k; i += 32) {
+      int64_t ps = ~setv[i];
+      int64_t bb = upper_bound_seq(GV.dcum + d0, nb, ps) - 1;
+      store_out(O, out + i, load_slot(GV.slots + __ldg(GV.dbase + d0 + bb) + (ps - __ldg(GV.dcum + d0 + bb))), qkey, i);
+    }
   }
 }
 
-// ---- the fused hop kernel ----------------------------------------------------------
-__global__ void __launch_bounds__(THREADS, 4) k_sample_hop(HopArgs A) {
-  __shared__ int64_t s_lo[TQ], s_hi[TQ], s_nv[TQ], s_k[TQ], s_blk[TQ], s_excl[TQ];
-  __shared__ int64_t s_base;
-  __shared__ unsigned int s_tile;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t n = A.n_dev ? *A.n_dev : A.n;
-  if (*A.overflow) n = 0;  // a previous hop overflowed: its outputs are incomplete
-  const int64_t ntiles = (n + TQ - 1) / TQ;
-  while (true) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(A.tile_counter, 1u);
-    __syncthreads();
-    const int64_t tile = s_tile;
-    if (tile >= ntiles) break;
-    // phase 1
-    for (int j = 0; j < QW; j++) {
-      int idx = warp * QW + j;
-      int64_t q = tile * TQ + idx;
-      QState S{0, 0, 0, 0, -1};
-      if (q < n) S = search_query(A, q);
-      if (lane == 0) {
-        s_lo[idx] = S.lo;
-        s_hi[idx] = S.hi;
-        s_nv[idx] = S.nv;
-        s_k[idx] = S.k;
-        s_blk[idx] = S.blk;
-      }
-    }
-    __syncthreads();
-    // tile scan + decoupled look-back (warp 0)
-    if (warp == 0) {
-      int64_t c = s_k[lane], incl = c;
-      for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      s_excl[lane] = incl - c;
-      int64_t agg = __shfl_sync(0xffffffffu, incl, 31);
-      if (lane == 0) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> mine(A.tile_state[tile]);
-        int64_t excl = 0;
-        if (tile == 0) {
-          mine.store(FLAG_P | (unsigned long long)agg, cuda::memory_order_release);
-        } else {
-          mine.store(FLAG_A | (unsigned long long)agg, cuda::memory_order_release);
-          int64_t t = tile - 1;
-          while (true) {
-            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> pred(A.tile_state[t]);
-            unsigned long long st = pred.load(cuda::memory_order_acquire);
-            if ((st >> 62) == 0) continue;
-            excl += (int64_t)(st & VAL_MASK);
-            if ((st >> 62) == 2) break;
-            t--;
-          }
-          mine.store(FLAG_P | (unsigned long long)(excl + agg), cuda::memory_order_release);
-        }
-        s_base = excl;
-        if (tile == ntiles - 1) *A.total = excl + agg;
-        if (tile == 0) A.offsets[0] = 0;
-      }
-    }
-    __syncthreads();
-    // phase 2
-    const int64_t base = s_base;
-    for (int j = 0; j < QW; j++) {
-      int idx = warp * QW + j;
-      int64_t q = tile * TQ + idx;
-      if (q >= n) break;
-      int64_t out = base + s_excl[idx];
-      QState S{s_lo[idx], s_hi[idx], s_nv[idx], s_k[idx], s_blk[idx]};
-      if (lane == 0) A.offsets[q + 1] = out + S.k;
-      if (S.k > 0) emit_query(A, q, S, out);
-    }
-    __syncthreads();
-  }
+// ============================== host side ====================================
+
+__global__ void k_total(const int64_t* offsets, const int64_t* n_dev, int64_t n, int64_t* total) {
+  *total = offsets[n_dev ? *n_dev : n];
 }
 
-__global__ void k_zero_total(int64_t* total, int64_t* offsets) {
-  // a hop with no queries has total 0 and offsets[0] = 0
-  *total = 0;
-  offsets[0] = 0;
-}
-
-int64_t persistent_grid() {
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sample_hop, THREADS, 0);
-    if (per_sm <= 0) per_sm = 1;
-  }
-  return (int64_t)num_sms() * per_sm;
+template <class F>
+gf_status cub_call(F f, cudaStream_t s) {
+  size_t bytes = 0;
+  GF_CUDA(f((void*)nullptr, bytes));
+  Scratch tmp(s);
+  GF_TRY(tmp.alloc(bytes));
+  GF_CUDA(f(tmp.p, bytes));
+  return GF_OK;
 }
 
 gf_status check_args(int64_t n, int64_t fanout, int policy, int64_t delta) {
@@ -457,15 +596,37 @@ gf_status check_args(int64_t n, int64_t fanout, int policy, int64_t delta) {
   return GF_OK;
 }
 
-// Launch one hop.  `state` is tile bookkeeping for at most max_q queries.
-gf_status launch_hop(HopArgs A, int64_t max_q, unsigned long long* state, cudaStream_t s) {
-  int64_t max_tiles = (max_q + TQ - 1) / TQ;
-  A.tile_state = state + 1;
-  A.tile_counter = reinterpret_cast<unsigned int*>(state);
-  GF_CUDA(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (size_t)(max_tiles + 1), s));
-  GF_LAUNCH(k_zero_total, 1, 1, 0, s, A.total, A.offsets);
-  int64_t grid = std::min<int64_t>(persistent_grid(), std::max<int64_t>(max_tiles, 1));
-  GF_LAUNCH(k_sample_hop, grid, THREADS, 0, s, A);
+int64_t grid_for_queries(int64_t cap_q, int per_query_threads) {
+  int64_t blocks = (cap_q * per_query_threads + THREADS - 1) / THREADS;
+  return std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)num_sms() * 16));
+}
+
+// One layer: count -> scan -> total -> write.  cap_q bounds the query count
+// (exact when Q.n_dev is NULL).  total: device slot for this layer's total.
+gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_offsets, const LayerOut& O, int64_t* total,
+                       cudaStream_t s) {
+  GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
+  if (cap_q == 0) {
+    GF_CUDA(cudaMemsetAsync(total, 0, sizeof(int64_t), s));
+    return GF_OK;
+  }
+  Scratch sb(s);
+  Arena A;
+  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + 4096));
+  A.base = sb.as<char>();
+  QState S{A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q),
+           A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q)};
+  int64_t* counts = A.take<int64_t>(cap_q);
+  GraphView GV = view_of(g);
+  const bool fast = !g->any_deleted;
+  if (fast) GF_LAUNCH(k_count_fast, grid_for_queries(cap_q, G), THREADS, 0, s, GV, Q, S, counts, cap_q);
+  else GF_LAUNCH(k_count_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, counts, cap_q);
+  cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
+  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
+  if (e0) prof_stop("cub_scan_offsets", s, e0);
+  GF_LAUNCH(k_total, 1, 1, 0, s, d_offsets, Q.n_dev, Q.n, total);
+  if (fast) GF_LAUNCH(k_write_fast, grid_for_queries(cap_q, G), THREADS, 0, s, GV, Q, S, O);
+  else GF_LAUNCH(k_write_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, O);
   return GF_OK;
 }
 
@@ -479,29 +640,22 @@ gf_status gf_sample_layer(gf_graph* g, const int64_t* d_src, const int64_t* d_t_
                           uint64_t* d_out_keys, int64_t out_cap, int64_t* h_out_total, void* stream) {
   if (!g || !h_out_total || !d_offsets) return fail(GF_EINVAL, "NULL argument");
   GF_TRY(check_args(n, fanout, policy, delta));
-  if (n >= ((int64_t)1 << 40)) return fail(GF_EINVAL, "too many queries in one call");
   DeviceGuard dg(g->device);
   cudaStream_t s = (cudaStream_t)stream;
   *h_out_total = 0;
-  if (n == 0) {
-    GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
-    return GF_OK;
-  }
-  int64_t max_tiles = (n + TQ - 1) / TQ;
   Scratch sb(s);
-  GF_TRY(sb.alloc(sizeof(unsigned long long) * (size_t)(max_tiles + 1) + 64));
-  unsigned long long* state = sb.as<unsigned long long>();
-  int64_t* total = reinterpret_cast<int64_t*>(state + max_tiles + 1);
+  GF_TRY(sb.alloc(64));
+  int64_t* total = sb.as<int64_t>();
   int* overflow = reinterpret_cast<int*>(total + 1);
-  GF_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int), s));
-  HopArgs A{view_of(g), d_src, d_t_start, d_t_end, d_keys, key_base, n, nullptr, fanout, policy, delta, seed,
-            d_offsets, d_nbr, d_eid, d_ts, d_out_keys, out_cap, nullptr, nullptr, total, overflow};
-  GF_TRY(launch_hop(A, n, state, s));
+  GF_CUDA(cudaMemsetAsync(total, 0, 16, s));
+  QueryIn Q{d_src, d_t_start, d_t_end, d_keys, key_base, n, nullptr, fanout, policy, delta, seed};
+  LayerOut O{d_offsets, d_nbr, d_eid, d_ts, d_out_keys, out_cap, overflow};
+  GF_TRY(layer_launch(g, Q, n, d_offsets, O, total, s));
   int64_t h[2] = {0, 0};
-  GF_CUDA(cudaMemcpyAsync(h, total, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaMemcpyAsync(h, total, 16, cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
   *h_out_total = h[0];
-  if (*reinterpret_cast<int*>(&h[1]) || h[0] > out_cap) return fail(GF_ERANGE, "output buffer too small");
+  if ((int)h[1] || h[0] > out_cap) return fail(GF_ERANGE, "output buffer too small");
   return GF_OK;
 }
 
@@ -521,10 +675,6 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
   DeviceGuard dg(g->device);
   cudaStream_t s = (cudaStream_t)stream;
   const bool need_keys = policy != GF_POLICY_RECENT;
-  // scratch: tile state (sized for the largest hop), per-hop totals + overflow flag, key buffers
-  int64_t max_q = n_roots;
-  for (int h = 0; h + 1 < n_hops; h++) max_q = std::max(max_q, h_caps[h]);
-  int64_t max_tiles = (max_q + TQ - 1) / TQ;
   int64_t key_cap = 0;
   if (need_keys)
     for (int h = 0; h + 1 < n_hops; h++) key_cap = std::max(key_cap, h_caps[h]);
@@ -532,14 +682,12 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
   Arena Ar;
   {
     Arena probe;
-    probe.take<unsigned long long>(max_tiles + 1);
     probe.take<int64_t>(n_hops + 2);
     probe.take<uint64_t>(key_cap);
     probe.take<uint64_t>(key_cap);
     GF_TRY(sb.alloc(probe.off + 1024));
   }
   Ar.base = sb.as<char>();
-  unsigned long long* state = Ar.take<unsigned long long>(max_tiles + 1);
   int64_t* totals = Ar.take<int64_t>(n_hops + 2);
   uint64_t* keybuf[2] = {Ar.take<uint64_t>(key_cap), Ar.take<uint64_t>(key_cap)};
   int* overflow = reinterpret_cast<int*>(totals + n_hops);
@@ -550,11 +698,11 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
   const uint64_t* in_keys = nullptr;
   for (int h = 0; h < n_hops; h++) {
     uint64_t* out_keys = (need_keys && h + 1 < n_hops) ? keybuf[h & 1] : nullptr;
-    int64_t hop_max_q = (h == 0) ? n_roots : h_caps[h - 1];
-    HopArgs A{view_of(g), src, nullptr, tend, in_keys, root_key_base, n_roots, n_dev, h_fanouts[h], policy, delta,
-              gf::seed_sequence_2(seed, h), d_offsets[h], d_nbr[h], d_eid[h], d_ts_out[h], out_keys, h_caps[h],
-              nullptr, nullptr, totals + h, overflow};
-    GF_TRY(launch_hop(A, hop_max_q, state, s));
+    int64_t cap_q = (h == 0) ? n_roots : h_caps[h - 1];
+    QueryIn Q{src, nullptr, tend, in_keys, root_key_base, n_roots, n_dev, h_fanouts[h], policy, delta,
+              gf::seed_sequence_2(seed, h)};
+    LayerOut O{d_offsets[h], d_nbr[h], d_eid[h], d_ts_out[h], out_keys, h_caps[h], overflow};
+    GF_TRY(layer_launch(g, Q, cap_q, d_offsets[h], O, totals + h, s));
     src = d_nbr[h];
     tend = d_ts_out[h];
     n_dev = totals + h;
@@ -564,7 +712,7 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
   GF_CUDA(cudaMemcpyAsync(h.data(), totals, sizeof(int64_t) * (n_hops + 1), cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < n_hops; i++) h_totals[i] = h[i];
-  if (*reinterpret_cast<int*>(&h[n_hops])) return fail(GF_ERANGE, "output buffer too small");
+  if ((int)h[n_hops]) return fail(GF_ERANGE, "output buffer too small");
   for (int i = 0; i < n_hops; i++)
     if (h[i] > h_caps[i]) return fail(GF_ERANGE, "output buffer too small");
   return GF_OK;
