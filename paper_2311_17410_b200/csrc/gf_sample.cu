@@ -280,11 +280,34 @@ __global__ void __launch_bounds__(THREADS) k_count_fast(GraphView GV, QueryIn Q,
   }
 }
 
+// cum (first list position) of block b for regular lists (SizingLaw)
+__device__ __forceinline__ int64_t law_cum(const SizingLaw& L, int64_t b) {
+  if (L.kind == GF_SIZING_FIXED) return b * L.size;
+  if (b <= L.m) return b == 0 ? 0 : (1ll << (b - 1));
+  return L.cum_m + (b - L.m) * L.tau;
+}
+
+constexpr int WG = 16;  // lanes per query in the write pass: one output per lane
+
+__device__ __forceinline__ Slot slot_at_position(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
+  int64_t b, cum;
+  if (irregular) {
+    b = upper_bound_seq(GV.dcum + d0, nb, p) - 1;
+    cum = __ldg(GV.dcum + d0 + b);
+  } else {
+    b = law_block(GV.law, p);
+    cum = law_cum(GV.law, b);
+  }
+  return load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - cum));
+}
+
 __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q, QState S, LayerOut O) {
-  const Grp g = make_grp();
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (WG - 1), gbase = lane & WG;
+  const unsigned mask = 0xFFFFu << gbase;
   const int64_t n = query_count(Q);
-  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / WG;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / WG;
   for (int64_t q = gid; q < n; q += ngroups) {
     const int64_t out = O.offsets[q];
     const int64_t k = O.offsets[q + 1] - out;
@@ -292,83 +315,44 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
     const int64_t lo = S.lo[q], hi = S.hi[q], nv = hi - lo;
     const uint64_t qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
     if (Q.policy == GF_POLICY_RECENT || k == nv) {
-      // newest first: positions hi-1, hi-2, ... (sampling.py:188-190)
-      int64_t slot_hi = S.slot[q], cum = S.cum[q];
-      int64_t inblk = hi - cum;  // candidates inside the block holding hi-1
-      for (int64_t r0 = 0; r0 < k; r0 += G * 2) {
-        Slot s0, s1;
-        int64_t r_a = r0 + g.gl, r_b = r0 + G + g.gl;
-        // both loads in flight before either store
-        bool a_ok = r_a < k, b_ok = r_b < k;
-        if (a_ok && r_a < inblk) s0 = load_slot(GV.slots + slot_hi - r_a);
-        if (b_ok && r_b < inblk) s1 = load_slot(GV.slots + slot_hi - r_b);
-        if ((a_ok && r_a >= inblk) || (b_ok && r_b >= inblk)) {
-          // crosses into earlier blocks (rare): locate by directory
-          int64_t d0 = S.d0[q];
-          int64_t nb = S.meta[q] >> 32 & 0x3fffffff;
-          if (a_ok && r_a >= inblk) {
-            int64_t p = hi - 1 - r_a;
-            int64_t b = upper_bound_seq(GV.dcum + d0, nb, p) - 1;
-            s0 = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b)));
-          }
-          if (b_ok && r_b >= inblk) {
-            int64_t p = hi - 1 - r_b;
-            int64_t b = upper_bound_seq(GV.dcum + d0, nb, p) - 1;
-            s1 = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b)));
-          }
+      // newest first: output r is list position hi-1-r (sampling.py:188-190)
+      const int64_t slot_hi = S.slot[q], inblk = hi - S.cum[q];
+      for (int64_t r = gl; r < k; r += WG) {
+        Slot s;
+        if (r < inblk) {
+          s = load_slot(GV.slots + slot_hi - r);
+        } else {  // crosses into earlier blocks
+          const int64_t meta = S.meta[q];
+          s = slot_at_position(GV, (meta >> 62) & 1, S.d0[q], meta >> 32 & 0x3fffffff, hi - 1 - r);
         }
-        if (a_ok) store_out(O, out + r_a, s0, qkey, r_a);
-        if (b_ok) store_out(O, out + r_b, s1, qkey, r_b);
+        store_out(O, out + r, s, qkey, r);
       }
       continue;
     }
-    // uniform / time_window with k < nv: Floyd's algorithm, draws i = gl*V + j
+    // uniform / time_window with k < nv: Floyd's algorithm over candidate indices
     const int64_t meta = S.meta[q], d0 = S.d0[q];
     const bool irregular = (meta >> 62) & 1;
     const int64_t nb = meta >> 32 & 0x3fffffff;
-    if (k <= G * V) {
-      int64_t t[V], sel[V];
-#pragma unroll
-      for (int j = 0; j < V; j += 2) {
-        int64_t i = g.gl * V + j;
-        // one Philox call yields draws i and i+1 (i even)
-        uint32_t c[4] = {(uint32_t)(i >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+    if (k <= WG) {
+      int64_t t = 0, sel = -1;
+      if (gl < k) {
+        // draw i = gl: lanes 2m and 2m+1 evaluate the same Philox block
+        uint32_t c[4] = {(uint32_t)(gl >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
         philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
-        uint64_t r0 = (uint64_t)c[0] | ((uint64_t)c[1] << 32), r1 = (uint64_t)c[2] | ((uint64_t)c[3] << 32);
-        t[j] = (int64_t)bounded64(r0, (uint64_t)(nv - k + i + 1));
-        t[j + 1] = (int64_t)bounded64(r1, (uint64_t)(nv - k + i + 2));
-        sel[j] = sel[j + 1] = -1;
+        uint64_t r = (gl & 1) ? ((uint64_t)c[2] | ((uint64_t)c[3] << 32)) : ((uint64_t)c[0] | ((uint64_t)c[1] << 32));
+        t = (int64_t)bounded64(r, (uint64_t)(nv - k + gl + 1));
       }
-#pragma unroll
-      for (int i = 0; i < G * V; i++) {
-        if (i < k) {
-          int64_t ti = gbcast(g, t[i % V], i / V);
-          bool dup = false;
-#pragma unroll
-          for (int j = 0; j < V; j++) dup |= (g.gl * V + j < i) && sel[j] == ti;
-          dup = gcount(g, dup) > 0;
-          if (g.gl == i / V) sel[i % V] = dup ? (nv - k + i) : ti;
-        }
+      for (int i = 0; i < (int)k; i++) {
+        int64_t ti = __shfl_sync(mask, t, gbase + i);
+        bool dup = (__ballot_sync(mask, gl < i && sel == ti) & mask) != 0;
+        if (gl == i) sel = dup ? (nv - k + i) : ti;
       }
-      Slot sl[V];
-      int64_t idx[V];
-#pragma unroll
-      for (int j = 0; j < V; j++) {
-        idx[j] = g.gl * V + j;
-        if (idx[j] < k) {
-          int64_t p = lo + sel[j];
-          int64_t b = irregular ? upper_bound_seq(GV.dcum + d0, nb, p) - 1 : law_block(GV.law, p);
-          sl[j] = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b)));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < V; j++)
-        if (idx[j] < k) store_out(O, out + idx[j], sl[j], qkey, idx[j]);
+      if (gl < k) store_out(O, out + gl, slot_at_position(GV, irregular, d0, nb, lo + sel), qkey, gl);
       continue;
     }
     // large fanout: keep the Floyd set in the output's eid column while drawing
     if (out + k > O.cap) {
-      if (g.gl == 0) *O.overflow = 1;
+      if (gl == 0) *O.overflow = 1;
       continue;
     }
     int64_t* setv = O.eid + out;
@@ -376,24 +360,20 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
       int64_t j = nv - k + i;
       int64_t ti = (int64_t)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
       bool dup = false;
-      for (int64_t c0 = 0; c0 < i; c0 += G) {
-        int64_t c = c0 + g.gl;
-        if (gcount(g, c < i && setv[c] == ti) > 0) dup = true;
+      for (int64_t c0 = 0; c0 < i; c0 += WG) {
+        int64_t c = c0 + gl;
+        if (__ballot_sync(mask, c < i && setv[c] == ti) & mask) dup = true;
       }
-      __syncwarp(g.mask);
-      if (g.gl == 0) setv[i] = dup ? j : ti;
-      __syncwarp(g.mask);
+      __syncwarp(mask);
+      if (gl == 0) setv[i] = dup ? j : ti;
+      __syncwarp(mask);
     }
-    for (int64_t i0 = 0; i0 < k; i0 += G) {
-      int64_t i = i0 + g.gl;
+    for (int64_t i0 = 0; i0 < k; i0 += WG) {
+      int64_t i = i0 + gl;
       int64_t rk = (i < k) ? setv[i] : -1;
-      __syncwarp(g.mask);
-      if (i < k) {
-        int64_t p = lo + rk;
-        int64_t b = irregular ? upper_bound_seq(GV.dcum + d0, nb, p) - 1 : law_block(GV.law, p);
-        store_out(O, out + i, load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - __ldg(GV.dcum + d0 + b))), qkey, i);
-      }
-      __syncwarp(g.mask);
+      __syncwarp(mask);
+      if (i < k) store_out(O, out + i, slot_at_position(GV, irregular, d0, nb, lo + rk), qkey, i);
+      __syncwarp(mask);
     }
   }
 }
@@ -625,7 +605,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
   if (e0) prof_stop("cub_scan_offsets", s, e0);
   GF_LAUNCH(k_total, 1, 1, 0, s, d_offsets, Q.n_dev, Q.n, total);
-  if (fast) GF_LAUNCH(k_write_fast, grid_for_queries(cap_q, G), THREADS, 0, s, GV, Q, S, O);
+  if (fast) GF_LAUNCH(k_write_fast, grid_for_queries(cap_q, WG), THREADS, 0, s, GV, Q, S, O);
   else GF_LAUNCH(k_write_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, O);
   return GF_OK;
 }
