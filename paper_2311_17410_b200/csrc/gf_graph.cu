@@ -60,7 +60,7 @@ __global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tai
     r[0] = -1;
     r[1] = 0;
     r[2] = NREC_VALID;
-    r[3] = r[4] = r[5] = r[6] = r[7] = 0;
+    for (int w = 3; w < NREC; w++) r[w] = 0;
   }
 }
 
@@ -347,7 +347,7 @@ struct NodeArrays {
   int64_t* nrec;
 };
 struct DirArrays {
-  int64_t *tmin, *cum, *base;
+  int64_t* e;  // DIRW words per entry
 };
 
 __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
@@ -373,22 +373,21 @@ __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__
       // block directory: grow (copy) if needed, then append the new blocks
       if (P.dir_new[s] > 0) {
         int64_t no = dir_used + diroff[s], oo = N.dir_off[v];
-        for (int64_t b = 0; b < nb_old; b++) {
-          D.tmin[no + b] = D.tmin[oo + b];
-          D.cum[no + b] = D.cum[oo + b];
-          D.base[no + b] = D.base[oo + b];
-        }
+        for (int64_t w = 0; w < nb_old * DIRW; w++) D.e[no * DIRW + w] = D.e[oo * DIRW + w];
         N.dir_off[v] = no;
         N.dir_cap[v] = P.dir_new[s];
       }
       int64_t d0 = N.dir_off[v] + nb_old;
       for (int64_t k = 0; k < nb; k++) {
         int64_t rec = blkoff[s] + k, h = R.handle[rec];
-        D.tmin[d0 + k] = B.tmin[h];
-        D.cum[d0 + k] = ns_old + R.first[rec];
-        D.base[d0 + k] = B.base[h];
+        int64_t* e = D.e + (d0 + k) * DIRW;
+        e[0] = B.tmin[h];
+        e[1] = ns_old + R.first[rec];
+        e[2] = B.base[h];
+        e[3] = B.tmax[h];
       }
     }
+    if (t != GF_NO_BLOCK && fill > 0) D.e[(N.dir_off[v] + nb_old - 1) * DIRW + 3] = B.tmax[t];  // old tail grew
     N.num_blocks[v] = nb_old + nb;
     N.degree[v] += cnt;
     N.nslots[v] = ns_old + cnt;
@@ -397,10 +396,12 @@ __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__
     r[0] = doff;
     r[1] = ns_old + cnt;
     r[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
-    r[3] = D.cum[doff];
-    r[4] = D.cum[doff + nbt - 1];
+    r[3] = D.e[doff * DIRW + 1];
+    r[4] = D.e[(doff + nbt - 1) * DIRW + 1];
     r[5] = B.base[tl];
     r[6] = B.tmin[tl];
+    r[7] = B.tmax[tl];
+    r[8] = D.e[doff * DIRW];
   }
 }
 
@@ -529,9 +530,7 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
 gf_status ensure_dir(gf_graph* g, int64_t need, cudaStream_t s) {
   if (need <= g->dir_cap_total) return GF_OK;
   int64_t nc = std::max<int64_t>(need, std::max<int64_t>(4096, g->dir_cap_total * 2));
-  GF_TRY(grow_array(g->dtmin, g->dir_used, nc, s));
-  GF_TRY(grow_array(g->dcum, g->dir_used, nc, s));
-  GF_TRY(grow_array(g->dbase, g->dir_used, nc, s));
+  GF_TRY(grow_array(g->dir, g->dir_used * DIRW, nc * DIRW, s));
   g->dir_cap_total = nc;
   return GF_OK;
 }
@@ -687,7 +686,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
     NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid, g->nflags,
                  g->nrec};
-    DirArrays D{g->dtmin, g->dcum, g->dbase};
+    DirArrays D{g->dir};
     GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
               dir, N, B, D);
     GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
@@ -750,7 +749,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
-                g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dtmin, g->dcum, g->dbase,
+                g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dir,
                 g->slots, g->sts, g->fts, g->nflags, g->nrec};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -883,7 +882,7 @@ gf_status gf_graph_get_info(gf_graph* g, gf_graph_info* out) {
   out->tau = g->tau;
   out->sizing_kind = g->sizing_kind;
   out->sizing_param = g->sizing_param;
-  out->device_bytes = g->node_cap * (8 * 7 + 2) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * 3 +
+  out->device_bytes = g->node_cap * (8 * 7 + 2 + 8 * NREC) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * DIRW +
                       g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8;
   return GF_OK;
 }

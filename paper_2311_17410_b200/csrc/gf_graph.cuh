@@ -5,9 +5,9 @@
 //                                              nslots (list end position), dir_off / dir_cap (block directory)
 //   block arena (SoA, indexed by block handle) capacity, size, tmin, tmax, prev, next (int64, FastTier
 //                                              columns storage.py:147-152) + base (slot-pool offset)
-//   block directory (per node, contiguous)     tmin, cum (list position of first slot), base -- one entry
-//                                              per block, head..tail, so the sampler can binary-search
-//                                              blocks instead of chasing prev pointers
+//   block directory (per node, contiguous)     32-byte entries {tmin, cum (list position of the first
+//                                              slot), base, tmax}, one per block, head..tail, so the
+//                                              sampler can search blocks instead of chasing prev pointers
 //   slot pool  (AoS, 32 B per slot)            Slot{ts, eid, nbr, owner, valid}; block h owns
 //                                              [base[h], base[h] + capacity[h])
 //   sts        (int64 per slot)                dense copy of the slot timestamps (window reads)
@@ -42,7 +42,7 @@ struct gf_graph {
   int64_t *bcap = nullptr, *bsize = nullptr, *btmin = nullptr, *btmax = nullptr, *bprev = nullptr,
           *bnext = nullptr, *bbase = nullptr;
   // block directory pool
-  int64_t *dtmin = nullptr, *dcum = nullptr, *dbase = nullptr;
+  int64_t* dir = nullptr;  // DIRW words per entry: tmin, cum, base, tmax
   // slot pool
   gf::Slot* slots = nullptr;
   int64_t* sts = nullptr;
@@ -53,11 +53,13 @@ namespace gf {
 
 constexpr int FENCE = 32;  // pool slots per fence entry
 
-// NodeRec: one 64-byte line per node, everything a sampler query needs first
-// (one coalesced load by 8 lanes): word 0 dir_off, 1 nslots (list end),
-// 2 num_blocks | valid << 32 | irregular << 33, 3 first live list position,
-// 4 tail block cum, 5 tail block slot base, 6 tail block tmin, 7 reserved.
-constexpr int NREC = 8;
+// NodeRec: one 128-byte line per node, everything a sampler query needs first
+// (one coalesced load): word 0 dir_off, 1 nslots (list end), 2 num_blocks |
+// valid << 32 | irregular << 33, 3 first live list position, 4 tail block
+// cum, 5 tail block slot base, 6 tail block tmin, 7 latest timestamp,
+// 8 head block tmin, 9-15 reserved.
+constexpr int NREC = 16;
+constexpr int DIRW = 4;  // directory entry: tmin, cum, base, tmax
 constexpr int64_t NREC_VALID = 1ll << 32;
 constexpr int64_t NREC_IRREG = 1ll << 33;
 
@@ -88,9 +90,7 @@ struct GraphView {
   const int64_t* num_blocks;
   const int64_t* nslots;
   const int64_t* dir_off;
-  const int64_t* dtmin;
-  const int64_t* dcum;
-  const int64_t* dbase;
+  const int64_t* dir;
   const Slot* slots;
   const int64_t* sts;
   const int64_t* fts;
@@ -102,7 +102,7 @@ struct GraphView {
 };
 
 inline GraphView view_of(const gf_graph* g) {
-  return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off, g->dtmin, g->dcum, g->dbase, g->slots,
+  return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off, g->dir, g->slots,
                    g->sts,        g->fts,        g->nflags, g->nrec,      g->num_nodes, g->any_deleted,
                    sizing_law(g->sizing_kind, g->tau, g->sizing_param)};
 }

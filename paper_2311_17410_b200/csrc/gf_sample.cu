@@ -177,13 +177,40 @@ __device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __
   return lo + c;
 }
 
-// timestamps < x inside the block whose slots are sts[base, base + size)
+// index guess for x in a sorted run spanning times [t0, t1] with n entries
+__device__ __forceinline__ int64_t interp_guess(int64_t x, int64_t t0, int64_t t1, int64_t n) {
+  if (x <= t0) return 0;
+  if (x > t1) return n;
+  double f = ((double)x - (double)t0) / ((double)t1 - (double)t0 + 1.0);
+  return (int64_t)(f * (double)n);
+}
+
+// g_lower_bound that first probes the 32 entries around `guess` (interpolation),
+// falling back to the galloping search on the side the window rules out
+__device__ __forceinline__ int64_t g_lower_bound_guess(const Grp& g, const int64_t* __restrict__ a, int64_t stride,
+                                                       int64_t n, int64_t x, int64_t guess) {
+  if (n <= 32) return g_lower_bound(g, a, stride, n, x);
+  int64_t ws = guess - 16;
+  ws = ws < 0 ? 0 : (ws > n - 32 ? n - 32 : ws);
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (ws + g.gl * V + j) * stride) < x);
+  if (c == 32) {
+    int64_t we = ws + 32;
+    return we == n ? n : we + g_lower_bound(g, a + we * stride, stride, n - we, x);
+  }
+  if (c == 0) return ws == 0 ? 0 : g_lower_bound(g, a, stride, ws, x);
+  return ws + c;
+}
+
+// timestamps < x inside a block whose slots are sts[base, base + size) and whose
+// timestamps span [tmin, tmax]
 __device__ __forceinline__ int64_t g_block_lower_bound(const Grp& g, const GraphView& GV, int64_t base, int64_t size,
-                                                       int64_t x) {
+                                                       int64_t tmin, int64_t tmax, int64_t x) {
   int64_t seg_lo = base, seg_hi = base + size;
   if (size > FENCE) {
-    int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;
-    int64_t j = g_lower_bound(g, GV.fts + f0, 1, f1 - f0 + 1, x);
+    int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE, nf = f1 - f0 + 1;
+    int64_t j = g_lower_bound_guess(g, GV.fts + f0, 1, nf, x, interp_guess(x, tmin, tmax, nf));
     if (j == 0) {
       seg_hi = f0 * FENCE;
     } else {
@@ -201,12 +228,13 @@ __device__ __forceinline__ int64_t g_block_lower_bound(const Grp& g, const Graph
 }
 
 struct NodeView {
-  int64_t d0, ns, nb, first, tcum, tbase, ttmin;
+  int64_t d0, ns, nb, first, tcum, tbase, ttmin, tmax, htmin;
   bool valid, irregular;
 };
 
 __device__ __forceinline__ NodeView load_node(const Grp& g, const GraphView& GV, int64_t v) {
-  int64_t w = __ldg(GV.nrec + v * NREC + g.gl);
+  const int64_t* r = GV.nrec + v * NREC;
+  int64_t w = __ldg(r + g.gl), w8 = __ldg(r + 8 + g.gl);
   NodeView N;
   N.d0 = gbcast(g, w, 0);
   N.ns = gbcast(g, w, 1);
@@ -215,6 +243,8 @@ __device__ __forceinline__ NodeView load_node(const Grp& g, const GraphView& GV,
   N.tcum = gbcast(g, w, 4);
   N.tbase = gbcast(g, w, 5);
   N.ttmin = gbcast(g, w, 6);
+  N.tmax = gbcast(g, w, 7);
+  N.htmin = gbcast(g, w8, 0);
   N.nb = w2 & 0xffffffffll;
   N.valid = (w2 & NREC_VALID) != 0;
   N.irregular = (w2 & NREC_IRREG) != 0;
@@ -226,24 +256,32 @@ struct Bnd {
 };
 
 __device__ __forceinline__ Bnd g_list_lower_bound(const Grp& g, const GraphView& GV, const NodeView& N, int64_t x) {
-  int64_t b, cum, base, size;
+  int64_t b, cum, base, size, tmin, tmax;
   if (N.ttmin < x) {  // boundary inside the tail block
     b = N.nb - 1;
     cum = N.tcum;
     base = N.tbase;
     size = N.ns - N.tcum;
+    tmin = N.ttmin;
+    tmax = N.tmax;
   } else {
-    int64_t B = g_lower_bound(g, GV.dtmin + N.d0, 1, N.nb - 1, x);  // non-tail blocks with tmin < x
+    // non-tail blocks with tmin < x (directory entries are DIRW words, tmin first)
+    const int64_t* d = GV.dir + N.d0 * DIRW;
+    int64_t nt = N.nb - 1;
+    int64_t B = g_lower_bound_guess(g, d, DIRW, nt, x, interp_guess(x, N.htmin, N.ttmin, nt));
     if (B == 0) return Bnd{N.first, -1, 0, 0};
     b = B - 1;
-    cum = __ldg(GV.dcum + N.d0 + b);
-    size = __ldg(GV.dcum + N.d0 + b + 1) - cum;
-    base = __ldg(GV.dbase + N.d0 + b);
+    const int64_t* e = d + b * DIRW;  // just probed: an L1 hit
+    tmin = __ldg(e);
+    cum = __ldg(e + 1);
+    base = __ldg(e + 2);
+    tmax = __ldg(e + 3);
+    size = (b + 1 < nt ? __ldg(e + DIRW + 1) : N.tcum) - cum;
   }
-  return Bnd{cum + g_block_lower_bound(g, GV, base, size, x), b, cum, base};
+  return Bnd{cum + g_block_lower_bound(g, GV, base, size, tmin, tmax, x), b, cum, base};
 }
 
-__global__ void __launch_bounds__(THREADS) k_count_fast(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
+__global__ void __launch_bounds__(THREADS, 4) k_count_fast(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
   const Grp g = make_grp();
   const int64_t n = query_count(Q);
   const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
@@ -289,16 +327,29 @@ __device__ __forceinline__ int64_t law_cum(const SizingLaw& L, int64_t b) {
 
 constexpr int WG = 16;  // lanes per query in the write pass: one output per lane
 
+// per-thread: directory index of the block holding list position p (cum is word 1)
+__device__ __forceinline__ int64_t dir_block_of(const GraphView& GV, int64_t d0, int64_t nb, int64_t p) {
+  const int64_t* d = GV.dir + d0 * DIRW + 1;
+  int64_t lo = 0, hi = nb;
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (__ldg(d + m * DIRW) <= p) lo = m + 1;
+    else hi = m;
+  }
+  return lo - 1;
+}
+
 __device__ __forceinline__ Slot slot_at_position(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
   int64_t b, cum;
+  const int64_t* d = GV.dir + d0 * DIRW;
   if (irregular) {
-    b = upper_bound_seq(GV.dcum + d0, nb, p) - 1;
-    cum = __ldg(GV.dcum + d0 + b);
+    b = dir_block_of(GV, d0, nb, p);
+    cum = __ldg(d + b * DIRW + 1);
   } else {
     b = law_block(GV.law, p);
     cum = law_cum(GV.law, b);
   }
-  return load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (p - cum));
+  return load_slot(GV.slots + __ldg(d + b * DIRW + 2) + (p - cum));
 }
 
 __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q, QState S, LayerOut O) {
@@ -414,12 +465,12 @@ struct WBound {
 };
 
 __device__ __forceinline__ WBound w_list_lower_bound(const GraphView& GV, int64_t d0, int64_t nb, int64_t ns_end, int64_t x) {
-  int64_t B = warp_lower_bound(GV.dtmin + d0, 1, nb, x);
-  if (B == 0) return WBound{__ldg(GV.dcum + d0), -1};
+  int64_t B = warp_lower_bound(GV.dir + d0 * DIRW, DIRW, nb, x);
+  if (B == 0) return WBound{__ldg(GV.dir + d0 * DIRW + 1), -1};
   int64_t b = B - 1;
-  int64_t cum = __ldg(GV.dcum + d0 + b);
-  int64_t size = (b == nb - 1) ? (ns_end - cum) : (__ldg(GV.dcum + d0 + b + 1) - cum);
-  return WBound{cum + w_block_lower_bound(GV, __ldg(GV.dbase + d0 + b), size, x), b};
+  int64_t cum = __ldg(GV.dir + (d0 + b) * DIRW + 1);
+  int64_t size = (b == nb - 1) ? (ns_end - cum) : (__ldg(GV.dir + (d0 + b + 1) * DIRW + 1) - cum);
+  return WBound{cum + w_block_lower_bound(GV, __ldg(GV.dir + (d0 + b) * DIRW + 2), size, x), b};
 }
 
 __global__ void __launch_bounds__(THREADS) k_count_general(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
@@ -438,7 +489,7 @@ __global__ void __launch_bounds__(THREADS) k_count_general(GraphView GV, QueryIn
       int64_t nb = GV.num_blocks[v], d0 = GV.dir_off[v], ns = GV.nslots[v];
       int64_t te = Q.t_end[q], tsr = t_start_of(Q, q, te);
       WBound h = w_list_lower_bound(GV, d0, nb, ns, te);
-      lo = (tsr == GF_TS_MIN) ? __ldg(GV.dcum + d0) : w_list_lower_bound(GV, d0, nb, ns, tsr).pos;
+      lo = (tsr == GF_TS_MIN) ? __ldg(GV.dir + d0 * DIRW + 1) : w_list_lower_bound(GV, d0, nb, ns, tsr).pos;
       hi = h.pos > lo ? h.pos : lo;
       blk = h.blk;
       if (hi > lo) {
@@ -446,11 +497,11 @@ __global__ void __launch_bounds__(THREADS) k_count_general(GraphView GV, QueryIn
         int64_t limit = (Q.policy == GF_POLICY_RECENT) ? Q.fanout : INT64_MAX;
         int64_t b = blk, p = hi, cnt = 0;
         while (p > lo && cnt < limit) {
-          int64_t cum = __ldg(GV.dcum + d0 + b);
+          int64_t cum = __ldg(GV.dir + (d0 + b) * DIRW + 1);
           int64_t cst = max(max(cum, lo), p - 32);
           int64_t pos = p - 1 - lane;
           bool ok = false;
-          if (pos >= cst) ok = slot_ok(GV, load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (pos - cum)));
+          if (pos >= cst) ok = slot_ok(GV, load_slot(GV.slots + __ldg(GV.dir + (d0 + b) * DIRW + 2) + (pos - cum)));
           cnt += __popc(__ballot_sync(0xffffffffu, ok));
           p = cst;
           if (p == cum) b--;
@@ -486,13 +537,13 @@ __global__ void __launch_bounds__(THREADS) k_write_general(GraphView GV, QueryIn
       const unsigned lt = (1u << lane) - 1u;
       int64_t b = S.meta[q], p = hi, done = 0;
       while (done < k && p > lo) {
-        int64_t cum = __ldg(GV.dcum + d0 + b);
+        int64_t cum = __ldg(GV.dir + (d0 + b) * DIRW + 1);
         int64_t cst = max(max(cum, lo), p - 32);
         int64_t pos = p - 1 - lane;
         bool ok = false;
         Slot s;
         if (pos >= cst) {
-          s = load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (pos - cum));
+          s = load_slot(GV.slots + __ldg(GV.dir + (d0 + b) * DIRW + 2) + (pos - cum));
           ok = slot_ok(GV, s);
         }
         unsigned m = __ballot_sync(0xffffffffu, ok);
@@ -524,14 +575,14 @@ __global__ void __launch_bounds__(THREADS) k_write_general(GraphView GV, QueryIn
     }
     // one forward pass over [lo, hi): a selected chronological valid rank r is
     // replaced by ~position (negative, so it cannot match again) when reached
-    int64_t b = upper_bound_seq(GV.dcum + d0, nb, lo) - 1;
+    int64_t b = dir_block_of(GV, d0, nb, lo);
     int64_t p = lo, rank0 = 0;
     while (p < hi) {
-      int64_t cum = __ldg(GV.dcum + d0 + b);
-      int64_t bend = (b == nb - 1) ? GV.nslots[v] : __ldg(GV.dcum + d0 + b + 1);
+      int64_t cum = __ldg(GV.dir + (d0 + b) * DIRW + 1);
+      int64_t bend = (b == nb - 1) ? GV.nslots[v] : __ldg(GV.dir + (d0 + b + 1) * DIRW + 1);
       int64_t cen = min(min(bend, hi), p + 32);
       int64_t pos = p + lane;
-      bool ok = pos < cen && slot_ok(GV, load_slot(GV.slots + __ldg(GV.dbase + d0 + b) + (pos - cum)));
+      bool ok = pos < cen && slot_ok(GV, load_slot(GV.slots + __ldg(GV.dir + (d0 + b) * DIRW + 2) + (pos - cum)));
       unsigned m = __ballot_sync(0xffffffffu, ok);
       int c = __popc(m);
       for (int64_t i0 = 0; i0 < k; i0 += 32) {
@@ -546,8 +597,8 @@ __global__ void __launch_bounds__(THREADS) k_write_general(GraphView GV, QueryIn
     }
     for (int64_t i = lane; i < k; i += 32) {
       int64_t ps = ~setv[i];
-      int64_t bb = upper_bound_seq(GV.dcum + d0, nb, ps) - 1;
-      store_out(O, out + i, load_slot(GV.slots + __ldg(GV.dbase + d0 + bb) + (ps - __ldg(GV.dcum + d0 + bb))), qkey, i);
+      int64_t bb = dir_block_of(GV, d0, nb, ps);
+      store_out(O, out + i, load_slot(GV.slots + __ldg(GV.dir + (d0 + bb) * DIRW + 2) + (ps - __ldg(GV.dir + (d0 + bb) * DIRW + 1))), qkey, i);
     }
   }
 }
