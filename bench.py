@@ -302,25 +302,35 @@ def bench_ours(args, cfg, world, rank, local):
 
     # per-kernel shares (separate profiled pass, same workload)
     _lib.profile_enable(True)
-    e_p, q_p, _ = run_step(g, roots, rts, key_base)
+    e_p, q_p, outs_p = run_step(g, roots, rts, key_base)
     prof = _lib.profile_summary()
     _lib.profile_enable(False)
-    # algorithmic bytes: count kernel 65 B/query, write kernel 50 B/sampled edge
-    alg = {"k_count_fast": BYTES_PER_QUERY * q_p, "k_write_fast": BYTES_PER_EDGE * e_p}
+    # per (policy, hop) layer sizes for the per-launch algorithmic bytes:
+    # count kernel 65 B/query, write kernel 50 B/sampled edge
+    layer_qs = {}
+    for pol, s_ in zip(POLICIES, outs_p):
+        for h, lay in enumerate(s_.layers):
+            layer_qs[f"{pol}/hop{h}"] = (int(lay.source_nodes.numel()), int(lay.neighbors.numel()))
     pk = peaks()
-    kernels = {}
+    kernels, base_ms, base_bytes = {}, {}, {}
     tot_ms = sum(v[1] for v in prof.values())
-    for name, (cnt, kms) in prof.items():
-        short = name.split("(")[0]
-        kernels[short] = {"launches": cnt, "ms": round(kms, 4), "share": round(kms / tot_ms, 4) if tot_ms else None}
-        if short in alg and kms > 0:
-            kernels[short]["achieved_gbs"] = round(alg[short] / (kms / 1e3) / 1e9, 1)
-    dom = max(((k, v) for k, v in kernels.items() if k in alg), key=lambda kv: kv[1]["ms"])
-    dom_name, dom_v = dom
-    achieved = alg[dom_name] / (dom_v["ms"] / 1e3) / 1e9
+    for name, (cnt, kms) in sorted(prof.items()):
+        base = name.split("[")[0]
+        tag = name[len(base) + 1:-1] if "[" in name else None
+        ent = {"launches": cnt, "ms": round(kms, 4), "share": round(kms / tot_ms, 4) if tot_ms else None}
+        if tag in layer_qs and base in ("k_count_fast", "k_write_fast", "k_count_general", "k_write_general"):
+            q_l, s_l = layer_qs[tag]
+            b = BYTES_PER_QUERY * q_l if base.startswith("k_count") else BYTES_PER_EDGE * s_l
+            ent["alg_bytes"] = b
+            ent["achieved_gbs"] = round(b / (kms / 1e3) / 1e9, 1) if kms > 0 else None
+            base_bytes[base] = base_bytes.get(base, 0) + b
+        base_ms[base] = base_ms.get(base, 0.0) + kms
+        kernels[name] = ent
+    dom_name = max(base_bytes, key=lambda k: base_ms[k])
+    achieved = base_bytes[dom_name] / (base_ms[dom_name] / 1e3) / 1e9
     traffic = load_traffic().get(dom_name)
-    pipe_ms = sum(v[1] for k, v in prof.items() if k.split("(")[0] in ("k_count_fast", "k_write_fast", "k_total",
-                                                                          "cub_scan_offsets"))
+    pipe_ms = sum(base_ms.get(k, 0.0) for k in ("k_count_fast", "k_write_fast", "k_count_general", "k_write_general",
+                                                 "k_total", "cub_scan_offsets"))
     pipe_gbs = (BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p) / (pipe_ms / 1e3) / 1e9 if pipe_ms else None
 
     # e2e through the public API with host (pinned) buffers: H2D roots, sample, D2H every layer

@@ -39,6 +39,7 @@ uint64_t seed_sequence_2(uint64_t a, uint64_t b);
 
 // optional per-launch CUDA-event profiling (gf_profile_enable)
 extern std::atomic<int> g_profile;
+extern thread_local std::string g_prof_tag;  // appended to profiled kernel names
 cudaEvent_t prof_start(cudaStream_t s);
 void prof_stop(const char* name, cudaStream_t s, cudaEvent_t e0);
 

@@ -733,7 +733,12 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
     QueryIn Q{src, nullptr, tend, in_keys, root_key_base, n_roots, n_dev, h_fanouts[h], policy, delta,
               gf::seed_sequence_2(seed, h)};
     LayerOut O{d_offsets[h], d_nbr[h], d_eid[h], d_ts_out[h], out_keys, h_caps[h], overflow};
-    GF_TRY(layer_launch(g, Q, cap_q, d_offsets[h], O, totals + h, s));
+    if (g_profile.load(std::memory_order_relaxed))
+      g_prof_tag = std::string(policy == GF_POLICY_RECENT ? "recent" : policy == GF_POLICY_UNIFORM ? "uniform" : "tw") +
+                   "/hop" + std::to_string(h);
+    gf_status st = layer_launch(g, Q, cap_q, d_offsets[h], O, totals + h, s);
+    g_prof_tag.clear();
+    GF_TRY(st);
     src = d_nbr[h];
     tend = d_ts_out[h];
     n_dev = totals + h;

@@ -13,8 +13,10 @@ static thread_local std::string t_err;
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_profile{0};
 
+thread_local std::string g_prof_tag;
+
 struct ProfRec {
-  const char* name;
+  std::string name;
   cudaEvent_t e0, e1;
 };
 static std::mutex g_prof_mu;
@@ -31,7 +33,7 @@ void prof_stop(const char* name, cudaStream_t s, cudaEvent_t e0) {
   if (cudaEventCreate(&e1) != cudaSuccess) return;
   cudaEventRecord(e1, s);
   std::lock_guard<std::mutex> lk(g_prof_mu);
-  g_prof.push_back({name, e0, e1});
+  g_prof.push_back({g_prof_tag.empty() ? std::string(name) : std::string(name) + "[" + g_prof_tag + "]", e0, e1});
 }
 static void prof_clear() {
   std::lock_guard<std::mutex> lk(g_prof_mu);
