@@ -25,6 +25,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -315,8 +316,9 @@ def bench_ours(args, cfg, world, rank, local):
     kernels, base_ms, base_bytes = {}, {}, {}
     tot_ms = sum(v[1] for v in prof.values())
     for name, (cnt, kms) in sorted(prof.items()):
-        base = name.split("[")[0]
-        tag = name[len(base) + 1:-1] if "[" in name else None
+        raw = name.split("[")[0]
+        tag = name[len(raw) + 1:-1] if "[" in name else None
+        base = re.sub(r"[()]|<.*>", "", raw).strip()
         ent = {"launches": cnt, "ms": round(kms, 4), "share": round(kms / tot_ms, 4) if tot_ms else None}
         if tag in layer_qs and base in ("k_count_fast", "k_write_fast", "k_count_general", "k_write_general"):
             q_l, s_l = layer_qs[tag]

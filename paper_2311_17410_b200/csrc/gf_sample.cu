@@ -325,7 +325,6 @@ __device__ __forceinline__ int64_t law_cum(const SizingLaw& L, int64_t b) {
   return L.cum_m + (b - L.m) * L.tau;
 }
 
-constexpr int WG = 16;  // lanes per query in the write pass: one output per lane
 
 // per-thread: directory index of the block holding list position p (cum is word 1)
 __device__ __forceinline__ int64_t dir_block_of(const GraphView& GV, int64_t d0, int64_t nb, int64_t p) {
@@ -352,13 +351,16 @@ __device__ __forceinline__ Slot slot_at_position(const GraphView& GV, bool irreg
   return load_slot(GV.slots + __ldg(d + b * DIRW + 2) + (p - cum));
 }
 
+// Write pass: WGT lanes per query, RT outputs per lane (WGT * RT = 16 outputs per round)
+template <int WGT, int RT>
 __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q, QState S, LayerOut O) {
+  static_assert(WGT * RT == 16, "16 outputs per round");
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (WG - 1), gbase = lane & WG;
-  const unsigned mask = 0xFFFFu << gbase;
+  const int gl = lane & (WGT - 1), gbase = lane & ~(WGT - 1);
+  const unsigned mask = ((WGT == 32) ? 0xFFFFFFFFu : ((1u << WGT) - 1u)) << gbase;
   const int64_t n = query_count(Q);
-  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / WG;
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / WG;
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / WGT;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / WGT;
   for (int64_t q = gid; q < n; q += ngroups) {
     const int64_t out = O.offsets[q];
     const int64_t k = O.offsets[q + 1] - out;
@@ -368,15 +370,25 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
     if (Q.policy == GF_POLICY_RECENT || k == nv) {
       // newest first: output r is list position hi-1-r (sampling.py:188-190)
       const int64_t slot_hi = S.slot[q], inblk = hi - S.cum[q];
-      for (int64_t r = gl; r < k; r += WG) {
-        Slot s;
-        if (r < inblk) {
-          s = load_slot(GV.slots + slot_hi - r);
-        } else {  // crosses into earlier blocks
-          const int64_t meta = S.meta[q];
-          s = slot_at_position(GV, (meta >> 62) & 1, S.d0[q], meta >> 32 & 0x3fffffff, hi - 1 - r);
+      for (int64_t r0 = 0; r0 < k; r0 += WGT * RT) {
+        Slot sl[RT];
+#pragma unroll
+        for (int j = 0; j < RT; j++) {
+          int64_t r = r0 + j * WGT + gl;
+          if (r < k) {
+            if (r < inblk) {
+              sl[j] = load_slot(GV.slots + slot_hi - r);
+            } else {  // crosses into earlier blocks
+              const int64_t meta = S.meta[q];
+              sl[j] = slot_at_position(GV, (meta >> 62) & 1, S.d0[q], meta >> 32 & 0x3fffffff, hi - 1 - r);
+            }
+          }
         }
-        store_out(O, out + r, s, qkey, r);
+#pragma unroll
+        for (int j = 0; j < RT; j++) {
+          int64_t r = r0 + j * WGT + gl;
+          if (r < k) store_out(O, out + r, sl[j], qkey, r);
+        }
       }
       continue;
     }
@@ -384,21 +396,41 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
     const int64_t meta = S.meta[q], d0 = S.d0[q];
     const bool irregular = (meta >> 62) & 1;
     const int64_t nb = meta >> 32 & 0x3fffffff;
-    if (k <= WG) {
-      int64_t t = 0, sel = -1;
-      if (gl < k) {
-        // draw i = gl: lanes 2m and 2m+1 evaluate the same Philox block
-        uint32_t c[4] = {(uint32_t)(gl >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
-        philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
-        uint64_t r = (gl & 1) ? ((uint64_t)c[2] | ((uint64_t)c[3] << 32)) : ((uint64_t)c[0] | ((uint64_t)c[1] << 32));
-        t = (int64_t)bounded64(r, (uint64_t)(nv - k + gl + 1));
+    if (k <= WGT * RT) {
+      // draw i = j * WGT + gl
+      int64_t t[RT], sel[RT];
+#pragma unroll
+      for (int j = 0; j < RT; j++) {
+        int64_t i = j * WGT + gl;
+        t[j] = 0;
+        sel[j] = -1;
+        if (i < k) {
+          uint32_t c[4] = {(uint32_t)(i >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+          philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
+          uint64_t r = (i & 1) ? ((uint64_t)c[2] | ((uint64_t)c[3] << 32)) : ((uint64_t)c[0] | ((uint64_t)c[1] << 32));
+          t[j] = (int64_t)bounded64(r, (uint64_t)(nv - k + i + 1));
+        }
       }
-      for (int i = 0; i < (int)k; i++) {
-        int64_t ti = __shfl_sync(mask, t, gbase + i);
-        bool dup = (__ballot_sync(mask, gl < i && sel == ti) & mask) != 0;
-        if (gl == i) sel = dup ? (nv - k + i) : ti;
+#pragma unroll
+      for (int i = 0; i < WGT * RT; i++) {
+        if (i < k) {
+          int64_t ti = __shfl_sync(mask, t[i / WGT], gbase + (i % WGT));
+          bool dup = false;
+#pragma unroll
+          for (int j = 0; j < RT; j++) dup |= (j * WGT + gl < i) && sel[j] == ti;
+          dup = (__ballot_sync(mask, dup) & mask) != 0;
+          if (gl == i % WGT) sel[i / WGT] = dup ? (nv - k + i) : ti;
+        }
       }
-      if (gl < k) store_out(O, out + gl, slot_at_position(GV, irregular, d0, nb, lo + sel), qkey, gl);
+      Slot sl[RT];
+#pragma unroll
+      for (int j = 0; j < RT; j++)
+        if (j * WGT + gl < k) sl[j] = slot_at_position(GV, irregular, d0, nb, lo + sel[j]);
+#pragma unroll
+      for (int j = 0; j < RT; j++) {
+        int64_t i = j * WGT + gl;
+        if (i < k) store_out(O, out + i, sl[j], qkey, i);
+      }
       continue;
     }
     // large fanout: keep the Floyd set in the output's eid column while drawing
@@ -411,7 +443,7 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
       int64_t j = nv - k + i;
       int64_t ti = (int64_t)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
       bool dup = false;
-      for (int64_t c0 = 0; c0 < i; c0 += WG) {
+      for (int64_t c0 = 0; c0 < i; c0 += WGT) {
         int64_t c = c0 + gl;
         if (__ballot_sync(mask, c < i && setv[c] == ti) & mask) dup = true;
       }
@@ -419,7 +451,7 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
       if (gl == 0) setv[i] = dup ? j : ti;
       __syncwarp(mask);
     }
-    for (int64_t i0 = 0; i0 < k; i0 += WG) {
+    for (int64_t i0 = 0; i0 < k; i0 += WGT) {
       int64_t i = i0 + gl;
       int64_t rk = (i < k) ? setv[i] : -1;
       __syncwarp(mask);
@@ -656,8 +688,13 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
   if (e0) prof_stop("cub_scan_offsets", s, e0);
   GF_LAUNCH(k_total, 1, 1, 0, s, d_offsets, Q.n_dev, Q.n, total);
-  if (fast) GF_LAUNCH(k_write_fast, grid_for_queries(cap_q, WG), THREADS, 0, s, GV, Q, S, O);
-  else GF_LAUNCH(k_write_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, O);
+  if (fast) {
+    static const int wg = getenv("GF_WRITE_LANES") ? atoi(getenv("GF_WRITE_LANES")) : 8;
+    if (wg == 16) GF_LAUNCH((k_write_fast<16, 1>), grid_for_queries(cap_q, 16), THREADS, 0, s, GV, Q, S, O);
+    else if (wg == 4) GF_LAUNCH((k_write_fast<4, 4>), grid_for_queries(cap_q, 4), THREADS, 0, s, GV, Q, S, O);
+    else GF_LAUNCH((k_write_fast<8, 2>), grid_for_queries(cap_q, 8), THREADS, 0, s, GV, Q, S, O);
+  }
+  if (!fast) GF_LAUNCH(k_write_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, O);
   return GF_OK;
 }
 
