@@ -86,14 +86,14 @@ __device__ __forceinline__ int64_t t_start_of(const QueryIn& Q, int64_t q, int64
 }
 
 __device__ __forceinline__ Slot load_slot(const Slot* p) {
-  const int4* q = reinterpret_cast<const int4*>(p);
-  int4 a = __ldg(q), b = __ldg(q + 1);
+  int64_t w0, w1, w2, w3;
+  ld256_stream(p, w0, w1, w2, w3);
   Slot s;
-  s.ts = ((int64_t)(uint32_t)a.y << 32) | (uint32_t)a.x;
-  s.eid = ((int64_t)(uint32_t)a.w << 32) | (uint32_t)a.z;
-  s.nbr = b.x;
-  s.owner = b.y;
-  s.valid = (uint32_t)b.z;
+  s.ts = w0;
+  s.eid = w1;
+  s.nbr = (int32_t)(w2 & 0xffffffff);
+  s.owner = (int32_t)(w2 >> 32);
+  s.valid = (uint32_t)(w3 & 0xffffffff);
   s.pad = 0;
   return s;
 }
@@ -150,7 +150,7 @@ __device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __
   if (n > 32) {
     int c = 0;
 #pragma unroll
-    for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (n - 32 + g.gl * V + j) * stride) < x);
+    for (int j = 0; j < V; j++) c += gcount(g, ld_keep(a + (n - 32 + g.gl * V + j) * stride, l2_keep_policy()) < x);
     if (c > 0) return n - 32 + c;
     hi = n - 32;
   }
@@ -160,7 +160,7 @@ __device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __
 #pragma unroll
     for (int j = 0; j < V; j++) {
       int64_t p = lo + (int64_t)(g.gl * V + j) * step;
-      c += gcount(g, p < hi && __ldg(a + p * stride) < x);
+      c += gcount(g, p < hi && ld_keep(a + p * stride, l2_keep_policy()) < x);
     }
     if (c == 0) return lo;
     int64_t plast = lo + (int64_t)(c - 1) * step;
@@ -172,7 +172,7 @@ __device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __
 #pragma unroll
   for (int j = 0; j < V; j++) {
     int64_t p = lo + g.gl * V + j;
-    c += gcount(g, p < hi && __ldg(a + p * stride) < x);
+    c += gcount(g, p < hi && ld_keep(a + p * stride, l2_keep_policy()) < x);
   }
   return lo + c;
 }
@@ -194,7 +194,7 @@ __device__ __forceinline__ int64_t g_lower_bound_guess(const Grp& g, const int64
   ws = ws < 0 ? 0 : (ws > n - 32 ? n - 32 : ws);
   int c = 0;
 #pragma unroll
-  for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (ws + g.gl * V + j) * stride) < x);
+  for (int j = 0; j < V; j++) c += gcount(g, ld_keep(a + (ws + g.gl * V + j) * stride, l2_keep_policy()) < x);
   if (c == 32) {
     int64_t we = ws + 32;
     return we == n ? n : we + g_lower_bound(g, a + we * stride, stride, n - we, x);
@@ -234,7 +234,7 @@ struct NodeView {
 
 __device__ __forceinline__ NodeView load_node(const Grp& g, const GraphView& GV, int64_t v) {
   const int64_t* r = GV.nrec + v * NREC;
-  int64_t w = __ldg(r + g.gl), w8 = __ldg(r + 8 + g.gl);
+  int64_t w = ld_keep(r + g.gl, l2_keep_policy()), w8 = ld_keep(r + 8 + g.gl, l2_keep_policy());
   NodeView N;
   N.d0 = gbcast(g, w, 0);
   N.ns = gbcast(g, w, 1);
@@ -272,11 +272,11 @@ __device__ __forceinline__ Bnd g_list_lower_bound(const Grp& g, const GraphView&
     if (B == 0) return Bnd{N.first, -1, 0, 0};
     b = B - 1;
     const int64_t* e = d + b * DIRW;  // just probed: an L1 hit
-    tmin = __ldg(e);
-    cum = __ldg(e + 1);
-    base = __ldg(e + 2);
-    tmax = __ldg(e + 3);
-    size = (b + 1 < nt ? __ldg(e + DIRW + 1) : N.tcum) - cum;
+    tmin = ld_keep(e, l2_keep_policy());
+    cum = ld_keep(e + 1, l2_keep_policy());
+    base = ld_keep(e + 2, l2_keep_policy());
+    tmax = ld_keep(e + 3, l2_keep_policy());
+    size = (b + 1 < nt ? ld_keep(e + DIRW + 1, l2_keep_policy()) : N.tcum) - cum;
   }
   return Bnd{cum + g_block_lower_bound(g, GV, base, size, tmin, tmax, x), b, cum, base};
 }
@@ -332,7 +332,7 @@ __device__ __forceinline__ int64_t dir_block_of(const GraphView& GV, int64_t d0,
   int64_t lo = 0, hi = nb;
   while (lo < hi) {
     int64_t m = (lo + hi) >> 1;
-    if (__ldg(d + m * DIRW) <= p) lo = m + 1;
+    if (ld_keep(d + m * DIRW, l2_keep_policy()) <= p) lo = m + 1;
     else hi = m;
   }
   return lo - 1;
@@ -343,12 +343,12 @@ __device__ __forceinline__ Slot slot_at_position(const GraphView& GV, bool irreg
   const int64_t* d = GV.dir + d0 * DIRW;
   if (irregular) {
     b = dir_block_of(GV, d0, nb, p);
-    cum = __ldg(d + b * DIRW + 1);
+    cum = ld_keep(d + b * DIRW + 1, l2_keep_policy());
   } else {
     b = law_block(GV.law, p);
     cum = law_cum(GV.law, b);
   }
-  return load_slot(GV.slots + __ldg(d + b * DIRW + 2) + (p - cum));
+  return load_slot(GV.slots + ld_keep(d + b * DIRW + 2, l2_keep_policy()) + (p - cum));
 }
 
 // Write pass: WGT lanes per query, RT outputs per lane (WGT * RT = 16 outputs per round)
