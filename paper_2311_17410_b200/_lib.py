@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgfb200.so")
+LIB_PATH = os.environ.get("GF_LIB_PATH") or os.path.join(HERE, "libgfb200.so")  # override for A/B builds
 
 GF_OK, GF_EINVAL, GF_ENOTFOUND, GF_ENOMEM, GF_ECUDA, GF_ERANGE, GF_EFORMAT = range(7)
 POLICY_CODE = {"recent": 0, "uniform": 1, "time_window": 2}  # wire.py:27

@@ -71,10 +71,18 @@ constexpr int64_t NREC_IRREG = 1ll << 33;
 struct SizingLaw {
   int kind;
   int64_t tau, size, m, cum_m;
+  int tau_shift, size_shift;  // log2 when a power of two, else -1 (avoids 64-bit division)
 };
 
+inline int log2_exact(int64_t x) {
+  if (x <= 0 || (x & (x - 1))) return -1;
+  int s = 0;
+  while ((1ll << s) < x) s++;
+  return s;
+}
+
 inline SizingLaw sizing_law(int kind, int64_t tau, int64_t param) {
-  SizingLaw L{kind, tau, param, 0, 0};
+  SizingLaw L{kind, tau, param, 0, 0, log2_exact(tau), log2_exact(param)};
   if (kind == GF_SIZING_ADAPTIVE) {
     int64_t b = 1;
     while ((1ll << (b - 1)) < tau) b++;

@@ -111,8 +111,8 @@ __device__ __forceinline__ void store_out(const LayerOut& O, int64_t at, const S
 
 // closed-form block index of a list position for regular lists (SizingLaw)
 __device__ __forceinline__ int64_t law_block(const SizingLaw& L, int64_t p) {
-  if (L.kind == GF_SIZING_FIXED) return p / L.size;
-  if (p >= L.cum_m) return L.m + (p - L.cum_m) / L.tau;
+  if (L.kind == GF_SIZING_FIXED) return L.size_shift >= 0 ? (p >> L.size_shift) : p / L.size;
+  if (p >= L.cum_m) return L.m + (L.tau_shift >= 0 ? ((p - L.cum_m) >> L.tau_shift) : (p - L.cum_m) / L.tau);
   return p == 0 ? 0 : 64 - __clzll(p);
 }
 
