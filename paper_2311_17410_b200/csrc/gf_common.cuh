@@ -205,26 +205,6 @@ __host__ __device__ inline uint64_t child_key(uint64_t parent, uint64_t j) {
 
 // ---- cache-policy loads (sm_100a) ------------------------------------------------
 #ifdef __CUDACC__
-// L2 policy that keeps lines (block directory, fences, node records)
-__device__ __forceinline__ uint64_t l2_keep_policy() {
-#ifdef GF_NO_KEEP_HINT
-  return 0;
-#else
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-#endif
-}
-__device__ __forceinline__ int64_t ld_keep(const int64_t* p, uint64_t pol) {
-#ifdef GF_NO_KEEP_HINT
-  (void)pol;
-  return __ldg(p);
-#else
-  int64_t v;
-  asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
-  return v;
-#endif
-}
 // one 256-bit load marked evict-first (random slot records, streaming windows); p 32-byte aligned
 __device__ __forceinline__ void ld256_stream(const void* p, int64_t& a, int64_t& b, int64_t& c, int64_t& d) {
   asm volatile("ld.global.nc.L2::evict_first.v4.b64 {%0,%1,%2,%3}, [%4];"

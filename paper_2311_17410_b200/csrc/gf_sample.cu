@@ -150,7 +150,7 @@ __device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __
   if (n > 32) {
     int c = 0;
 #pragma unroll
-    for (int j = 0; j < V; j++) c += gcount(g, ld_keep(a + (n - 32 + g.gl * V + j) * stride, l2_keep_policy()) < x);
+    for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (n - 32 + g.gl * V + j) * stride) < x);
     if (c > 0) return n - 32 + c;
     hi = n - 32;
   }
@@ -160,7 +160,7 @@ __device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __
 #pragma unroll
     for (int j = 0; j < V; j++) {
       int64_t p = lo + (int64_t)(g.gl * V + j) * step;
-      c += gcount(g, p < hi && ld_keep(a + p * stride, l2_keep_policy()) < x);
+      c += gcount(g, p < hi && __ldg(a + p * stride) < x);
     }
     if (c == 0) return lo;
     int64_t plast = lo + (int64_t)(c - 1) * step;
@@ -172,7 +172,7 @@ __device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __
 #pragma unroll
   for (int j = 0; j < V; j++) {
     int64_t p = lo + g.gl * V + j;
-    c += gcount(g, p < hi && ld_keep(a + p * stride, l2_keep_policy()) < x);
+    c += gcount(g, p < hi && __ldg(a + p * stride) < x);
   }
   return lo + c;
 }
@@ -194,7 +194,7 @@ __device__ __forceinline__ int64_t g_lower_bound_guess(const Grp& g, const int64
   ws = ws < 0 ? 0 : (ws > n - 32 ? n - 32 : ws);
   int c = 0;
 #pragma unroll
-  for (int j = 0; j < V; j++) c += gcount(g, ld_keep(a + (ws + g.gl * V + j) * stride, l2_keep_policy()) < x);
+  for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (ws + g.gl * V + j) * stride) < x);
   if (c == 32) {
     int64_t we = ws + 32;
     return we == n ? n : we + g_lower_bound(g, a + we * stride, stride, n - we, x);
@@ -234,7 +234,7 @@ struct NodeView {
 
 __device__ __forceinline__ NodeView load_node(const Grp& g, const GraphView& GV, int64_t v) {
   const int64_t* r = GV.nrec + v * NREC;
-  int64_t w = ld_keep(r + g.gl, l2_keep_policy()), w8 = ld_keep(r + 8 + g.gl, l2_keep_policy());
+  int64_t w = __ldg(r + g.gl), w8 = __ldg(r + 8 + g.gl);
   NodeView N;
   N.d0 = gbcast(g, w, 0);
   N.ns = gbcast(g, w, 1);
@@ -272,11 +272,11 @@ __device__ __forceinline__ Bnd g_list_lower_bound(const Grp& g, const GraphView&
     if (B == 0) return Bnd{N.first, -1, 0, 0};
     b = B - 1;
     const int64_t* e = d + b * DIRW;  // just probed: an L1 hit
-    tmin = ld_keep(e, l2_keep_policy());
-    cum = ld_keep(e + 1, l2_keep_policy());
-    base = ld_keep(e + 2, l2_keep_policy());
-    tmax = ld_keep(e + 3, l2_keep_policy());
-    size = (b + 1 < nt ? ld_keep(e + DIRW + 1, l2_keep_policy()) : N.tcum) - cum;
+    tmin = __ldg(e);
+    cum = __ldg(e + 1);
+    base = __ldg(e + 2);
+    tmax = __ldg(e + 3);
+    size = (b + 1 < nt ? __ldg(e + DIRW + 1) : N.tcum) - cum;
   }
   return Bnd{cum + g_block_lower_bound(g, GV, base, size, tmin, tmax, x), b, cum, base};
 }
@@ -332,7 +332,7 @@ __device__ __forceinline__ int64_t dir_block_of(const GraphView& GV, int64_t d0,
   int64_t lo = 0, hi = nb;
   while (lo < hi) {
     int64_t m = (lo + hi) >> 1;
-    if (ld_keep(d + m * DIRW, l2_keep_policy()) <= p) lo = m + 1;
+    if (__ldg(d + m * DIRW) <= p) lo = m + 1;
     else hi = m;
   }
   return lo - 1;
@@ -343,24 +343,23 @@ __device__ __forceinline__ Slot slot_at_position(const GraphView& GV, bool irreg
   const int64_t* d = GV.dir + d0 * DIRW;
   if (irregular) {
     b = dir_block_of(GV, d0, nb, p);
-    cum = ld_keep(d + b * DIRW + 1, l2_keep_policy());
+    cum = __ldg(d + b * DIRW + 1);
   } else {
     b = law_block(GV.law, p);
     cum = law_cum(GV.law, b);
   }
-  return load_slot(GV.slots + ld_keep(d + b * DIRW + 2, l2_keep_policy()) + (p - cum));
+  return load_slot(GV.slots + __ldg(d + b * DIRW + 2) + (p - cum));
 }
 
-// Write pass: WGT lanes per query, RT outputs per lane (WGT * RT = 16 outputs per round)
-template <int WGT, int RT>
+constexpr int WG = 16;  // lanes per query in the write pass: one output per lane
+
 __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q, QState S, LayerOut O) {
-  static_assert(WGT * RT == 16, "16 outputs per round");
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (WGT - 1), gbase = lane & ~(WGT - 1);
-  const unsigned mask = ((WGT == 32) ? 0xFFFFFFFFu : ((1u << WGT) - 1u)) << gbase;
+  const int gl = lane & (WG - 1), gbase = lane & WG;
+  const unsigned mask = 0xFFFFu << gbase;
   const int64_t n = query_count(Q);
-  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / WGT;
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / WGT;
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / WG;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / WG;
   for (int64_t q = gid; q < n; q += ngroups) {
     const int64_t out = O.offsets[q];
     const int64_t k = O.offsets[q + 1] - out;
@@ -370,25 +369,15 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
     if (Q.policy == GF_POLICY_RECENT || k == nv) {
       // newest first: output r is list position hi-1-r (sampling.py:188-190)
       const int64_t slot_hi = S.slot[q], inblk = hi - S.cum[q];
-      for (int64_t r0 = 0; r0 < k; r0 += WGT * RT) {
-        Slot sl[RT];
-#pragma unroll
-        for (int j = 0; j < RT; j++) {
-          int64_t r = r0 + j * WGT + gl;
-          if (r < k) {
-            if (r < inblk) {
-              sl[j] = load_slot(GV.slots + slot_hi - r);
-            } else {  // crosses into earlier blocks
-              const int64_t meta = S.meta[q];
-              sl[j] = slot_at_position(GV, (meta >> 62) & 1, S.d0[q], meta >> 32 & 0x3fffffff, hi - 1 - r);
-            }
-          }
+      for (int64_t r = gl; r < k; r += WG) {
+        Slot s;
+        if (r < inblk) {
+          s = load_slot(GV.slots + slot_hi - r);
+        } else {  // crosses into earlier blocks
+          const int64_t meta = S.meta[q];
+          s = slot_at_position(GV, (meta >> 62) & 1, S.d0[q], meta >> 32 & 0x3fffffff, hi - 1 - r);
         }
-#pragma unroll
-        for (int j = 0; j < RT; j++) {
-          int64_t r = r0 + j * WGT + gl;
-          if (r < k) store_out(O, out + r, sl[j], qkey, r);
-        }
+        store_out(O, out + r, s, qkey, r);
       }
       continue;
     }
@@ -396,41 +385,21 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
     const int64_t meta = S.meta[q], d0 = S.d0[q];
     const bool irregular = (meta >> 62) & 1;
     const int64_t nb = meta >> 32 & 0x3fffffff;
-    if (k <= WGT * RT) {
-      // draw i = j * WGT + gl
-      int64_t t[RT], sel[RT];
-#pragma unroll
-      for (int j = 0; j < RT; j++) {
-        int64_t i = j * WGT + gl;
-        t[j] = 0;
-        sel[j] = -1;
-        if (i < k) {
-          uint32_t c[4] = {(uint32_t)(i >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
-          philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
-          uint64_t r = (i & 1) ? ((uint64_t)c[2] | ((uint64_t)c[3] << 32)) : ((uint64_t)c[0] | ((uint64_t)c[1] << 32));
-          t[j] = (int64_t)bounded64(r, (uint64_t)(nv - k + i + 1));
-        }
+    if (k <= WG) {
+      int64_t t = 0, sel = -1;
+      if (gl < k) {
+        // draw i = gl: lanes 2m and 2m+1 evaluate the same Philox block
+        uint32_t c[4] = {(uint32_t)(gl >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+        philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
+        uint64_t r = (gl & 1) ? ((uint64_t)c[2] | ((uint64_t)c[3] << 32)) : ((uint64_t)c[0] | ((uint64_t)c[1] << 32));
+        t = (int64_t)bounded64(r, (uint64_t)(nv - k + gl + 1));
       }
-#pragma unroll
-      for (int i = 0; i < WGT * RT; i++) {
-        if (i < k) {
-          int64_t ti = __shfl_sync(mask, t[i / WGT], gbase + (i % WGT));
-          bool dup = false;
-#pragma unroll
-          for (int j = 0; j < RT; j++) dup |= (j * WGT + gl < i) && sel[j] == ti;
-          dup = (__ballot_sync(mask, dup) & mask) != 0;
-          if (gl == i % WGT) sel[i / WGT] = dup ? (nv - k + i) : ti;
-        }
+      for (int i = 0; i < (int)k; i++) {
+        int64_t ti = __shfl_sync(mask, t, gbase + i);
+        bool dup = (__ballot_sync(mask, gl < i && sel == ti) & mask) != 0;
+        if (gl == i) sel = dup ? (nv - k + i) : ti;
       }
-      Slot sl[RT];
-#pragma unroll
-      for (int j = 0; j < RT; j++)
-        if (j * WGT + gl < k) sl[j] = slot_at_position(GV, irregular, d0, nb, lo + sel[j]);
-#pragma unroll
-      for (int j = 0; j < RT; j++) {
-        int64_t i = j * WGT + gl;
-        if (i < k) store_out(O, out + i, sl[j], qkey, i);
-      }
+      if (gl < k) store_out(O, out + gl, slot_at_position(GV, irregular, d0, nb, lo + sel), qkey, gl);
       continue;
     }
     // large fanout: keep the Floyd set in the output's eid column while drawing
@@ -443,7 +412,7 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
       int64_t j = nv - k + i;
       int64_t ti = (int64_t)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
       bool dup = false;
-      for (int64_t c0 = 0; c0 < i; c0 += WGT) {
+      for (int64_t c0 = 0; c0 < i; c0 += WG) {
         int64_t c = c0 + gl;
         if (__ballot_sync(mask, c < i && setv[c] == ti) & mask) dup = true;
       }
@@ -451,7 +420,7 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
       if (gl == 0) setv[i] = dup ? j : ti;
       __syncwarp(mask);
     }
-    for (int64_t i0 = 0; i0 < k; i0 += WGT) {
+    for (int64_t i0 = 0; i0 < k; i0 += WG) {
       int64_t i = i0 + gl;
       int64_t rk = (i < k) ? setv[i] : -1;
       __syncwarp(mask);
@@ -688,12 +657,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
   if (e0) prof_stop("cub_scan_offsets", s, e0);
   GF_LAUNCH(k_total, 1, 1, 0, s, d_offsets, Q.n_dev, Q.n, total);
-  if (fast) {
-    static const int wg = getenv("GF_WRITE_LANES") ? atoi(getenv("GF_WRITE_LANES")) : 8;
-    if (wg == 16) GF_LAUNCH((k_write_fast<16, 1>), grid_for_queries(cap_q, 16), THREADS, 0, s, GV, Q, S, O);
-    else if (wg == 4) GF_LAUNCH((k_write_fast<4, 4>), grid_for_queries(cap_q, 4), THREADS, 0, s, GV, Q, S, O);
-    else GF_LAUNCH((k_write_fast<8, 2>), grid_for_queries(cap_q, 8), THREADS, 0, s, GV, Q, S, O);
-  }
+  if (fast) GF_LAUNCH(k_write_fast, grid_for_queries(cap_q, WG), THREADS, 0, s, GV, Q, S, O);
   if (!fast) GF_LAUNCH(k_write_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, O);
   return GF_OK;
 }
