@@ -183,29 +183,17 @@ def build_graph(cfg, src, dst, ts, world, rank, device):
     slots = n * (1 if cfg["directed"] else 2)
     g.reserve(cfg["nodes"], cfg["nodes"] * 16 + slots // max(1, cfg["tau"]) + 1024,
               slots + min(cfg["nodes"] * cfg["tau"], slots // 2))
-    if world > 1:
-        import torch.distributed as dist
+    from paper_2311_17410_b200.distributed import ReplicatedGraph, shard_range
+
+    rg = ReplicatedGraph(g)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for lo in range(0, n, INGEST_BATCH):
         hi = min(n, lo + INGEST_BATCH)
-        if world > 1:
-            b = hi - lo
-            per = (b + world - 1) // world
-            pad = per * world
-            shard = torch.zeros((3, per), dtype=torch.int64, device=device)
-            s_lo, s_hi = lo + rank * per, min(hi, lo + (rank + 1) * per)
-            if s_hi > s_lo:
-                shard[0, : s_hi - s_lo] = src[s_lo:s_hi]
-                shard[1, : s_hi - s_lo] = dst[s_lo:s_hi]
-                shard[2, : s_hi - s_lo] = ts[s_lo:s_hi]
-            full = torch.empty((world, 3, per), dtype=torch.int64, device=device)
-            dist.all_gather_into_tensor(full, shard)
-            batch = full.permute(1, 0, 2).reshape(3, pad)[:, :b]
-            g.add_edges_arrays(batch[0].contiguous(), batch[1].contiguous(), batch[2].contiguous())
-        else:
-            g.add_edges_arrays(src[lo:hi], dst[lo:hi], ts[lo:hi])
+        # this rank's shard of the batch; N>1 all-gathers the shards (NCCL) before K1
+        a, b = shard_range(hi - lo, world, rank)
+        rg.ingest(src[lo + a:lo + b], dst[lo + a:lo + b], ts[lo + a:lo + b])
     e1.record()
     torch.cuda.synchronize()
     return g, e0.elapsed_time(e1)

@@ -1,0 +1,105 @@
+"""Multi-GPU replicated mode: one process per GPU, full graph replica per rank.
+
+* Ingest: each rank holds a shard of the new edge batch; ``gather_edge_batch``
+  all-gathers the shards (NCCL over NVLink on GPUs, gloo on CPU) into the
+  global batch in rank order, and every rank appends it with the same
+  deterministic K1 -- replicas stay identical (block handles are assigned by
+  scan, not atomics).
+* Sampling: each rank samples its own root shard.  ``root_key_base`` places
+  the shard in the global root order (an exclusive prefix of per-rank root
+  counts -- one integer per rank, not a data-path collective), so the union of
+  the ranks' samples equals a single-GPU sample of all roots bit for bit
+  (query keys are root_key_base + i and path-derived below that).
+* No collective on the sampling path; the reference's distributed sampler
+  reaches the same invariance with its content-keyed RNG (sampling.py:140-142,
+  cluster.py:226-292).
+"""
+
+from __future__ import annotations
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def world() -> tuple[int, int]:
+    dist = _dist()
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(), dist.get_rank()
+
+
+def exclusive_prefix(count: int, device=None) -> tuple[int, int]:
+    """(sum of counts on lower ranks, global total) for this rank's count."""
+    import torch
+
+    n, r = world()
+    if n == 1:
+        return 0, int(count)
+    dist = _dist()
+    t = torch.tensor([int(count)], dtype=torch.int64, device=device)
+    allc = [torch.zeros_like(t) for _ in range(n)]
+    dist.all_gather(allc, t)
+    vals = [int(x.item()) for x in allc]
+    return sum(vals[:r]), sum(vals)
+
+
+def gather_edge_batch(src, dst, ts):
+    """All-gather per-rank edge shards into the global batch (rank order).
+
+    Shards may have different lengths: lengths are exchanged first and the
+    shards padded to the longest one for a single all_gather_into_tensor.
+    """
+    import torch
+
+    n, r = world()
+    if n == 1:
+        return src, dst, ts
+    dist = _dist()
+    dev = src.device
+    local = torch.stack([src.to(torch.int64), dst.to(torch.int64), ts.to(torch.int64)])  # [3, m]
+    m = torch.tensor([local.shape[1]], dtype=torch.int64, device=dev)
+    lens = [torch.zeros_like(m) for _ in range(n)]
+    dist.all_gather(lens, m)
+    lens = [int(x.item()) for x in lens]
+    per = max(lens)
+    pad = torch.zeros((3, per), dtype=torch.int64, device=dev)
+    pad[:, : local.shape[1]] = local
+    full = torch.empty((n, 3, per), dtype=torch.int64, device=dev)
+    if hasattr(dist, "all_gather_into_tensor") and dev.type == "cuda":
+        dist.all_gather_into_tensor(full, pad)
+    else:
+        parts = [torch.empty_like(pad) for _ in range(n)]
+        dist.all_gather(parts, pad)
+        full = torch.stack(parts)
+    cols = [full[i, :, : lens[i]] for i in range(n)]
+    batch = torch.cat(cols, dim=1)
+    return batch[0].contiguous(), batch[1].contiguous(), batch[2].contiguous()
+
+
+def shard_range(total: int, n: int, r: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) slice of `total` items for rank r of n."""
+    per = (total + n - 1) // n
+    lo = min(total, r * per)
+    return lo, min(total, lo + per)
+
+
+class ReplicatedGraph:
+    """A DynamicGraph replica per rank with all-gather ingest and sharded sampling."""
+
+    def __init__(self, graph):
+        self.graph = graph
+
+    def ingest(self, src, dst, ts):
+        """Append this rank's shard of a new batch; every rank applies the whole batch."""
+        s, d, t = gather_edge_batch(src, dst, ts)
+        return self.graph.add_edges_arrays(s, d, t)
+
+    def sample(self, roots, ts, fanouts, strategy="recent", delta=0, seed=0):
+        """Sample this rank's root shard; keys are positioned in the global root order."""
+        from .sampling import TemporalSampler
+
+        base, _ = exclusive_prefix(int(roots.numel()), device=roots.device)
+        return TemporalSampler(self.graph, fanouts, strategy, delta, seed).sample(roots, ts, root_key_base=base)
