@@ -430,6 +430,121 @@ __global__ void __launch_bounds__(THREADS) k_write_fast(GraphView GV, QueryIn Q,
   }
 }
 
+// Write pass for fanout <= KMAX: one lane per query selects its k slots
+// (recent: the k newest positions; uniform: Philox draws + Floyd, in
+// registers), then the warp moves the 32 queries' outputs cooperatively:
+// output e of the warp's contiguous output range is handled by lane e % 32,
+// so slot loads have 32 independent addresses in flight and every store
+// instruction writes 32 consecutive int64s.
+constexpr int KMAX = 16;
+
+__global__ void __launch_bounds__(THREADS) k_write_coop(GraphView GV, QueryIn Q, QState S, LayerOut O) {
+  __shared__ uint32_t s_sel[THREADS / 32][32][KMAX];  // pool index of every selected slot
+  __shared__ uint8_t s_owner[THREADS / 32][32 * KMAX];
+  __shared__ uint64_t s_key[THREADS / 32][32];
+  __shared__ int32_t s_pre[THREADS / 32][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t n = query_count(Q);
+  const int64_t nchunks = (n + 31) / 32;
+  for (int64_t chunk = blockIdx.x * (int64_t)(THREADS / 32) + w; chunk < nchunks;
+       chunk += (int64_t)gridDim.x * (THREADS / 32)) {
+    const int64_t q = chunk * 32 + lane;
+    int k = 0;
+    int64_t out = 0;
+    if (q < n) {
+      out = O.offsets[q];
+      k = (int)(O.offsets[q + 1] - out);
+    }
+    if (k > 0) {
+      const int64_t lo = S.lo[q], hi = S.hi[q], nv = hi - lo;
+      const uint64_t qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
+      s_key[w][lane] = qkey;
+      if (Q.policy == GF_POLICY_RECENT || k == nv) {
+        // newest first: output r is list position hi-1-r (sampling.py:188-190)
+        const int64_t slot_hi = S.slot[q], inblk = hi - S.cum[q];
+#pragma unroll
+        for (int r = 0; r < KMAX; r++) {
+          if (r < k) {
+            int64_t sl;
+            if (r < inblk) {
+              sl = slot_hi - r;
+            } else {  // crosses into earlier blocks (short lists)
+              const int64_t meta = S.meta[q], d0 = S.d0[q], nb = meta >> 32 & 0x3fffffff;
+              const int64_t p = hi - 1 - r;
+              const int64_t b = dir_block_of(GV, d0, nb, p);
+              const int64_t* e = GV.dir + (d0 + b) * DIRW;
+              sl = __ldg(e + 2) + (p - __ldg(e + 1));
+            }
+            s_sel[w][lane][r] = (uint32_t)sl;
+          }
+        }
+      } else {
+        // uniform / time_window (k < nv): Floyd over candidate indices 0..nv-1,
+        // draws t_i in [0, nv-k+i] from Philox block i/2 (two draws per block)
+        int32_t pick[KMAX];
+#pragma unroll
+        for (int i = 0; i < KMAX; i += 2) {
+          if (i < k) {
+            uint32_t c[4] = {(uint32_t)(i >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+            philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
+            int64_t t0 = (int64_t)bounded64((uint64_t)c[0] | ((uint64_t)c[1] << 32), (uint64_t)(nv - k + i + 1));
+            bool dup0 = false;
+#pragma unroll
+            for (int j = 0; j < KMAX; j++) dup0 |= (j < i) && pick[j] == (int32_t)t0;
+            pick[i] = dup0 ? (int32_t)(nv - k + i) : (int32_t)t0;
+            if (i + 1 < k) {
+              int64_t t1 = (int64_t)bounded64((uint64_t)c[2] | ((uint64_t)c[3] << 32), (uint64_t)(nv - k + i + 2));
+              bool dup1 = false;
+#pragma unroll
+              for (int j = 0; j < KMAX; j++) dup1 |= (j < i + 1) && pick[j] == (int32_t)t1;
+              pick[i + 1] = dup1 ? (int32_t)(nv - k + i + 1) : (int32_t)t1;
+            }
+          }
+        }
+        const int64_t meta = S.meta[q], d0 = S.d0[q];
+        const bool irregular = (meta >> 62) & 1;
+        const int64_t nb = meta >> 32 & 0x3fffffff;
+        const int64_t* dd = GV.dir + d0 * DIRW;
+#pragma unroll
+        for (int i = 0; i < KMAX; i++) {
+          if (i < k) {
+            const int64_t p = lo + pick[i];
+            int64_t b, cum;
+            if (irregular) {
+              b = dir_block_of(GV, d0, nb, p);
+              cum = __ldg(dd + b * DIRW + 1);
+            } else {
+              b = law_block(GV.law, p);
+              cum = law_cum(GV.law, b);
+            }
+            s_sel[w][lane][i] = (uint32_t)(__ldg(dd + b * DIRW + 2) + (p - cum));
+          }
+        }
+      }
+    }
+    // warp scan of the counts: the 32 queries' outputs are one contiguous range
+    int incl = k;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int pre = incl - k;
+    s_pre[w][lane] = pre;
+    for (int i = 0; i < k; i++) s_owner[w][pre + i] = (uint8_t)lane;
+    const int64_t out0 = __shfl_sync(0xffffffffu, out, 0);  // outputs of the chunk start at offsets[chunk * 32]
+    __syncwarp();
+    for (int e = lane; e < total; e += 32) {
+      const int j = s_owner[w][e];
+      const int i = e - s_pre[w][j];
+      const Slot s = load_slot(GV.slots + s_sel[w][j][i]);
+      store_out(O, out0 + e, s, s_key[w][j], i);
+    }
+    __syncwarp();
+  }
+}
+
 // ========================== general path (deletions) =========================
 
 __device__ __forceinline__ bool node_ok(const GraphView& G_, int64_t v) {
@@ -657,7 +772,10 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
   if (e0) prof_stop("cub_scan_offsets", s, e0);
   GF_LAUNCH(k_total, 1, 1, 0, s, d_offsets, Q.n_dev, Q.n, total);
-  if (fast) GF_LAUNCH(k_write_fast, grid_for_queries(cap_q, WG), THREADS, 0, s, GV, Q, S, O);
+  if (fast && Q.fanout <= KMAX && g->slot_cap < (1ll << 32))
+    GF_LAUNCH(k_write_coop, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, O);
+  else if (fast)
+    GF_LAUNCH(k_write_fast, grid_for_queries(cap_q, WG), THREADS, 0, s, GV, Q, S, O);
   if (!fast) GF_LAUNCH(k_write_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, O);
   return GF_OK;
 }
