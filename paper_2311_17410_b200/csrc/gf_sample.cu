@@ -29,6 +29,8 @@
 // sampling.py:178).
 #include <cub/cub.cuh>
 
+#include <string.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -279,6 +281,170 @@ __device__ __forceinline__ Bnd g_list_lower_bound(const Grp& g, const GraphView&
     size = (b + 1 < nt ? __ldg(e + DIRW + 1) : N.tcum) - cum;
   }
   return Bnd{cum + g_block_lower_bound(g, GV, base, size, tmin, tmax, x), b, cum, base};
+}
+
+// ===================== lane-per-query window search ==========================
+// One thread per query: every search step is a single dependent load, but 32
+// queries per warp are in flight, and interpolation (timestamps are the
+// search keys) keeps the number of steps small.  Directory entries and
+// 4-timestamp groups are read with one 256-bit load each.
+
+__device__ __forceinline__ void ld256(const void* p, int64_t& a, int64_t& b, int64_t& c, int64_t& d) {
+  asm volatile("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+
+// interpolated probe index strictly inside (lo, hi) for key x with known
+// neighbour keys tl < x <= th
+__device__ __forceinline__ int64_t probe_between(int64_t lo, int64_t hi, int64_t x, int64_t tl, int64_t th, int step) {
+  if (step >= 2 || th <= tl) return (lo + hi) >> 1;  // interpolation twice, then bisection
+  float f = __fdividef((float)(x - tl), (float)(th - tl));
+  int64_t g = lo + 1 + (int64_t)(f * (float)(hi - lo - 1));
+  return g <= lo ? lo + 1 : (g >= hi ? hi - 1 : g);
+}
+
+// count of timestamps < x in sts[base, base + size) whose values lie in [t0, t1]
+__device__ __forceinline__ int64_t lane_block_lower_bound(const GraphView& GV, int64_t base, int64_t size, int64_t t0,
+                                                          int64_t t1, int64_t x) {
+  int64_t seg_lo = base, seg_hi = base + size;
+  if (size > FENCE) {
+    const int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;
+    // fences f0..f1 are sorted; find j = #fences < x by interpolation + bisection
+    int64_t lo = f0 - 1, hi = f1 + 1;  // virtual fences: fts[lo] < x <= fts[hi]
+    int64_t tl = t0 - 1, th = t1 + 1;
+    if (x > t1) {
+      lo = f1;
+    } else {
+      for (int step = 0; hi - lo > 1; step++) {
+        int64_t g = probe_between(lo, hi, x, tl, th, step);
+        int64_t v = __ldg(GV.fts + g);
+        if (v < x) {
+          lo = g;
+          tl = v;
+        } else {
+          hi = g;
+          th = v;
+        }
+      }
+    }
+    const int64_t j = lo - (f0 - 1);  // fences < x
+    if (j == 0) {
+      seg_hi = f0 * FENCE;  // head part before the first fence (< 32 slots): bisection below
+    } else {
+      seg_lo = (f0 + j - 1) * FENCE;
+      seg_hi = min(seg_lo + FENCE, base + size);
+      // seg_lo is 256-byte aligned here: eight 256-bit loads cover the window
+      int64_t c = 0;
+#pragma unroll
+    for (int w = 0; w < FENCE; w += 4) {
+      if (seg_lo + w < seg_hi) {
+        int64_t a, b, cc, d;
+        ld256(GV.sts + seg_lo + w, a, b, cc, d);
+        c += (a < x) + (seg_lo + w + 1 < seg_hi && b < x) + (seg_lo + w + 2 < seg_hi && cc < x) +
+             (seg_lo + w + 3 < seg_hi && d < x);
+      }
+    }
+      return seg_lo - base + c;
+    }
+  }
+  // short block or head segment: bisection over at most 32 timestamps
+  int64_t lo = seg_lo, hi = seg_hi;
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (__ldg(GV.sts + m) < x) lo = m + 1;
+    else hi = m;
+  }
+  return lo - base;
+}
+
+struct LaneNode {
+  int64_t d0, ns, nb, first, tcum, tbase, ttmin, tmax, htmin;
+  bool valid, irregular;
+};
+
+struct LaneBnd {
+  int64_t pos, cum, base;  // boundary; block holding pos-1: its first position and slot base
+};
+
+__device__ __forceinline__ LaneBnd lane_list_lower_bound(const GraphView& GV, const LaneNode& N, int64_t x) {
+  if (N.htmin >= x) return LaneBnd{N.first, 0, 0};  // every block starts at or after x
+  int64_t cum, base, size, t0, t1;
+  if (N.ttmin < x) {  // boundary in the tail block
+    cum = N.tcum;
+    base = N.tbase;
+    size = N.ns - N.tcum;
+    t0 = N.ttmin;
+    t1 = N.tmax;
+  } else {
+    // last non-tail block with tmin < x: entries lo < b < hi, tmin[lo] < x <= tmin[hi]
+    const int64_t* d = GV.dir + N.d0 * DIRW;
+    int64_t lo = 0, hi = N.nb - 1, tl = N.htmin, th = N.ttmin;
+    int64_t lo_e1 = -1, lo_e2 = 0, lo_e3 = 0, hi_cum = N.tcum;  // cum/base/tmax of lo, cum of hi
+    for (int step = 0; hi - lo > 1; step++) {
+      int64_t g = probe_between(lo, hi, x, tl, th, step);
+      int64_t e0, e1, e2, e3;
+      ld256(d + g * DIRW, e0, e1, e2, e3);
+      if (e0 < x) {
+        lo = g;
+        tl = e0;
+        lo_e1 = e1;
+        lo_e2 = e2;
+        lo_e3 = e3;
+      } else {
+        hi = g;
+        th = e0;
+        hi_cum = e1;
+      }
+    }
+    if (lo_e1 < 0) {  // entry lo (= 0) was never probed
+      int64_t e0;
+      ld256(d + lo * DIRW, e0, lo_e1, lo_e2, lo_e3);
+    }
+    cum = lo_e1;
+    base = lo_e2;
+    t0 = tl;
+    t1 = lo_e3;
+    size = hi_cum - cum;
+  }
+  return LaneBnd{cum + lane_block_lower_bound(GV, base, size, t0, t1, x), cum, base};
+}
+
+__global__ void __launch_bounds__(THREADS) k_count_lane(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
+  const int64_t n = query_count(Q);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cap_q; q += (int64_t)gridDim.x * blockDim.x) {
+    if (q >= n) {
+      counts[q] = 0;
+      continue;
+    }
+    const int64_t v = Q.src[q];
+    const int64_t te = Q.t_end[q];
+    int64_t k = 0;
+    if (v >= 0 && v < GV.num_nodes) {
+      const int64_t* r = GV.nrec + v * NREC;
+      LaneNode N;
+      int64_t w2, w3;
+      ld256(r, N.d0, N.ns, w2, N.first);
+      ld256(r + 4, N.tcum, N.tbase, N.ttmin, N.tmax);
+      ld256(r + 8, N.htmin, w3, w3, w3);
+      N.nb = w2 & 0xffffffffll;
+      N.valid = (w2 & NREC_VALID) != 0;
+      N.irregular = (w2 & NREC_IRREG) != 0;
+      if (N.valid && N.nb > 0) {  // sampling.py:153-155
+        const LaneBnd h = lane_list_lower_bound(GV, N, te);
+        const int64_t tsr = t_start_of(Q, q, te);
+        const int64_t lo = (tsr == GF_TS_MIN) ? N.first : lane_list_lower_bound(GV, N, tsr).pos;
+        if (h.pos > lo) {
+          k = min(h.pos - lo, Q.fanout);
+          S.lo[q] = lo;
+          S.hi[q] = h.pos;
+          S.slot[q] = h.base + (h.pos - 1 - h.cum);
+          S.cum[q] = h.cum;
+          S.d0[q] = N.d0;
+          S.meta[q] = (N.nb << 32) | (N.irregular ? (1ll << 62) : 0);
+        }
+      }
+    }
+    counts[q] = k;
+  }
 }
 
 __global__ void __launch_bounds__(THREADS, 4) k_count_fast(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
@@ -766,7 +932,9 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   int64_t* counts = A.take<int64_t>(cap_q);
   GraphView GV = view_of(g);
   const bool fast = !g->any_deleted;
-  if (fast) GF_LAUNCH(k_count_fast, grid_for_queries(cap_q, G), THREADS, 0, s, GV, Q, S, counts, cap_q);
+  static const bool group_count = getenv("GF_COUNT") && !strcmp(getenv("GF_COUNT"), "group");
+  if (fast && !group_count) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
+  else if (fast) GF_LAUNCH(k_count_fast, grid_for_queries(cap_q, G), THREADS, 0, s, GV, Q, S, counts, cap_q);
   else GF_LAUNCH(k_count_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, counts, cap_q);
   cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
