@@ -308,7 +308,7 @@ def bench_ours(args, cfg, world, rank, local):
         tag = name[len(raw) + 1:-1] if "[" in name else None
         base = re.sub(r"[()]|<.*>", "", raw).strip()
         ent = {"launches": cnt, "ms": round(kms, 4), "share": round(kms / tot_ms, 4) if tot_ms else None}
-        if tag in layer_qs and base in ("k_count_fast", "k_write_fast", "k_count_general", "k_write_general"):
+        if tag in layer_qs and (base.startswith("k_count") or base.startswith("k_write")):
             q_l, s_l = layer_qs[tag]
             b = BYTES_PER_QUERY * q_l if base.startswith("k_count") else BYTES_PER_EDGE * s_l
             ent["alg_bytes"] = b
@@ -319,8 +319,7 @@ def bench_ours(args, cfg, world, rank, local):
     dom_name = max(base_bytes, key=lambda k: base_ms[k])
     achieved = base_bytes[dom_name] / (base_ms[dom_name] / 1e3) / 1e9
     traffic = load_traffic().get(dom_name)
-    pipe_ms = sum(base_ms.get(k, 0.0) for k in ("k_count_fast", "k_write_fast", "k_count_general", "k_write_general",
-                                                 "k_total", "cub_scan_offsets"))
+    pipe_ms = sum(v for k, v in base_ms.items() if k.startswith(("k_count", "k_write", "k_total", "cub_scan")))
     pipe_gbs = (BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p) / (pipe_ms / 1e3) / 1e9 if pipe_ms else None
 
     # e2e through the public API with host (pinned) buffers: H2D roots, sample, D2H every layer
