@@ -7,12 +7,13 @@
 // rejects out-of-order edges), so the in-window candidates of a query are one
 // contiguous run [lo, hi) of list positions.  Finding hi replaces the
 // reference's tail->head block walk with block skipping (sampling.py:157-172):
-//   1. the node's 64-byte NodeRec (one load) -- if the tail block's tmin is
-//      below t_end the boundary is in the tail block (the common case for
-//      recent roots), else a 32-ary search over the node's block directory;
-//   2. a 32-ary search over the block's fence index (every 32nd timestamp,
-//      L2-resident), newest fences probed first;
-//   3. one 32-timestamp window of the dense ts array.
+//   1. the node's 128-byte NodeRec -- if the tail block's tmin is below
+//      t_end the boundary is in the tail block (the common case for recent
+//      roots), else an interpolation/bisection search over the node's block
+//      directory (32-byte entries, one 256-bit load per probe);
+//   2. the same search over the block's fence index (every 32nd timestamp,
+//      L2-sized);
+//   3. one 32-timestamp window of the dense ts array (eight 256-bit loads).
 // Selection:
 //   recent:     the k newest valid candidates, newest first (sampling.py:188-190) -- bit-exact.
 //   uniform/tw: k distinct candidates by Floyd's algorithm on a Philox4x32-10 stream
@@ -22,11 +23,12 @@
 // on the device so a k-hop call is a fixed launch sequence with one host
 // synchronisation at the end.
 //
-// Fast path (no deletions ever applied): 8-lane groups, 4 queries in flight
-// per warp; each lane issues 4 independent loads per search step, so a group
-// still performs 32-ary searches.  General path (after deletions): one warp
-// per query, scanning candidate validity (valid edge and valid neighbour,
-// sampling.py:178).
+// Fast path (no deletions ever applied): the window search runs one query per
+// lane (32 in flight per warp; interpolation on timestamps keeps the chain of
+// dependent loads short); the write pass selects per lane and moves the
+// selected slots warp-cooperatively (coalesced stores).  General path (after
+// deletions): one warp per query, scanning candidate validity (valid edge and
+// valid neighbour, sampling.py:178).
 #include <cub/cub.cuh>
 
 #include <string.h>
@@ -41,8 +43,6 @@ using namespace gf;
 namespace {
 
 constexpr int THREADS = 256;
-constexpr int G = 8;   // lanes per query group (fast path)
-constexpr int V = 4;   // loads per lane per search step: G * V = 32-ary search
 
 struct QueryIn {
   const int64_t* src;
@@ -116,171 +116,6 @@ __device__ __forceinline__ int64_t law_block(const SizingLaw& L, int64_t p) {
   if (L.kind == GF_SIZING_FIXED) return L.size_shift >= 0 ? (p >> L.size_shift) : p / L.size;
   if (p >= L.cum_m) return L.m + (L.tau_shift >= 0 ? ((p - L.cum_m) >> L.tau_shift) : (p - L.cum_m) / L.tau);
   return p == 0 ? 0 : 64 - __clzll(p);
-}
-
-// ============================ group-of-8 fast path ===========================
-
-struct Grp {
-  int gl;          // lane within the group
-  int gbase;       // first lane of the group
-  unsigned mask;   // group lanes
-};
-
-__device__ __forceinline__ Grp make_grp() {
-  int lane = threadIdx.x & 31;
-  Grp g;
-  g.gl = lane & (G - 1);
-  g.gbase = lane & ~(G - 1);
-  g.mask = ((1u << G) - 1) << g.gbase;
-  return g;
-}
-
-__device__ __forceinline__ int gcount(const Grp& g, bool p) {
-  return __popc(__ballot_sync(g.mask, p) & g.mask);
-}
-
-template <class T>
-__device__ __forceinline__ T gbcast(const Grp& g, T v, int src) {
-  return __shfl_sync(g.mask, v, g.gbase + src);
-}
-
-// number of elements < x in the sorted a[0], a[stride], ..., a[(n-1)*stride];
-// 32 probes per step (V loads per lane), the newest 32 first
-__device__ __forceinline__ int64_t g_lower_bound(const Grp& g, const int64_t* __restrict__ a, int64_t stride, int64_t n,
-                                                 int64_t x) {
-  int64_t lo = 0, hi = n;
-  if (n > 32) {
-    int c = 0;
-#pragma unroll
-    for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (n - 32 + g.gl * V + j) * stride) < x);
-    if (c > 0) return n - 32 + c;
-    hi = n - 32;
-  }
-  while (hi - lo > 32) {
-    int64_t step = (hi - lo + 31) / 32;
-    int c = 0;
-#pragma unroll
-    for (int j = 0; j < V; j++) {
-      int64_t p = lo + (int64_t)(g.gl * V + j) * step;
-      c += gcount(g, p < hi && __ldg(a + p * stride) < x);
-    }
-    if (c == 0) return lo;
-    int64_t plast = lo + (int64_t)(c - 1) * step;
-    int64_t nh = plast + step;
-    lo = plast + 1;
-    if (nh < hi) hi = nh;
-  }
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < V; j++) {
-    int64_t p = lo + g.gl * V + j;
-    c += gcount(g, p < hi && __ldg(a + p * stride) < x);
-  }
-  return lo + c;
-}
-
-// index guess for x in a sorted run spanning times [t0, t1] with n entries
-__device__ __forceinline__ int64_t interp_guess(int64_t x, int64_t t0, int64_t t1, int64_t n) {
-  if (x <= t0) return 0;
-  if (x > t1) return n;
-  double f = ((double)x - (double)t0) / ((double)t1 - (double)t0 + 1.0);
-  return (int64_t)(f * (double)n);
-}
-
-// g_lower_bound that first probes the 32 entries around `guess` (interpolation),
-// falling back to the galloping search on the side the window rules out
-__device__ __forceinline__ int64_t g_lower_bound_guess(const Grp& g, const int64_t* __restrict__ a, int64_t stride,
-                                                       int64_t n, int64_t x, int64_t guess) {
-  if (n <= 32) return g_lower_bound(g, a, stride, n, x);
-  int64_t ws = guess - 16;
-  ws = ws < 0 ? 0 : (ws > n - 32 ? n - 32 : ws);
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < V; j++) c += gcount(g, __ldg(a + (ws + g.gl * V + j) * stride) < x);
-  if (c == 32) {
-    int64_t we = ws + 32;
-    return we == n ? n : we + g_lower_bound(g, a + we * stride, stride, n - we, x);
-  }
-  if (c == 0) return ws == 0 ? 0 : g_lower_bound(g, a, stride, ws, x);
-  return ws + c;
-}
-
-// timestamps < x inside a block whose slots are sts[base, base + size) and whose
-// timestamps span [tmin, tmax]
-__device__ __forceinline__ int64_t g_block_lower_bound(const Grp& g, const GraphView& GV, int64_t base, int64_t size,
-                                                       int64_t tmin, int64_t tmax, int64_t x) {
-  int64_t seg_lo = base, seg_hi = base + size;
-  if (size > FENCE) {
-    int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE, nf = f1 - f0 + 1;
-    int64_t j = g_lower_bound_guess(g, GV.fts + f0, 1, nf, x, interp_guess(x, tmin, tmax, nf));
-    if (j == 0) {
-      seg_hi = f0 * FENCE;
-    } else {
-      seg_lo = (f0 + j - 1) * FENCE;
-      seg_hi = min(seg_lo + FENCE, base + size);
-    }
-  }
-  int c = 0;  // window of <= 32 timestamps
-#pragma unroll
-  for (int j = 0; j < V; j++) {
-    int64_t p = seg_lo + g.gl * V + j;
-    c += gcount(g, p < seg_hi && __ldg(GV.sts + p) < x);
-  }
-  return seg_lo - base + c;
-}
-
-struct NodeView {
-  int64_t d0, ns, nb, first, tcum, tbase, ttmin, tmax, htmin;
-  bool valid, irregular;
-};
-
-__device__ __forceinline__ NodeView load_node(const Grp& g, const GraphView& GV, int64_t v) {
-  const int64_t* r = GV.nrec + v * NREC;
-  int64_t w = __ldg(r + g.gl), w8 = __ldg(r + 8 + g.gl);
-  NodeView N;
-  N.d0 = gbcast(g, w, 0);
-  N.ns = gbcast(g, w, 1);
-  int64_t w2 = gbcast(g, w, 2);
-  N.first = gbcast(g, w, 3);
-  N.tcum = gbcast(g, w, 4);
-  N.tbase = gbcast(g, w, 5);
-  N.ttmin = gbcast(g, w, 6);
-  N.tmax = gbcast(g, w, 7);
-  N.htmin = gbcast(g, w8, 0);
-  N.nb = w2 & 0xffffffffll;
-  N.valid = (w2 & NREC_VALID) != 0;
-  N.irregular = (w2 & NREC_IRREG) != 0;
-  return N;
-}
-
-struct Bnd {
-  int64_t pos, blk, cum, base;  // boundary position; block holding pos-1 with its cum/base
-};
-
-__device__ __forceinline__ Bnd g_list_lower_bound(const Grp& g, const GraphView& GV, const NodeView& N, int64_t x) {
-  int64_t b, cum, base, size, tmin, tmax;
-  if (N.ttmin < x) {  // boundary inside the tail block
-    b = N.nb - 1;
-    cum = N.tcum;
-    base = N.tbase;
-    size = N.ns - N.tcum;
-    tmin = N.ttmin;
-    tmax = N.tmax;
-  } else {
-    // non-tail blocks with tmin < x (directory entries are DIRW words, tmin first)
-    const int64_t* d = GV.dir + N.d0 * DIRW;
-    int64_t nt = N.nb - 1;
-    int64_t B = g_lower_bound_guess(g, d, DIRW, nt, x, interp_guess(x, N.htmin, N.ttmin, nt));
-    if (B == 0) return Bnd{N.first, -1, 0, 0};
-    b = B - 1;
-    const int64_t* e = d + b * DIRW;  // just probed: an L1 hit
-    tmin = __ldg(e);
-    cum = __ldg(e + 1);
-    base = __ldg(e + 2);
-    tmax = __ldg(e + 3);
-    size = (b + 1 < nt ? __ldg(e + DIRW + 1) : N.tcum) - cum;
-  }
-  return Bnd{cum + g_block_lower_bound(g, GV, base, size, tmin, tmax, x), b, cum, base};
 }
 
 // ===================== lane-per-query window search ==========================
@@ -444,43 +279,6 @@ __global__ void __launch_bounds__(THREADS) k_count_lane(GraphView GV, QueryIn Q,
       }
     }
     counts[q] = k;
-  }
-}
-
-__global__ void __launch_bounds__(THREADS, 4) k_count_fast(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
-  const Grp g = make_grp();
-  const int64_t n = query_count(Q);
-  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
-  for (int64_t q = gid; q < cap_q; q += ngroups) {
-    if (q >= n) {
-      if (g.gl == 0) counts[q] = 0;
-      continue;
-    }
-    int64_t v = Q.src[q];
-    int64_t te = Q.t_end[q];
-    int64_t lo = 0, hi = 0, k = 0;
-    Bnd h{0, -1, 0, 0};
-    NodeView N{0, 0, 0, 0, 0, 0, 0, false, false};
-    if (v >= 0 && v < GV.num_nodes) N = load_node(g, GV, v);
-    if (N.valid && N.nb > 0) {  // sampling.py:153-155
-      h = g_list_lower_bound(g, GV, N, te);
-      int64_t tsr = t_start_of(Q, q, te);
-      lo = (tsr == GF_TS_MIN) ? N.first : g_list_lower_bound(g, GV, N, tsr).pos;
-      hi = h.pos > lo ? h.pos : lo;
-      k = min(hi - lo, Q.fanout);
-    }
-    if (g.gl == 0) {
-      counts[q] = k;
-      if (k > 0) {
-        S.lo[q] = lo;
-        S.hi[q] = hi;
-        S.slot[q] = h.base + (hi - 1 - h.cum);
-        S.cum[q] = h.cum;
-        S.d0[q] = N.d0;
-        S.meta[q] = (h.blk & 0xffffffffll) | (N.nb << 32) | (N.irregular ? (1ll << 62) : 0);
-      }
-    }
   }
 }
 
@@ -932,9 +730,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   int64_t* counts = A.take<int64_t>(cap_q);
   GraphView GV = view_of(g);
   const bool fast = !g->any_deleted;
-  static const bool group_count = getenv("GF_COUNT") && !strcmp(getenv("GF_COUNT"), "group");
-  if (fast && !group_count) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
-  else if (fast) GF_LAUNCH(k_count_fast, grid_for_queries(cap_q, G), THREADS, 0, s, GV, Q, S, counts, cap_q);
+  if (fast) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
   else GF_LAUNCH(k_count_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, counts, cap_q);
   cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
