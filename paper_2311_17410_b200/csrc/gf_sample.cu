@@ -730,40 +730,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   int64_t* counts = A.take<int64_t>(cap_q);
   GraphView GV = view_of(g);
   const bool fast = !g->any_deleted;
-  if (fast) {
-    // keep the fence index resident in L2 while the searches run (persisting window)
-    static const int pw = getenv("GF_L2_PERSIST") ? atoi(getenv("GF_L2_PERSIST")) : 0;
-    if (pw) {
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute attr[1];
-      size_t bytes = (size_t)(g->slots_used / FENCE + 1) * 8;
-      int max_win = 0, dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-      static bool limit_set = false;
-      if (!limit_set) {
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)pw << 20);
-        limit_set = true;
-      }
-      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-      attr[0].val.accessPolicyWindow.base_ptr = g->fts;
-      attr[0].val.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_win);
-      attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cfg.gridDim = dim3((unsigned)grid_for_queries(cap_q, 1));
-      cfg.blockDim = dim3(THREADS);
-      cfg.stream = s;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaEvent_t pe = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
-      GF_CUDA(cudaLaunchKernelEx(&cfg, k_count_lane, GV, Q, S, counts, cap_q));
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      if (pe) prof_stop("k_count_lane", s, pe);
-    } else {
-      GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
-    }
-  }
+  if (fast) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
   else GF_LAUNCH(k_count_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, counts, cap_q);
   cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
