@@ -275,6 +275,32 @@ def misc() -> dict:
     return {"hop_seed": hs, "generate_synthetic_sha256": gens}
 
 
+HARNESS_CONFIGS = [
+    dict(generate_nodes=300, generate_edges=6000, generate_time_span=200_000, batch_edges=1000, epochs_per_round=2,
+         replay_ratio=0.2, minibatch_size=200, fanouts=(5, 5), seed=3, label="lru"),
+    dict(generate_nodes=500, generate_edges=8000, generate_time_span=500_000, batch_edges=2000, epochs_per_round=3,
+         replay_ratio=0.0, minibatch_size=300, fanouts=(4, 3), seed=5, directed=True, tau=16, label="mixed",
+         cache=dict(node_policy="lfu", edge_policy="fifo", node_capacity_frac=0.05, edge_capacity_frac=0.01, lam=0.5,
+                    reuse=False, restore=False)),
+    dict(generate_nodes=200, generate_edges=5000, generate_time_span=100_000, batch_by="time", batch_interval=20_000,
+         epochs_per_round=2, replay_ratio=0.5, minibatch_size=150, fanouts=(6,), seed=7, label="time-batches",
+         memory_dim=4, cache=dict(node_policy="lru", edge_policy="lfu", node_capacity_frac=0.1, edge_capacity_frac=0.02)),
+]
+
+
+def harness_reports() -> dict:
+    """RoundReports of the reference's continuous loop (recent policy) for HARNESS_CONFIGS."""
+    from ctdg.harness import CacheConfig, RunConfig, run_continuous
+
+    out = {}
+    for i, kw in enumerate(HARNESS_CONFIGS):
+        kw = dict(kw)
+        cache = CacheConfig(**kw.pop("cache", {}))
+        cfg = RunConfig(**kw, cache=cache)
+        out[str(i)] = {"config": HARNESS_CONFIGS[i], "reports": [r.to_json() for r in run_continuous(cfg)]}
+    return out
+
+
 def main() -> None:
     np.savez_compressed(os.path.join(HERE, "store_cases.npz"), **store_cases())
     np.savez_compressed(os.path.join(HERE, "sample_cases.npz"), **sample_cases())
@@ -282,6 +308,8 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "feature_cases.npz"), **feature_cases())
     with open(os.path.join(HERE, "misc.json"), "w") as fh:
         json.dump(misc(), fh, indent=1, sort_keys=True)
+    with open(os.path.join(HERE, "harness_reports.json"), "w") as fh:
+        json.dump(harness_reports(), fh, indent=1)
 
 
 if __name__ == "__main__":
