@@ -243,7 +243,10 @@ __device__ __forceinline__ LaneBnd lane_list_lower_bound(const GraphView& GV, co
   return LaneBnd{cum + lane_block_lower_bound(GV, base, size, t0, t1, x), cum, base};
 }
 
-__global__ void __launch_bounds__(THREADS) k_count_lane(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
+#ifndef GF_COUNT_MINB
+#define GF_COUNT_MINB 1
+#endif
+__global__ void __launch_bounds__(THREADS, GF_COUNT_MINB) k_count_lane(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
   const int64_t n = query_count(Q);
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cap_q; q += (int64_t)gridDim.x * blockDim.x) {
     if (q >= n) {
