@@ -97,6 +97,17 @@ gf_status gf_graph_delete_edges(gf_graph* g, const int64_t* d_eids, int64_t n, i
 /* DynamicGraph.delete_node (storage.py:507-512): *h_out_deleted = 1 if the node was live */
 gf_status gf_graph_delete_node(gf_graph* g, int64_t node, int* h_out_deleted, void* stream);
 
+/* DynamicGraph.offload_before (storage.py:516-574): blocks with tmax < cutoff
+ * that form a prefix of their node's list are serialised to a TGOF blob
+ * (storage.py:535-556) and, if `commit`, unlinked (head/tail/num_blocks/live
+ * degree; freed handles are reused LIFO by later appends, storage.py:171-191).
+ * *h_blob_len = blob size; *h_edges = edge records in it.  h_blob (host, may be
+ * NULL) receives the blob when blob_cap is large enough (else GF_ERANGE).
+ * Call with commit = 0 to fetch the blob, write it, then commit = 1: the
+ * graph is unchanged until the commit call. */
+gf_status gf_graph_offload_before(gf_graph* g, int64_t cutoff, uint8_t* h_blob, int64_t blob_cap, int64_t* h_blob_len,
+                                  int64_t* h_edges, int commit, void* stream);
+
 typedef struct {
   int64_t num_nodes;            /* storage.py:327-329 */
   int64_t num_block_handles;    /* arena length (FastTier._blk_used) */

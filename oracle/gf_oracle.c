@@ -268,6 +268,60 @@ int or_delete_node(or_graph* g, int64_t node) {
   return 1;
 }
 
+static void put_le(uint8_t* p, uint64_t v, int n) {
+  for (int i = 0; i < n; i++) p[i] = (uint8_t)(v >> (8 * i));
+}
+
+/* DynamicGraph.offload_before, storage.py:516-574 (TGOF blob into `blob`).
+ * Returns the number of edge records, or -1 when the blob does not fit
+ * (nothing is unlinked then, as when the reference's sink.write fails). */
+int64_t or_offload_before(or_graph* g, int64_t cutoff, uint8_t* blob, int64_t cap, int64_t* blob_len) {
+  int64_t bytes = 8, n_edges = 0;
+  for (int64_t v = 0; v < g->n_nodes; v++)
+    for (int64_t h = g->head[v]; h != NO_BLOCK && g->tmax[h] < cutoff && g->size[h] > 0; h = g->next[h]) {
+      bytes += 12 + 25 * g->size[h];
+      n_edges += g->size[h];
+    }
+  *blob_len = bytes;
+  if (!blob || cap < bytes) return -1;
+  memcpy(blob, "TGOF", 4); /* :536-537 */
+  put_le(blob + 4, 1, 4);
+  uint8_t* p = blob + 8;
+  for (int64_t v = 0; v < g->n_nodes; v++) /* :539-554 */
+    for (int64_t h = g->head[v]; h != NO_BLOCK && g->tmax[h] < cutoff && g->size[h] > 0; h = g->next[h]) {
+      put_le(p, (uint64_t)v, 8);
+      put_le(p + 8, (uint64_t)g->size[h], 4);
+      p += 12;
+      for (int64_t i = 0; i < g->size[h]; i++) {
+        put_le(p, (uint64_t)g->edges[h].nbr[i], 8);
+        put_le(p + 8, (uint64_t)g->edges[h].eid[i], 8);
+        put_le(p + 16, (uint64_t)g->edges[h].ts[i], 8);
+        p[24] = g->edges[h].valid[i] ? 1 : 0;
+        p += 25;
+      }
+    }
+  for (int64_t v = 0; v < g->n_nodes; v++) { /* unlink, :558-573 */
+    int64_t h = g->head[v], k = 0, live = 0;
+    while (h != NO_BLOCK && g->tmax[h] < cutoff && g->size[h] > 0) {
+      for (int64_t i = 0; i < g->size[h]; i++) live += g->edges[h].valid[i] != 0;
+      if (g->n_free == g->free_alloc) {
+        g->free_alloc = g->free_alloc ? 2 * g->free_alloc : 64;
+        g->free_handles = xrealloc(g->free_handles, g->free_alloc * 8);
+      }
+      g->free_handles[g->n_free++] = h;
+      k++;
+      h = g->next[h];
+    }
+    if (!k) continue;
+    g->head[v] = h;
+    if (h == NO_BLOCK) g->tail[v] = NO_BLOCK;
+    else g->prev[h] = NO_BLOCK;
+    g->num_blocks[v] -= k;
+    g->degree[v] -= live;
+  }
+  return n_edges;
+}
+
 int64_t or_num_nodes(const or_graph* g) { return g->n_nodes; }
 int64_t or_num_block_handles(const or_graph* g) { return g->blk_used; }
 int64_t or_next_edge_id(const or_graph* g) { return g->next_edge_id; }

@@ -49,6 +49,8 @@ int64_t or_delete_edges(or_graph* g, const int64_t* eids, int64_t n);
 /* storage.py:507-512 */
 int or_delete_node(or_graph* g, int64_t node);
 
+/* storage.py:516-574: writes the TGOF blob and unlinks; -1 if cap too small */
+int64_t or_offload_before(or_graph* g, int64_t cutoff, uint8_t* blob, int64_t cap, int64_t* blob_len);
 int64_t or_num_nodes(const or_graph* g);
 int64_t or_num_block_handles(const or_graph* g);
 int64_t or_next_edge_id(const or_graph* g);

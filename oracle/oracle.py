@@ -43,6 +43,8 @@ def _load():
     for name in ("or_num_nodes", "or_num_block_handles", "or_next_edge_id", "or_total_edges_inserted"):
         getattr(lib, name).restype = ctypes.c_int64
         getattr(lib, name).argtypes = [ctypes.c_void_p]
+    lib.or_offload_before.restype = ctypes.c_int64
+    lib.or_offload_before.argtypes = [ctypes.c_void_p, ctypes.c_int64, _u8p, ctypes.c_int64, _i64p]
     lib.or_export_nodes.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _i64p, _u8p]
     lib.or_export_blocks.argtypes = [ctypes.c_void_p] + [_i64p] * 6
     lib.or_export_block_edges.restype = ctypes.c_int64
@@ -129,6 +131,14 @@ class OracleGraph:
 
     def delete_node(self, node: int) -> bool:
         return bool(lib().or_delete_node(self._h, int(node)))
+
+    def offload_before(self, cutoff: int):
+        """storage.py:516-574: returns (TGOF blob bytes, edge records)."""
+        blen = ctypes.c_int64(0)
+        lib().or_offload_before(self._h, int(cutoff), None, 0, ctypes.byref(blen))
+        buf = np.zeros(blen.value, dtype=np.uint8)
+        n = lib().or_offload_before(self._h, int(cutoff), _p(buf, _u8p), len(buf), ctypes.byref(blen))
+        return buf.tobytes(), int(n)
 
     # -- inspection -------------------------------------------------------
     @property

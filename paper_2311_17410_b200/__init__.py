@@ -24,6 +24,8 @@ from .storage import (  # noqa: F401
     TS_MAX,
     TS_MIN,
     new_graph,
+    parse_offload,
+    write_offload_records,
 )
 from .sampling import (  # noqa: F401
     LayeredSample,

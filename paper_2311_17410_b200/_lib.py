@@ -51,6 +51,7 @@ _SIGS = {
     "gf_graph_delete_edges": (c_int, [c_vp, c_vp, c_i64, P_i64, c_vp]),
     "gf_graph_delete_node": (c_int, [c_vp, c_i64, ctypes.POINTER(c_int), c_vp]),
     "gf_graph_get_info": (c_int, [c_vp, ctypes.POINTER(GraphInfo)]),
+    "gf_graph_offload_before": (c_int, [c_vp, c_i64, P_u8, c_i64, P_i64, P_i64, c_int, c_vp]),
     "gf_graph_export_nodes": (c_int, [c_vp, P_i64, P_i64, P_i64, P_i64, P_u8, c_vp]),
     "gf_graph_export_blocks": (c_int, [c_vp, P_i64, P_i64, P_i64, P_i64, P_i64, P_i64, c_vp]),
     "gf_graph_export_slots": (c_int, [c_vp, c_i64, c_i64, P_i64, P_i64, P_i64, P_i64, P_u8, c_vp]),

@@ -303,11 +303,12 @@ __global__ void k_enumerate(const int64_t* __restrict__ ce_pend, const uint32_t*
   }
 }
 
+// r-th allocation takes free_handles.pop() (LIFO, storage.py:172-173) while any are left, then fresh handles
 __global__ void k_assign_handles(const uint32_t* __restrict__ perm, int64_t nrec, int64_t blk_used, const int64_t* rcap,
-                                 int64_t* handle, int64_t* cap_sorted) {
+                                 const int64_t* __restrict__ freel, int64_t nfree, int64_t* handle, int64_t* cap_sorted) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
     uint32_t rec = perm[r];
-    handle[rec] = blk_used + r;
+    handle[rec] = r < nfree ? freel[nfree - 1 - r] : blk_used + (r - nfree);
     cap_sorted[r] = rcap[rec];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) cap_sorted[nrec] = 0;
@@ -324,7 +325,7 @@ __global__ void k_write_blocks(const uint32_t* __restrict__ perm, int64_t nrec, 
                                int directed, BlockArrays B) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
     uint32_t rec = perm[r];
-    int64_t h = blk_used + r;
+    int64_t h = R.handle[rec];
     int32_t s = R.seg[rec];
     int64_t k = rec - blkoff[s], nb = P.nb_new[s];
     int64_t cs = P.cstart[s];
@@ -640,7 +641,10 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   GF_CUDA(cudaStreamSynchronize(s));
 
   const int64_t nrec = hc.new_blocks;
-  GF_TRY(ensure_blocks(g, g->blk_used + nrec, s));
+  // freed handles (offload) are reused first, LIFO (storage.py:171-181)
+  const int64_t nfree = (int64_t)g->free_handles.size();
+  const int64_t nfresh = std::max<int64_t>(0, nrec - nfree);
+  GF_TRY(ensure_blocks(g, g->blk_used + nfresh, s));
   GF_TRY(ensure_slots(g, g->slots_used + hc.new_slots, s));
   GF_TRY(ensure_dir(g, g->dir_used + hc.dir_need, s));
 
@@ -651,6 +655,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     for (int q = 0; q < 3; q++) probe.take<int64_t>(nrec + 1);
     probe.take<int32_t>(nrec); probe.take<uint32_t>(nrec); probe.take<uint32_t>(nrec); probe.take<uint32_t>(nrec);
     probe.take<uint32_t>(nrec); probe.take<int64_t>(nrec + 1); probe.take<int64_t>(nrec + 1); probe.take<int64_t>(nrec + 1);
+    probe.take<int64_t>(nfree);
     GF_TRY(rb.alloc(probe.off + 4096));
   }
   RA.base = rb.as<char>();
@@ -666,6 +671,8 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   R.handle = RA.take<int64_t>(nrec + 1);
   int64_t* cap_sorted = RA.take<int64_t>(nrec + 1);
   int64_t* base_scan = RA.take<int64_t>(nrec + 1);
+  int64_t* d_free = RA.take<int64_t>(nfree);
+  if (nfree && nrec) GF_CUDA(cudaMemcpyAsync(d_free, g->free_handles.data(), 8 * nfree, cudaMemcpyHostToDevice, s));
 
   if (nrec > 0) {
     GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
@@ -674,7 +681,8 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     GF_TRY(cub_call([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, R.key, key_sorted, R.idx, perm, (int)nrec, 0, kb, s);
     }, s));
-    GF_LAUNCH(k_assign_handles, grid_for(nrec, T, G), T, 0, s, perm, nrec, g->blk_used, R.cap, R.handle, cap_sorted);
+    GF_LAUNCH(k_assign_handles, grid_for(nrec, T, G), T, 0, s, perm, nrec, g->blk_used, R.cap, d_free, nfree, R.handle,
+              cap_sorted);
     GF_TRY(cub_call([&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, cap_sorted, base_scan, (int)(nrec + 1), s);
     }, s));
@@ -692,7 +700,8 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
               g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
   }
-  g->blk_used += nrec;
+  g->blk_used += nfresh;
+  g->free_handles.resize(nfree - std::min(nfree, nrec));
   g->slots_used += hc.new_slots;
   g->dir_used += hc.dir_need;
   if (eids_in) {
@@ -873,7 +882,7 @@ gf_status gf_graph_get_info(gf_graph* g, gf_graph_info* out) {
   if (!g || !out) return fail(GF_EINVAL, "NULL argument");
   out->num_nodes = g->num_nodes;
   out->num_block_handles = g->blk_used;
-  out->live_blocks = g->blk_used;
+  out->live_blocks = g->blk_used - (int64_t)g->free_handles.size();
   out->slots_allocated = g->slots_used;
   out->next_edge_id = g->next_edge_id;
   out->total_edges_inserted = g->total_edges_inserted;

@@ -16,6 +16,8 @@
 //   nflags     (u8 per node)                   bit 0: block list not on the sizing law's closed form
 #pragma once
 
+#include <vector>
+
 #include "gf_common.cuh"
 
 struct gf_graph {
@@ -30,6 +32,7 @@ struct gf_graph {
   int64_t slots_used = 0, slot_cap = 0;
   int64_t dir_used = 0, dir_cap_total = 0;
   int64_t next_edge_id = 0, total_edges_inserted = 0;
+  std::vector<int64_t> free_handles;  // FastTier._free_handles (storage.py:154, 190-191)
   int any_deleted = 0;
 
   // node table

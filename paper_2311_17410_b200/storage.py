@@ -141,7 +141,8 @@ class EdgeArrays:
 class FastTierView:
     """Host mirror of FastTier's columns (storage.py:140-152), exported from the device."""
 
-    def __init__(self, nodes: dict, blocks: dict):
+    def __init__(self, nodes: dict, blocks: dict, live_blocks: int | None = None):
+        self._live = live_blocks
         self.head = nodes["head"]
         self.tail = nodes["tail"]
         self.num_blocks = nodes["num_blocks"]
@@ -161,7 +162,7 @@ class FastTierView:
 
     @property
     def live_blocks(self) -> int:
-        return len(self.blk_capacity)
+        return len(self.blk_capacity) if self._live is None else self._live
 
     def metadata_bytes(self) -> int:
         return self.num_nodes * NODE_ENTRY_BYTES + self.live_blocks * BLOCK_META_BYTES
@@ -311,7 +312,8 @@ class DynamicGraph:
 
     @property
     def fast(self) -> FastTierView:
-        return self._exported("fast", lambda: FastTierView(self._export_nodes(), self._export_blocks()))
+        return self._exported("fast", lambda: FastTierView(self._export_nodes(), self._export_blocks(),
+                                                           int(self.info().live_blocks)))
 
     def node_entry(self, node: int) -> NodeEntry:
         if not self.has_node(node):
@@ -433,7 +435,33 @@ class DynamicGraph:
         return bool(out.value)
 
     def offload_before(self, cutoff: int, sink) -> int:
-        raise NotImplementedError("offload (storage.py:516-574) is SURVEY.md 8(f) row 3; not implemented yet")
+        """storage.py:516-574: serialise and unlink every block with t_max < cutoff.
+
+        The TGOF blob is assembled on the device and written to ``sink``
+        before anything is unlinked, so an I/O failure leaves the graph
+        unchanged.  Returns the number of edge records written.
+        """
+        lib = load()
+        blen, edges = ctypes.c_int64(0), ctypes.c_int64(0)
+        check(lib.gf_graph_offload_before(self._h, int(cutoff), None, 0, ctypes.byref(blen), ctypes.byref(edges), 0,
+                                          stream_ptr()))
+        blob = np.zeros(int(blen.value), dtype=np.uint8)
+        check(lib.gf_graph_offload_before(self._h, int(cutoff), _lib.np_ptr(blob, ctypes.c_uint8), len(blob),
+                                          ctypes.byref(blen), ctypes.byref(edges), 0, stream_ptr()))
+        sink.write(blob.tobytes())
+        self._version += 1
+        check(lib.gf_graph_offload_before(self._h, int(cutoff), None, 0, ctypes.byref(blen), ctypes.byref(edges), 1,
+                                          stream_ptr()))
+        return int(edges.value)
+
+    def _live_handles(self) -> list[int]:
+        nodes, nxt = self._export_nodes(), self._export_blocks()["next"]
+        out = []
+        for h in nodes["head"].tolist():
+            while h != NO_BLOCK:
+                out.append(h)
+                h = int(nxt[h])
+        return out
 
     # -- statistics (storage.py:578-617) --------------------------------------------
     def storage_stats(self) -> StorageStats:
@@ -441,8 +469,12 @@ class DynamicGraph:
         active = f.degree > 0
         avg = float(f.num_blocks[active].mean()) if active.any() else 0.0
         max_len = int(f.num_blocks.max()) if f.num_nodes else 0
-        wasted = int((f.blk_capacity - f.blk_size).sum())
-        return StorageStats(avg, max_len, int(f.blk_capacity.sum()) * EDGE_SLOT_BYTES, f.metadata_bytes(), wasted)
+        live = np.asarray(self._live_handles(), dtype=np.int64)
+        cap = f.blk_capacity[live] if len(live) else np.zeros(0, np.int64)
+        size = f.blk_size[live] if len(live) else np.zeros(0, np.int64)
+        wasted = int((cap - size).sum())
+        metadata = f.num_nodes * NODE_ENTRY_BYTES + int(self.info().live_blocks) * BLOCK_META_BYTES
+        return StorageStats(avg, max_len, int(cap.sum()) * EDGE_SLOT_BYTES, metadata, wasted)
 
     def check_waste_bound(self) -> bool:
         stats = self.storage_stats()
@@ -456,3 +488,42 @@ class DynamicGraph:
 
 def new_graph(directed: bool = False, tau: int = 48, sizing: BlockSizing | None = None, device=None) -> DynamicGraph:
     return DynamicGraph(directed=directed, tau=tau, sizing=sizing, device=device)
+
+
+OFFLOAD_MAGIC = b"TGOF"  # storage.py:42-43
+OFFLOAD_VERSION = 1
+
+
+def parse_offload(source) -> list[tuple[int, list[tuple[int, int, int, bool]]]]:
+    """Parse an offload blob into (node, [(neighbor, edge_id, ts, valid)]) (storage.py:624-647)."""
+    import struct
+
+    data = source.read() if hasattr(source, "read") else bytes(source)
+    if data[:4] != OFFLOAD_MAGIC:
+        raise GraphFormatError("bad offload magic")
+    (version,) = struct.unpack_from("<I", data, 4)
+    if version != OFFLOAD_VERSION:
+        raise GraphFormatError(f"unsupported offload version {version}")
+    pos, out = 8, []
+    while pos < len(data):
+        if pos + 12 > len(data):
+            raise GraphFormatError("truncated block header")
+        node, size = struct.unpack_from("<QI", data, pos)
+        pos += 12
+        if pos + 25 * size > len(data):
+            raise GraphFormatError("truncated edge record")
+        recs = [struct.unpack_from("<QQqB", data, pos + 25 * i) for i in range(size)]
+        pos += 25 * size
+        out.append((int(node), [(n, e, t, bool(v)) for n, e, t, v in recs]))
+    return out
+
+
+def write_offload_records(records) -> bytes:
+    """Re-serialise parsed offload records (storage.py:650-659)."""
+    import struct
+
+    buf = [OFFLOAD_MAGIC, struct.pack("<I", OFFLOAD_VERSION)]
+    for node, recs in records:
+        buf.append(struct.pack("<QI", node, len(recs)))
+        buf.extend(struct.pack("<QQqB", n, e, t, 1 if v else 0) for n, e, t, v in recs)
+    return b"".join(buf)

@@ -275,6 +275,71 @@ def misc() -> dict:
     return {"hop_seed": hs, "generate_synthetic_sha256": gens}
 
 
+def offload_cases() -> dict:
+    """ingest -> offload(c1) -> ingest -> offload(c2) -> ingest: TGOF blobs, eids and the live layout.
+
+    Later ingests reuse the freed block handles (LIFO, storage.py:171-191)."""
+    import io
+
+    rng = np.random.default_rng(31337)
+    out: dict = {}
+    meta = []
+    for i in range(24):
+        directed = bool(i % 2)
+        tau = int(rng.choice([1, 2, 4, 16, 48]))
+        sizing_kind = ["adaptive", "fixed", "adaptive", "batch"][i % 4]
+        param = int(rng.integers(1, 6))
+        sizing = {"adaptive": None, "fixed": FixedSizing(param), "batch": BatchSizing()}[sizing_kind]
+        g = DynamicGraph(directed=directed, tau=tau, sizing=sizing)
+        nn = int(rng.integers(2, 40))
+        p = f"o{i}/"
+        t0 = 0
+        steps = []
+        for step in range(3):
+            m = int(rng.integers(1, 250))
+            src = rng.integers(0, nn, m); dst = rng.integers(0, nn, m)
+            ts = np.sort(rng.integers(t0, t0 + 5 * m, m))
+            t0 = int(ts[-1])
+            r = g.add_edges(list(zip(src.tolist(), dst.tolist(), ts.tolist())))
+            out[p + f"{step}_src"], out[p + f"{step}_dst"], out[p + f"{step}_ts"] = src, dst, ts
+            out[p + f"{step}_eids"] = np.array([-1 if e is None else e for e in r.edge_ids], np.int64)
+            if step < 2:
+                cutoff = int(rng.integers(0, t0 + 2))
+                if i % 5 == 0 and step == 1:  # an edge deletion between offloads
+                    ids = [e for e in r.edge_ids if e is not None][:3]
+                    g.delete_edges(ids)
+                    out[p + f"{step}_del"] = np.array(ids, np.int64)
+                buf = io.BytesIO()
+                n_off = g.offload_before(cutoff, buf)
+                out[p + f"{step}_blob"] = np.frombuffer(buf.getvalue(), np.uint8).copy()
+                steps.append({"cutoff": cutoff, "n": n_off})
+        f = g.fast
+        live = []
+        for v in range(g.num_nodes):
+            live.extend(g.blocks_of(v))
+        out[p + "live"] = np.array(live, np.int64)
+        for name in ("head", "tail", "num_blocks", "degree", "node_valid"):
+            out[p + name] = getattr(f, name).copy()
+        for name in ("blk_capacity", "blk_size", "blk_tmin", "blk_tmax", "blk_prev", "blk_next"):
+            out[p + name] = getattr(f, name)[live].copy() if live else np.zeros(0, np.int64)
+        offs, cols = [0], {"nbr": [], "eid": [], "ts": [], "valid": []}
+        for h in live:
+            a = g.shared.get(h)
+            s = int(f.blk_size[h])
+            cols["nbr"].append(a.neighbors[:s]); cols["eid"].append(a.edge_ids[:s])
+            cols["ts"].append(a.timestamps[:s]); cols["valid"].append(a.valid[:s])
+            offs.append(offs[-1] + s)
+        out[p + "slot_offsets"] = np.array(offs, np.int64)
+        for k, dt in (("nbr", np.int64), ("eid", np.int64), ("ts", np.int64), ("valid", bool)):
+            out[p + "slot_" + k] = np.concatenate(cols[k]).astype(dt) if cols[k] else np.zeros(0, dt)
+        st = g.storage_stats()
+        meta.append({"id": i, "directed": directed, "tau": tau, "sizing": sizing_kind, "param": param, "steps": steps,
+                     "stats": [st.avg_list_len, st.max_list_len, st.edge_data_bytes, st.metadata_bytes, st.wasted_slots],
+                     "num_block_handles": int(f._blk_used)})
+    out["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    return out
+
+
 HARNESS_CONFIGS = [
     dict(generate_nodes=300, generate_edges=6000, generate_time_span=200_000, batch_edges=1000, epochs_per_round=2,
          replay_ratio=0.2, minibatch_size=200, fanouts=(5, 5), seed=3, label="lru"),
@@ -308,8 +373,10 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "feature_cases.npz"), **feature_cases())
     with open(os.path.join(HERE, "misc.json"), "w") as fh:
         json.dump(misc(), fh, indent=1, sort_keys=True)
-    with open(os.path.join(HERE, "harness_reports.json"), "w") as fh:
-        json.dump(harness_reports(), fh, indent=1)
+    np.savez_compressed(os.path.join(HERE, "offload_cases.npz"), **offload_cases())
+    if not os.path.exists(os.path.join(HERE, "harness_reports.json")) or os.environ.get("GOLDEN_HARNESS"):
+        with open(os.path.join(HERE, "harness_reports.json"), "w") as fh:
+            json.dump(harness_reports(), fh, indent=1)
 
 
 if __name__ == "__main__":

@@ -241,3 +241,37 @@ def test_oracle_against_live_reference_random_corpus():
         offs, nb, eid, tts = ora.sample_layer(q, np.full(40, TS_MIN), t1, 4)
         assert offs.tolist() == lay.offsets.tolist() and nb.tolist() == lay.neighbors.tolist()
         assert eid.tolist() == lay.edge_ids.tolist() and tts.tolist() == lay.timestamps.tolist()
+
+
+class _OracleOffloadAdapter:
+    def __init__(self, m):
+        self.g = OracleGraph(m["directed"], m["tau"], m["sizing"], m["param"])
+
+    def add_edges(self, s, d, t):
+        return self.g.add_edges(s, d, t)
+
+    def delete_edges(self, ids):
+        return self.g.delete_edges(ids)
+
+    def offload(self, cutoff):
+        return self.g.offload_before(cutoff)
+
+
+def test_oracle_offload_matches_reference():
+    """storage.py:516-574 incl. TGOF bytes and LIFO handle reuse by later ingests."""
+    from fixtures import live_layout_from, replay_offload_case
+
+    fx, meta = load("offload_cases.npz")
+    for m in meta:
+        p = f"o{m['id']}/"
+        a = _OracleOffloadAdapter(m)
+        for what, step, got, want in replay_offload_case(a, fx, p, m):
+            if what == "n":
+                assert got == want, (p, step)
+            else:
+                np.testing.assert_array_equal(got, want, err_msg=f"{p} {what} {step}")
+        live = fx[p + "live"]
+        lay = live_layout_from(a.g.export_nodes(), a.g.export_blocks(), lambda h: a.g.block_edges(h), live)
+        for k, v in lay.items():
+            np.testing.assert_array_equal(v, fx[p + k], err_msg=f"{p} {k}")
+        assert a.g.num_block_handles == m["num_block_handles"]
