@@ -1,0 +1,248 @@
+"""Partitioned multi-GPU mode (MAG config): the graph is edge-cut hash partitioned.
+
+Rank r owns the nodes v with v % P == r (partition.py:38-39) and stores each
+owned node's whole list (cluster.py:126-140): a directed edge lives with
+the owner of its source, an undirected edge additionally as (dst, src) with
+the owner of its destination, under one global edge id (cluster.py:178-201).
+
+Ingest: every rank holds a contiguous shard of the new batch (rank order);
+global ids are the batch base plus the shard offset; entries are bucketed by
+owner and exchanged with one all-to-all, then appended on the owner in
+stream order (received chunks are concatenated in source-rank order, so the
+per-node append order equals the unpartitioned store's).
+
+Sampling, per hop (cluster.py:242-292): queries are bucketed by the owner of
+their source and exchanged (node, t_end, query key); the owner runs the
+device sampler with the given keys; counts and sampled (nbr, eid, ts, child
+key) go back with a second all-to-all and are merged into the original
+query order.  Because the sampler's randomness is keyed by the query key,
+not by where the query runs, the result equals a single-GPU sample of the
+unpartitioned graph bit for bit (tests/test_partitioned*.py), the property
+the reference checks for its cluster (tests/test_cluster.py:62-84).
+
+Transports: ``DistTransport`` (torch.distributed all_to_all_single: NCCL over
+NVLink between GPUs, gloo on CPU) and ``ThreadTransport`` (P ranks as
+threads of one process on one GPU, the counterpart of the reference's
+in-process LocalTransport, cluster.py:143-157).
+"""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+from .sampling import LayeredSample, SampleLayer, SamplingPolicy, hop_seed
+
+
+class DistTransport:
+    """all_to_all over the default torch.distributed process group."""
+
+    def __init__(self):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.P = dist.get_world_size()
+        self.rank = dist.get_rank()
+
+    def exchange(self, chunks):
+        """chunks[d]: int64 tensor [k, n_d] for rank d -> list of tensors received from each rank."""
+        import torch
+
+        k = chunks[0].shape[0]
+        dev = chunks[0].device
+        send_n = torch.tensor([c.shape[1] for c in chunks], dtype=torch.int64, device=dev)
+        recv_n = torch.empty_like(send_n)
+        self.dist.all_to_all_single(recv_n, send_n)
+        rn = recv_n.tolist()
+        send = torch.cat([c.t().contiguous() for c in chunks]) if chunks else torch.empty((0, k), dtype=torch.int64)
+        recv = torch.empty((sum(rn), k), dtype=torch.int64, device=dev)
+        self.dist.all_to_all_single(recv, send, [int(x) for x in rn], [int(c.shape[1]) for c in chunks])
+        out, pos = [], 0
+        for n in rn:
+            out.append(recv[pos:pos + n].t().contiguous())
+            pos += n
+        return out
+
+    def allgather_int(self, x: int) -> list[int]:
+        import torch
+
+        t = torch.tensor([x], dtype=torch.int64)
+        if self.dist.get_backend() == "nccl":
+            t = t.cuda()
+        parts = [torch.zeros_like(t) for _ in range(self.P)]
+        self.dist.all_gather(parts, t)
+        return [int(p.item()) for p in parts]
+
+
+class ThreadTransport:
+    """P ranks as threads of one process (single-GPU simulation of the partitioned mode)."""
+
+    class _Shared:
+        def __init__(self, P):
+            self.P = P
+            self.table = [None] * P
+            self.barrier = threading.Barrier(P)
+
+    def __init__(self, shared: "_Shared", rank: int):
+        self.shared, self.P, self.rank = shared, shared.P, rank
+
+    @classmethod
+    def group(cls, P: int):
+        sh = cls._Shared(P)
+        return [cls(sh, r) for r in range(P)]
+
+    def exchange(self, chunks):
+        sh = self.shared
+        sh.table[self.rank] = chunks
+        sh.barrier.wait()
+        out = [sh.table[s][self.rank] for s in range(self.P)]
+        sh.barrier.wait()
+        return out
+
+    def allgather_int(self, x: int) -> list[int]:
+        sh = self.shared
+        sh.table[self.rank] = x
+        sh.barrier.wait()
+        out = list(sh.table)
+        sh.barrier.wait()
+        return out
+
+
+class GpuEngine:
+    """This rank's partition on its GPU (libgfb200)."""
+
+    def __init__(self, tau: int = 48, sizing=None, device=None):
+        from .storage import DynamicGraph
+
+        # a partition stores directed per-endpoint entries (cluster.py:131-140)
+        self.graph = DynamicGraph(directed=True, tau=tau, sizing=sizing, device=device)
+        self.device = self.graph.device
+
+    def add(self, src, dst, ts, eids):
+        self.graph.add_edges_arrays(src, dst, ts, eids)
+
+    def delete_node(self, v: int) -> bool:
+        return self.graph.delete_node(v)
+
+    def sample(self, src, tend, keys, fanout, policy: SamplingPolicy, seed):
+        from .sampling import _layer_device
+
+        offs, nbr, eid, ts, okeys = _layer_device(self.graph, src, None, tend, fanout, policy, seed, keys=keys,
+                                                  want_keys=True)
+        return offs, nbr, eid, ts, okeys
+
+
+class PartitionedGraph:
+    def __init__(self, transport, engine, directed: bool = False):
+        self.t = transport
+        self.e = engine
+        self.P, self.rank = transport.P, transport.rank
+        self.directed = directed
+        self.next_edge_id = 0
+
+    @property
+    def device(self):
+        return self.e.device
+
+    # -- ingest -------------------------------------------------------------------
+    def add_edges(self, src, dst, ts):
+        """Append this rank's shard of a global batch; returns the shard's global edge ids."""
+        import torch
+
+        dev = self.device
+        src = torch.as_tensor(src, dtype=torch.int64, device=dev)
+        dst = torch.as_tensor(dst, dtype=torch.int64, device=dev)
+        ts = torch.as_tensor(ts, dtype=torch.int64, device=dev)
+        sizes = self.t.allgather_int(int(src.numel()))
+        base = self.next_edge_id + sum(sizes[: self.rank])
+        ids = base + torch.arange(src.numel(), dtype=torch.int64, device=dev)
+        self.next_edge_id += sum(sizes)
+        # entries in stream order: edge j -> (src, dst) [, (dst, src)]
+        if self.directed:
+            es, ed, et, ei = src, dst, ts, ids
+        else:
+            es = torch.stack([src, dst], 1).reshape(-1)
+            ed = torch.stack([dst, src], 1).reshape(-1)
+            et = torch.stack([ts, ts], 1).reshape(-1)
+            ei = torch.stack([ids, ids], 1).reshape(-1)
+        owner = es % self.P
+        chunks = [torch.stack([es[owner == d], ed[owner == d], et[owner == d], ei[owner == d]]) for d in range(self.P)]
+        got = torch.cat(self.t.exchange(chunks), dim=1)  # source-rank order = stream order
+        if got.shape[1]:
+            self.e.add(got[0].contiguous(), got[1].contiguous(), got[2].contiguous(), got[3].contiguous())
+        return ids
+
+    def delete_node(self, v: int) -> bool:
+        # node validity is checked at the sampling owner for sources and neighbours: every partition
+        return bool(self.e.delete_node(v))
+
+    # -- sampling -------------------------------------------------------------------
+    def sample_layer(self, src, tend, keys, fanout: int, policy: SamplingPolicy, seed_h: int):
+        import torch
+
+        dev = self.device
+        n = int(src.numel())
+        owner = src % self.P
+        order = torch.argsort(owner, stable=True)
+        owner_sorted = owner[order]
+        chunks = []
+        for d in range(self.P):
+            sel = order[owner_sorted == d]
+            chunks.append(torch.stack([src[sel], tend[sel], keys[sel]]))  # keys: uint64 bit patterns in int64
+        recv = self.t.exchange(chunks)
+        q = torch.cat(recv, dim=1)
+        per_src = [int(c.shape[1]) for c in recv]
+        if q.shape[1]:
+            offs, nbr, eid, ts, okeys = self.e.sample(q[0].contiguous(), q[1].contiguous(), q[2].contiguous(), fanout,
+                                                      policy, seed_h)
+            counts = offs[1:] - offs[:-1]
+        else:
+            counts = torch.zeros(0, dtype=torch.int64, device=dev)
+            nbr = eid = ts = okeys = torch.zeros(0, dtype=torch.int64, device=dev)
+            offs = torch.zeros(1, dtype=torch.int64, device=dev)
+        # answers back to each origin: per query counts, then the flat edges
+        back_counts, back_edges, qpos, epos = [], [], 0, 0
+        for s, nq in enumerate(per_src):
+            c = counts[qpos:qpos + nq]
+            ne = int(c.sum().item()) if nq else 0
+            back_counts.append(c.reshape(1, -1))
+            back_edges.append(torch.stack([nbr[epos:epos + ne], eid[epos:epos + ne], ts[epos:epos + ne],
+                                           okeys[epos:epos + ne]]))
+            qpos += nq
+            epos += ne
+        cnt_recv = self.t.exchange(back_counts)
+        edge_recv = self.t.exchange(back_edges)
+        # merge into the original query order
+        cnt_sorted = torch.cat([c.reshape(-1) for c in cnt_recv])  # in `order`
+        edges_sorted = torch.cat(edge_recv, dim=1)
+        counts_orig = torch.empty(n, dtype=torch.int64, device=dev)
+        counts_orig[order] = cnt_sorted
+        offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(counts_orig, 0, out=offsets[1:])
+        # sorted query i's edges go to offsets[order[i]] .. + cnt_sorted[i]
+        start_sorted = torch.zeros_like(cnt_sorted)
+        if n:
+            start_sorted[1:] = torch.cumsum(cnt_sorted, 0)[:-1]
+        total = int(offsets[-1].item())
+        qid = torch.repeat_interleave(torch.arange(n, device=dev), cnt_sorted)
+        within = torch.arange(total, device=dev) - start_sorted[qid]
+        dest = offsets[order[qid]] + within
+        out = torch.empty((4, total), dtype=torch.int64, device=dev)
+        out[:, dest] = edges_sorted
+        return SampleLayer(src, tend, offsets, out[0], out[1], out[2]), out[3]
+
+    def sample_khop(self, roots, ts, fanouts, policy: SamplingPolicy, seed: int = 0, root_key_base: int = 0):
+        """This rank's roots; keys root_key_base + i (cf. sampling.sample_khop)."""
+        import torch
+
+        dev = self.device
+        src = torch.as_tensor(roots, dtype=torch.int64, device=dev)
+        tend = torch.as_tensor(ts, dtype=torch.int64, device=dev)
+        keys = (torch.arange(src.numel(), dtype=torch.int64, device=dev) + int(root_key_base))
+        layers = []
+        for hop, f in enumerate(fanouts):
+            lay, keys = self.sample_layer(src, tend, keys, int(f), policy, hop_seed(seed, hop))
+            layers.append(lay)
+            src, tend = lay.neighbors, lay.timestamps
+        return LayeredSample(layers)

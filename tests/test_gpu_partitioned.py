@@ -1,0 +1,63 @@
+"""Partitioned mode on the GPU: P partitions (threads, one GPU) equal the unpartitioned graph bitwise."""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("P,directed", [(2, True), (3, False), (4, True)])
+def test_partitioned_threads_equal_single_gpu(cuda_device, P, directed):
+    import torch
+
+    import paper_2311_17410_b200 as gf
+    from paper_2311_17410_b200.distributed import shard_range
+    from paper_2311_17410_b200.partitioned import GpuEngine, PartitionedGraph, ThreadTransport
+
+    src, dst, ts = gf.generate_synthetic_arrays(3000, 300_000, 2.2, 175_200, seed=4, src_skew=2.2)
+    roots = np.concatenate([src[-3000:], dst[-3000:]])
+    rts = np.concatenate([ts[-3000:], ts[-3000:]])
+    transports = ThreadTransport.group(P)
+    results = [None] * P
+    errors = []
+
+    def rank_main(r):
+        try:
+            pg = PartitionedGraph(transports[r], GpuEngine(tau=64), directed=directed)
+            for lo in range(0, len(src), 50_000):
+                hi = min(len(src), lo + 50_000)
+                a, b = shard_range(hi - lo, P, r)
+                pg.add_edges(src[lo + a:lo + b], dst[lo + a:lo + b], ts[lo + a:lo + b])
+            a, b = shard_range(len(roots), P, r)
+            out = {}
+            for pol in ("recent", "uniform"):
+                s = pg.sample_khop(roots[a:b], rts[a:b], [10, 10], gf.SamplingPolicy(pol), seed=8, root_key_base=a)
+                out[pol] = [(lay.neighbors.cpu().numpy(), lay.edge_ids.cpu().numpy(), lay.timestamps.cpu().numpy())
+                            for lay in s.layers]
+            torch.cuda.synchronize()
+            results[r] = out
+        except Exception as e:  # surface thread failures
+            errors.append(e)
+            transports[r].shared.barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    g = gf.DynamicGraph(directed=directed, tau=64)
+    for lo in range(0, len(src), 50_000):
+        g.add_edges_arrays(src[lo:lo + 50_000], dst[lo:lo + 50_000], ts[lo:lo + 50_000])
+    dev = torch.device("cuda:0")
+    for pol in ("recent", "uniform"):
+        want = gf.TemporalSampler(g, [10, 10], pol, seed=8).sample(torch.from_numpy(roots).to(dev),
+                                                                   torch.from_numpy(rts).to(dev))
+        for h, lay in enumerate(want.layers):
+            for i, nm in enumerate(("neighbors", "edge_ids", "timestamps")):
+                got = np.concatenate([results[r][pol][h][i] for r in range(P)])
+                np.testing.assert_array_equal(got, getattr(lay, nm).cpu().numpy(), err_msg=f"{pol} hop{h} {nm}")

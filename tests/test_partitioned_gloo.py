@@ -1,0 +1,118 @@
+"""Partitioned mode host logic, world_size 2 over gloo (CPU), with the oracle as each rank's engine.
+
+Every rank ingests its shard of every batch (all-to-all dispatch by owner) and
+samples its own roots through per-hop all-to-all exchanges; the union must
+equal single-process sampling of the unpartitioned graph, bitwise.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class OracleEngine:
+    def __init__(self, tau):
+        from oracle import OracleGraph
+
+        self.g = OracleGraph(True, tau)
+        self.device = torch.device("cpu")
+
+    def add(self, src, dst, ts, eids):
+        out = self.g.add_edges(src.numpy(), dst.numpy(), ts.numpy(), eids.numpy())
+        assert (out >= 0).all()
+
+    def delete_node(self, v):
+        return self.g.delete_node(v)
+
+    def sample(self, src, tend, keys, fanout, policy, seed):
+        from oracle.oracle import _child_keys_vec
+
+        k = keys.numpy().view(np.uint64)
+        offs, nb, eid, ts = self.g.sample_layer(src.numpy(), np.full(len(src), -2**63, np.int64), tend.numpy(), fanout,
+                                                policy.kind, policy.delta, seed, keys=k)
+        cnt = np.diff(offs)
+        ok = _child_keys_vec(np.repeat(k, cnt), np.arange(len(nb)) - np.repeat(offs[:-1], cnt)).view(np.int64)
+        return tuple(torch.from_numpy(np.ascontiguousarray(a)) for a in (offs, nb, eid, ts, ok))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _stream():
+    from paper_2311_17410_b200.synth import generate_synthetic_arrays
+
+    return generate_synthetic_arrays(400, 20_000, 2.2, 40_000, seed=11, src_skew=2.2)
+
+
+def _worker(rank, world, port, out_dir, directed):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2311_17410_b200 import SamplingPolicy
+        from paper_2311_17410_b200.distributed import shard_range
+        from paper_2311_17410_b200.partitioned import DistTransport, PartitionedGraph
+
+        pg = PartitionedGraph(DistTransport(), OracleEngine(32), directed=directed)
+        src, dst, ts = _stream()
+        for lo in range(0, len(src), 5_000):
+            hi = min(len(src), lo + 5_000)
+            a, b = shard_range(hi - lo, world, rank)
+            pg.add_edges(torch.from_numpy(src[lo + a:lo + b]), torch.from_numpy(dst[lo + a:lo + b]),
+                         torch.from_numpy(ts[lo + a:lo + b]))
+        roots = np.concatenate([src[-200:], dst[-200:]])
+        rts = np.concatenate([ts[-200:], ts[-200:]])
+        lo, hi = shard_range(len(roots), world, rank)
+        res = {}
+        for pol in ("recent", "uniform"):
+            s = pg.sample_khop(torch.from_numpy(roots[lo:hi]), torch.from_numpy(rts[lo:hi]), [4, 3],
+                               SamplingPolicy(pol), seed=2, root_key_base=lo)
+            for h, lay in enumerate(s.layers):
+                for nm in ("offsets", "neighbors", "edge_ids", "timestamps"):
+                    res[f"{pol}_{h}_{nm}"] = getattr(lay, nm).numpy()
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **res)
+    finally:
+        dist.destroy_process_group()
+
+
+def _check(tmp_path, directed):
+    from oracle import OracleGraph
+
+    src, dst, ts = _stream()
+    g = OracleGraph(directed, 32)
+    for lo in range(0, len(src), 5_000):
+        g.add_edges(src[lo:lo + 5_000], dst[lo:lo + 5_000], ts[lo:lo + 5_000])
+    roots = np.concatenate([src[-200:], dst[-200:]])
+    rts = np.concatenate([ts[-200:], ts[-200:]])
+    parts = [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
+    for pol in ("recent", "uniform"):
+        want = g.sample_khop(roots, rts, [4, 3], pol, seed=2)
+        # per-rank layer h covers the rank's share of layer h's queries, in order
+        for h, lay in enumerate(want):
+            nb = np.concatenate([p[f"{pol}_{h}_neighbors"] for p in parts])
+            eid = np.concatenate([p[f"{pol}_{h}_edge_ids"] for p in parts])
+            tts = np.concatenate([p[f"{pol}_{h}_timestamps"] for p in parts])
+            np.testing.assert_array_equal(nb, lay[3], err_msg=f"{pol} hop{h}")
+            np.testing.assert_array_equal(eid, lay[4])
+            np.testing.assert_array_equal(tts, lay[5])
+
+
+def test_partitioned_two_ranks_equal_unpartitioned_directed(tmp_path):
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path), True), nprocs=2, join=True)
+    _check(tmp_path, True)
+
+
+def test_partitioned_two_ranks_equal_unpartitioned_undirected(tmp_path):
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path), False), nprocs=2, join=True)
+    _check(tmp_path, False)
