@@ -109,6 +109,69 @@ class ThreadTransport:
         return out
 
 
+def _exchange_rows(transport, chunks):
+    """Exchange float32 [n_d, dim] row blocks (viewed as int32 columns for the int64 exchange)."""
+    import torch
+
+    dim = chunks[0].shape[1] if chunks else 0
+    as_int = [torch.cat([c.contiguous().view(torch.int32).to(torch.int64).t(),
+                         torch.zeros((0, c.shape[0]), dtype=torch.int64, device=c.device)]) for c in chunks]
+    got = transport.exchange(as_int)
+    return [g.t().to(torch.int32).contiguous().view(torch.float32).reshape(-1, dim) for g in got]
+
+
+class PartitionedFeatures:
+    """Feature rows sharded by owner = id % P (cluster.py:296-325), fetched over the transport.
+
+    ``table`` is this rank's local feature table (NodeFeatureTable /
+    EdgeFeatureTable on the GPU) holding the rows of the ids it owns.
+    """
+
+    def __init__(self, transport, table, dim: int):
+        self.t, self.table, self.dim = transport, table, dim
+        self.P, self.rank = transport.P, transport.rank
+
+    def get(self, ids):
+        """(rows, found) for arbitrary ids, in order; one id/rows all-to-all round trip."""
+        import torch
+
+        dev = ids.device
+        n = int(ids.numel())
+        owner = ids % self.P
+        order = torch.argsort(owner, stable=True)
+        owner_sorted = owner[order]
+        chunks = [ids[order[owner_sorted == d]].reshape(1, -1) for d in range(self.P)]
+        asked = self.t.exchange(chunks)
+        replies_rows, replies_found = [], []
+        for q in asked:
+            if q.shape[1]:
+                rows, found = self.table.get(q.reshape(-1))
+            else:
+                rows = torch.zeros((0, self.dim), dtype=torch.float32, device=dev)
+                found = torch.zeros(0, dtype=torch.bool, device=dev)
+            replies_rows.append(rows.to(torch.float32))
+            replies_found.append(found.to(torch.int64).reshape(1, -1))
+        rows_back = torch.cat(_exchange_rows(self.t, replies_rows)) if n else torch.zeros((0, self.dim), device=dev)
+        found_back = torch.cat([f.reshape(-1) for f in self.t.exchange(replies_found)])
+        out = torch.zeros((n, self.dim), dtype=torch.float32, device=dev)
+        found = torch.zeros(n, dtype=torch.bool, device=dev)
+        out[order] = rows_back
+        found[order] = found_back.bool()
+        return out, found
+
+
+def fetch_features_partitioned(cache, features: PartitionedFeatures, keys):
+    """The harness fetch block (harness.py:438-446) with peer-owned rows:
+    cache.fetch -> owner fetch of the misses -> cache.insert_batch(found)."""
+    values, hit, miss = cache.fetch_device(keys)
+    admitted = 0
+    if miss.numel():
+        rows, found = features.get(miss)
+        if bool(found.any()):
+            admitted = cache.insert_batch(miss[found].contiguous(), rows[found].contiguous())
+    return values, hit, int(miss.numel()), admitted
+
+
 class GpuEngine:
     """This rank's partition on its GPU (libgfb200)."""
 

@@ -61,3 +61,59 @@ def test_partitioned_threads_equal_single_gpu(cuda_device, P, directed):
             for i, nm in enumerate(("neighbors", "edge_ids", "timestamps")):
                 got = np.concatenate([results[r][pol][h][i] for r in range(P)])
                 np.testing.assert_array_equal(got, getattr(lay, nm).cpu().numpy(), err_msg=f"{pol} hop{h} {nm}")
+
+
+def test_peer_feature_fetch_threads(cuda_device):
+    """Rows owned by other partitions come back through the transport, bit-exact; cache state
+    equals a single-table fetch block (harness.py:438-446)."""
+    import torch
+
+    import paper_2311_17410_b200 as gf
+    from paper_2311_17410_b200.partitioned import PartitionedFeatures, ThreadTransport, fetch_features_partitioned
+
+    P, dim = 3, 19
+    rng = np.random.default_rng(3)
+    n_nodes = 5000
+    rows = rng.random((n_nodes, dim), dtype=np.float32)
+    keys_all = [rng.integers(-5, n_nodes + 50, 4000) for _ in range(6)]
+    transports = ThreadTransport.group(P)
+    out = [None] * P
+    errors = []
+
+    def rank_main(r):
+        try:
+            table = gf.NodeFeatureTable(dim)
+            mine = np.arange(r, n_nodes, P)
+            table.set_many(mine, rows[mine])
+            feats = PartitionedFeatures(transports[r], table, dim)
+            cache = gf.VectorCache("lru", 300, dim, 0.3)
+            res = []
+            for keys in keys_all:
+                k = torch.from_numpy(keys).cuda()
+                got, found = feats.get(k)
+                res.append((got.cpu().numpy(), found.cpu().numpy()))
+                fetch_features_partitioned(cache, feats, k)
+            res.append((cache.keys, cache.scores))
+            out[r] = res
+        except Exception as e:
+            errors.append(e)
+            transports[r].shared.barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    single = gf.NodeFeatureTable(dim)
+    single.set_many(np.arange(n_nodes), rows)
+    ref_cache = gf.VectorCache("lru", 300, dim, 0.3)
+    for i, keys in enumerate(keys_all):
+        want_rows, want_found = single.get(keys)
+        for r in range(P):
+            np.testing.assert_array_equal(out[r][i][0], want_rows)
+            np.testing.assert_array_equal(out[r][i][1], want_found)
+        gf.fetch_features(ref_cache, single, keys)
+    for r in range(P):
+        np.testing.assert_array_equal(out[r][-1][0], ref_cache.keys)
+        np.testing.assert_array_equal(out[r][-1][1], ref_cache.scores)
