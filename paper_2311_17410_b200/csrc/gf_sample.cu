@@ -137,58 +137,70 @@ __device__ __forceinline__ int64_t probe_between(int64_t lo, int64_t hi, int64_t
   return g <= lo ? lo + 1 : (g >= hi ? hi - 1 : g);
 }
 
+// number of a[i] < x for i in [seg_lo, seg_hi) (sorted, seg_hi - seg_lo <= 32): aligned
+// 256-bit chunks, all independent, so one round trip for any alignment
+__device__ __forceinline__ int64_t window_count(const int64_t* __restrict__ a, int64_t seg_lo, int64_t seg_hi, int64_t x) {
+  int64_t c = 0;
+  const int64_t a0 = seg_lo & ~int64_t(3);
+#pragma unroll
+  for (int w = 0; w < 36; w += 4) {
+    const int64_t p = a0 + w;
+    if (p < seg_hi) {
+      int64_t v0, v1, v2, v3;
+      ld256(a + p, v0, v1, v2, v3);
+      c += (p >= seg_lo && v0 < x) + (p + 1 >= seg_lo && p + 1 < seg_hi && v1 < x) +
+           (p + 2 >= seg_lo && p + 2 < seg_hi && v2 < x) + (p + 3 >= seg_lo && p + 3 < seg_hi && v3 < x);
+    }
+  }
+  return c;
+}
+
 // count of timestamps < x in sts[base, base + size) whose values lie in [t0, t1]
 __device__ __forceinline__ int64_t lane_block_lower_bound(const GraphView& GV, int64_t base, int64_t size, int64_t t0,
                                                           int64_t t1, int64_t x) {
   int64_t seg_lo = base, seg_hi = base + size;
   if (size > FENCE) {
     const int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;
-    // fences f0..f1 are sorted; find j = #fences < x by interpolation + bisection
+    // fences f0..f1 are sorted; j = #fences < x.  Each probe reads the aligned 4-fence chunk
+    // around an interpolated index and narrows the bracket with every fence inside it.
     int64_t lo = f0 - 1, hi = f1 + 1;  // virtual fences: fts[lo] < x <= fts[hi]
     int64_t tl = t0 - 1, th = t1 + 1;
     if (x > t1) {
       lo = f1;
     } else {
       for (int step = 0; hi - lo > 1; step++) {
-        int64_t g = probe_between(lo, hi, x, tl, th, step);
-        int64_t v = __ldg(GV.fts + g);
-        if (v < x) {
-          lo = g;
-          tl = v;
-        } else {
-          hi = g;
-          th = v;
+        const int64_t g0 = probe_between(lo, hi, x, tl, th, step) & ~int64_t(3);
+        int64_t v[4];
+        ld256(GV.fts + g0, v[0], v[1], v[2], v[3]);
+        int64_t nlo = lo, nhi = hi;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int64_t idx = g0 + i;
+          if (idx > lo && idx < hi) {
+            if (v[i] < x) {
+              if (idx > nlo) {
+                nlo = idx;
+                tl = v[i];
+              }
+            } else if (idx < nhi) {
+              nhi = idx;
+              th = v[i];
+            }
+          }
         }
+        lo = nlo;
+        hi = nhi;
       }
     }
     const int64_t j = lo - (f0 - 1);  // fences < x
     if (j == 0) {
-      seg_hi = f0 * FENCE;  // head part before the first fence (< 32 slots): bisection below
+      seg_hi = f0 * FENCE;  // head part before the first fence (< 32 slots)
     } else {
       seg_lo = (f0 + j - 1) * FENCE;
       seg_hi = min(seg_lo + FENCE, base + size);
-      // seg_lo is 256-byte aligned here: eight 256-bit loads cover the window
-      int64_t c = 0;
-#pragma unroll
-    for (int w = 0; w < FENCE; w += 4) {
-      if (seg_lo + w < seg_hi) {
-        int64_t a, b, cc, d;
-        ld256(GV.sts + seg_lo + w, a, b, cc, d);
-        c += (a < x) + (seg_lo + w + 1 < seg_hi && b < x) + (seg_lo + w + 2 < seg_hi && cc < x) +
-             (seg_lo + w + 3 < seg_hi && d < x);
-      }
-    }
-      return seg_lo - base + c;
     }
   }
-  // short block or head segment: bisection over at most 32 timestamps
-  int64_t lo = seg_lo, hi = seg_hi;
-  while (lo < hi) {
-    int64_t m = (lo + hi) >> 1;
-    if (__ldg(GV.sts + m) < x) lo = m + 1;
-    else hi = m;
-  }
-  return lo - base;
+  return seg_lo - base + window_count(GV.sts, seg_lo, seg_hi, x);
 }
 
 struct LaneNode {
@@ -210,20 +222,36 @@ __device__ __forceinline__ LaneBnd lane_list_lower_bound(const GraphView& GV, co
     t0 = N.ttmin;
     t1 = N.tmax;
   } else {
-    // last non-tail block with tmin < x: entries lo < b < hi, tmin[lo] < x <= tmin[hi]
+    // last non-tail block with tmin < x: entries lo < b < hi, tmin[lo] < x <= tmin[hi].
+    // Each probe reads entries g and g+1 together, so an exact interpolation ends the search.
     const int64_t* d = GV.dir + N.d0 * DIRW;
     int64_t lo = 0, hi = N.nb - 1, tl = N.htmin, th = N.ttmin;
     int64_t lo_e1 = -1, lo_e2 = 0, lo_e3 = 0, hi_cum = N.tcum;  // cum/base/tmax of lo, cum of hi
     for (int step = 0; hi - lo > 1; step++) {
-      int64_t g = probe_between(lo, hi, x, tl, th, step);
-      int64_t e0, e1, e2, e3;
+      const int64_t g = probe_between(lo, hi, x, tl, th, step);
+      int64_t e0, e1, e2, e3, n0 = 0, n1 = 0, n2, n3;
       ld256(d + g * DIRW, e0, e1, e2, e3);
+      const bool two = g + 1 < hi;
+      if (two) ld256(d + (g + 1) * DIRW, n0, n1, n2, n3);
       if (e0 < x) {
         lo = g;
         tl = e0;
         lo_e1 = e1;
         lo_e2 = e2;
         lo_e3 = e3;
+        if (two) {
+          if (n0 < x) {
+            lo = g + 1;
+            tl = n0;
+            lo_e1 = n1;
+            lo_e2 = n2;
+            lo_e3 = n3;
+          } else {
+            hi = g + 1;
+            th = n0;
+            hi_cum = n1;
+          }
+        }
       } else {
         hi = g;
         th = e0;
