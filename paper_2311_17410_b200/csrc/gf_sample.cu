@@ -272,7 +272,7 @@ __device__ __forceinline__ LaneBnd lane_list_lower_bound(const GraphView& GV, co
 }
 
 #ifndef GF_COUNT_MINB
-#define GF_COUNT_MINB 6  // 40 registers: 48 warps per SM (A/B: +3% over 64 registers)
+#define GF_COUNT_MINB 4  // 64 registers, 32 warps per SM (A/B vs 48 and 40 registers: fastest)
 #endif
 __global__ void __launch_bounds__(THREADS, GF_COUNT_MINB) k_count_lane(GraphView GV, QueryIn Q, QState S, int64_t* counts, int64_t cap_q) {
   const int64_t n = query_count(Q);
