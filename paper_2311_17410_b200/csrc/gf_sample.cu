@@ -130,77 +130,72 @@ __device__ __forceinline__ void ld256(const void* p, int64_t& a, int64_t& b, int
 
 // interpolated probe index strictly inside (lo, hi) for key x with known
 // neighbour keys tl < x <= th
+#ifndef GF_INTERP_STEPS
+#define GF_INTERP_STEPS 2
+#endif
 __device__ __forceinline__ int64_t probe_between(int64_t lo, int64_t hi, int64_t x, int64_t tl, int64_t th, int step) {
-  if (step >= 2 || th <= tl) return (lo + hi) >> 1;  // interpolation twice, then bisection
+  if (step >= GF_INTERP_STEPS || th <= tl) return (lo + hi) >> 1;  // interpolation twice, then bisection
   float f = __fdividef((float)(x - tl), (float)(th - tl));
   int64_t g = lo + 1 + (int64_t)(f * (float)(hi - lo - 1));
   return g <= lo ? lo + 1 : (g >= hi ? hi - 1 : g);
 }
 
-// number of a[i] < x for i in [seg_lo, seg_hi) (sorted, seg_hi - seg_lo <= 32): aligned
-// 256-bit chunks, all independent, so one round trip for any alignment
-__device__ __forceinline__ int64_t window_count(const int64_t* __restrict__ a, int64_t seg_lo, int64_t seg_hi, int64_t x) {
-  int64_t c = 0;
-  const int64_t a0 = seg_lo & ~int64_t(3);
+// Bracketed interpolation search over a sorted int64 run.  On entry a[lo] < x <= a[hi]
+// (either end may be virtual, i.e. outside the run) with known values tl = a[lo], th = a[hi].
+// Each probe reads the aligned 4-entry chunk (one 256-bit load) around an interpolated index
+// and narrows the bracket with every entry in it; on exit hi = lo + 1 is the first index
+// with a[i] >= x and tl / th are the bracket's values.
+__device__ __forceinline__ void bracket_search(const int64_t* __restrict__ a, int64_t& lo, int64_t& hi, int64_t& tl,
+                                               int64_t& th, int64_t x) {
+  for (int step = 0; hi - lo > 1; step++) {
+    const int64_t g0 = probe_between(lo, hi, x, tl, th, step) & ~int64_t(3);
+    int64_t v[4];
+    ld256(a + g0, v[0], v[1], v[2], v[3]);
+    int64_t nlo = lo, nhi = hi;
 #pragma unroll
-  for (int w = 0; w < 36; w += 4) {
-    const int64_t p = a0 + w;
-    if (p < seg_hi) {
-      int64_t v0, v1, v2, v3;
-      ld256(a + p, v0, v1, v2, v3);
-      c += (p >= seg_lo && v0 < x) + (p + 1 >= seg_lo && p + 1 < seg_hi && v1 < x) +
-           (p + 2 >= seg_lo && p + 2 < seg_hi && v2 < x) + (p + 3 >= seg_lo && p + 3 < seg_hi && v3 < x);
+    for (int i = 0; i < 4; i++) {
+      const int64_t idx = g0 + i;
+      if (idx > lo && idx < hi) {
+        if (v[i] < x) {
+          if (idx > nlo) {
+            nlo = idx;
+            tl = v[i];
+          }
+        } else if (idx < nhi) {
+          nhi = idx;
+          th = v[i];
+        }
+      }
     }
+    lo = nlo;
+    hi = nhi;
   }
-  return c;
 }
 
 // count of timestamps < x in sts[base, base + size) whose values lie in [t0, t1]
 __device__ __forceinline__ int64_t lane_block_lower_bound(const GraphView& GV, int64_t base, int64_t size, int64_t t0,
                                                           int64_t t1, int64_t x) {
-  int64_t seg_lo = base, seg_hi = base + size;
+  if (x > t1) return size;
+  int64_t lo = base - 1, hi = base + size, tl = t0 - 1, th = t1 + 1;  // bracket in sts positions
+#ifndef GF_NO_FENCE
   if (size > FENCE) {
+    // the fences f0..f1 (fts[f] = sts[f * FENCE], a 32x smaller array that stays in L2)
+    // narrow the bracket to one 32-slot segment first
     const int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;
-    // fences f0..f1 are sorted; j = #fences < x.  Each probe reads the aligned 4-fence chunk
-    // around an interpolated index and narrows the bracket with every fence inside it.
-    int64_t lo = f0 - 1, hi = f1 + 1;  // virtual fences: fts[lo] < x <= fts[hi]
-    int64_t tl = t0 - 1, th = t1 + 1;
-    if (x > t1) {
-      lo = f1;
-    } else {
-      for (int step = 0; hi - lo > 1; step++) {
-        const int64_t g0 = probe_between(lo, hi, x, tl, th, step) & ~int64_t(3);
-        int64_t v[4];
-        ld256(GV.fts + g0, v[0], v[1], v[2], v[3]);
-        int64_t nlo = lo, nhi = hi;
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-          const int64_t idx = g0 + i;
-          if (idx > lo && idx < hi) {
-            if (v[i] < x) {
-              if (idx > nlo) {
-                nlo = idx;
-                tl = v[i];
-              }
-            } else if (idx < nhi) {
-              nhi = idx;
-              th = v[i];
-            }
-          }
-        }
-        lo = nlo;
-        hi = nhi;
-      }
+    int64_t flo = f0 - 1, fhi = f1 + 1, ftl = tl, fth = th;
+    bracket_search(GV.fts, flo, fhi, ftl, fth, x);
+    if (flo >= f0) {
+      lo = flo * FENCE;
+      tl = ftl;
     }
-    const int64_t j = lo - (f0 - 1);  // fences < x
-    if (j == 0) {
-      seg_hi = f0 * FENCE;  // head part before the first fence (< 32 slots)
-    } else {
-      seg_lo = (f0 + j - 1) * FENCE;
-      seg_hi = min(seg_lo + FENCE, base + size);
+    if (fhi <= f1) {
+      hi = fhi * FENCE;
+      th = fth;
     }
   }
-  return seg_lo - base + window_count(GV.sts, seg_lo, seg_hi, x);
+#endif
+  bracket_search(GV.sts, lo, hi, tl, th, x);
+  return hi - base;
 }
 
 struct LaneNode {
