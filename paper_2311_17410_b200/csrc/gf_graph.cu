@@ -521,7 +521,7 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
   int64_t old = g->slot_cap;
   GF_TRY(grow_array(g->slots, g->slots_used, nc, s));
   GF_TRY(grow_array(g->sts, g->slots_used, nc + 2 * FENCE, s));  // window loads may read past the end
-  GF_TRY(grow_array(g->fts, (g->slots_used + FENCE - 1) / FENCE, nc / FENCE + 1, s));
+  GF_TRY(grow_array(g->fts, (g->slots_used + FENCE - 1) / FENCE, nc / FENCE + 8, s));  // chunk loads read up to 3 past
   // unused capacity slots must read as invalid (delete scans the whole pool)
   GF_CUDA(cudaMemsetAsync(g->slots + old, 0, sizeof(Slot) * (size_t)(nc - old), s));
   g->slot_cap = nc;

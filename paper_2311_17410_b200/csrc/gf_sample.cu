@@ -140,35 +140,40 @@ __device__ __forceinline__ int64_t probe_between(int64_t lo, int64_t hi, int64_t
   return g <= lo ? lo + 1 : (g >= hi ? hi - 1 : g);
 }
 
-// Bracketed interpolation search over a sorted int64 run.  On entry a[lo] < x <= a[hi]
-// (either end may be virtual, i.e. outside the run) with known values tl = a[lo], th = a[hi].
-// Each probe reads the aligned 4-entry chunk (one 256-bit load) around an interpolated index
-// and narrows the bracket with every entry in it; on exit hi = lo + 1 is the first index
-// with a[i] >= x and tl / th are the bracket's values.
-__device__ __forceinline__ void bracket_search(const int64_t* __restrict__ a, int64_t& lo, int64_t& hi, int64_t& tl,
+// 32-bit run-relative form of probe_between
+__device__ __forceinline__ int probe_rel(int lo, int hi, int64_t x, int64_t tl, int64_t th, int step) {
+  if (step >= GF_INTERP_STEPS || th <= tl) return (lo + hi) >> 1;
+  const float f = __fdividef((float)(x - tl), (float)(th - tl));
+  const int g = lo + 1 + __float2int_rz(f * (float)(hi - lo - 1));
+  return min(max(g, lo + 1), hi - 1);
+}
+
+// Bracketed interpolation search over a sorted int64 run, indices relative to `run`
+// (whose absolute index has residue `mis` mod 4).  On entry run[lo] < x <= run[hi], either
+// end possibly virtual (outside the run), with known values tl = run[lo], th = run[hi].
+// Each probe reads the 32-byte-aligned 4-entry chunk around an interpolated index (one
+// 256-bit load).  Within the chunk the predicate "idx <= lo || (idx < hi && v < x)" is a
+// prefix of trues, so its popcount k places the boundary directly.  On exit hi = lo + 1 is
+// the first index with run[i] >= x.
+__device__ __forceinline__ void bracket_search(const int64_t* __restrict__ run, int mis, int& lo, int& hi, int64_t& tl,
                                                int64_t& th, int64_t x) {
   for (int step = 0; hi - lo > 1; step++) {
-    const int64_t g0 = probe_between(lo, hi, x, tl, th, step) & ~int64_t(3);
-    int64_t v[4];
-    ld256(a + g0, v[0], v[1], v[2], v[3]);
-    int64_t nlo = lo, nhi = hi;
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const int64_t idx = g0 + i;
-      if (idx > lo && idx < hi) {
-        if (v[i] < x) {
-          if (idx > nlo) {
-            nlo = idx;
-            tl = v[i];
-          }
-        } else if (idx < nhi) {
-          nhi = idx;
-          th = v[i];
-        }
-      }
+    const int g0 = ((probe_rel(lo, hi, x, tl, th, step) + mis) & ~3) - mis;
+    int64_t v0, v1, v2, v3;
+    ld256(run + g0, v0, v1, v2, v3);
+    const bool p0 = g0 <= lo || (g0 < hi && v0 < x);
+    const bool p1 = g0 + 1 <= lo || (g0 + 1 < hi && v1 < x);
+    const bool p2 = g0 + 2 <= lo || (g0 + 2 < hi && v2 < x);
+    const bool p3 = g0 + 3 <= lo || (g0 + 3 < hi && v3 < x);
+    const int k = (int)p0 + (int)p1 + (int)p2 + (int)p3;
+    if (k > 0 && g0 + k - 1 > lo) {
+      lo = g0 + k - 1;
+      tl = p2 ? (p3 ? v3 : v2) : (p1 ? v1 : v0);  // run[g0 + k - 1]
     }
-    lo = nlo;
-    hi = nhi;
+    if (k < 4 && g0 + k < hi) {
+      hi = g0 + k;
+      th = p1 ? (p2 ? v3 : v2) : (p0 ? v1 : v0);  // run[g0 + k]
+    }
   }
 }
 
@@ -176,26 +181,31 @@ __device__ __forceinline__ void bracket_search(const int64_t* __restrict__ a, in
 __device__ __forceinline__ int64_t lane_block_lower_bound(const GraphView& GV, int64_t base, int64_t size, int64_t t0,
                                                           int64_t t1, int64_t x) {
   if (x > t1) return size;
-  int64_t lo = base - 1, hi = base + size, tl = t0 - 1, th = t1 + 1;  // bracket in sts positions
+  // bracket relative to base; block sizes are bounded by the sizing law / one ingest batch
+  int lo = -1, hi = (int)size;
+  int64_t tl = t0 - 1, th = t1 + 1;
 #ifndef GF_NO_FENCE
   if (size > FENCE) {
     // the fences f0..f1 (fts[f] = sts[f * FENCE], a 32x smaller array that stays in L2)
     // narrow the bracket to one 32-slot segment first
-    const int64_t f0 = (base + FENCE - 1) / FENCE, f1 = (base + size - 1) / FENCE;
-    int64_t flo = f0 - 1, fhi = f1 + 1, ftl = tl, fth = th;
-    bracket_search(GV.fts, flo, fhi, ftl, fth, x);
-    if (flo >= f0) {
-      lo = flo * FENCE;
+    const int64_t f0 = (base + FENCE - 1) / FENCE;
+    const int nf = (int)((base + size - 1) / FENCE - f0) + 1;
+    int flo = -1, fhi = nf;
+    int64_t ftl = tl, fth = th;
+    bracket_search(GV.fts + f0, (int)(f0 & 3), flo, fhi, ftl, fth, x);
+    const int off = (int)(f0 * FENCE - base);  // first fenced slot, relative
+    if (flo >= 0) {
+      lo = off + flo * FENCE;
       tl = ftl;
     }
-    if (fhi <= f1) {
-      hi = fhi * FENCE;
+    if (fhi < nf) {
+      hi = off + fhi * FENCE;
       th = fth;
     }
   }
 #endif
-  bracket_search(GV.sts, lo, hi, tl, th, x);
-  return hi - base;
+  bracket_search(GV.sts + base, (int)(base & 3), lo, hi, tl, th, x);
+  return hi;
 }
 
 struct LaneNode {

@@ -32,6 +32,10 @@ int main() {
   long long* o; cudaMalloc(&o, 8);
   int64_t n = 200000000;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int gran : {128, 64, 32}) {
+  cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+  size_t got = 0; cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+  printf("L2 fetch granularity %d (reads back %zu)\n", gran, got);
   for (int mode = 0; mode < 4; mode++) {
     for (int rep = 0; rep < 3; rep++) {
       cudaEventRecord(e0);
@@ -43,6 +47,7 @@ int main() {
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       if (rep == 2) printf("mode %d: %.3f ms  %.2f G records/s  (%.1f GB/s of 32B records)\n", mode, ms, n / ms / 1e6, n * 32.0 / ms / 1e6);
     }
+  }
   }
   return 0;
 }
