@@ -199,13 +199,41 @@ def build_graph(cfg, src, dst, ts, world, rank, device):
     return g, e0.elapsed_time(e1)
 
 
-def run_step(g, roots, rts, R_base):
+def replay_roots_for_rank(src, dst, ts, R, rank):
+    """Replay roots: R/2 edges drawn uniformly (seed 1 + rank) from the whole
+    stream, src+dst at their own timestamps -- deep boundaries, as in harness.py:383-389."""
+    import torch
+
+    gen = torch.Generator(device=src.device)
+    gen.manual_seed(1 + rank)
+    idx = torch.randint(0, src.numel(), (R // 2,), generator=gen, device=src.device)
+    return torch.cat([src[idx], dst[idx]]).contiguous(), torch.cat([ts[idx], ts[idx]]).contiguous()
+
+
+def timed_steps(g, roots, rts, key_base, steps, policies=None):
+    """Device time (ms, CUDA events on the current stream) and sampled edges of `steps` steps."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    run_step(g, roots, rts, key_base, policies)
+    torch.cuda.synchronize()
+    a.record(stream)
+    edges = 0
+    for _ in range(steps):
+        edges += run_step(g, roots, rts, key_base, policies)[0]
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b), edges
+
+
+def run_step(g, roots, rts, R_base, policies=None):
     import paper_2311_17410_b200 as gf
 
     edges = 0
     queries = 0
     out = []
-    for pol in POLICIES:
+    for pol in policies or POLICIES:
         s = gf.sample_khop_device(g, roots, rts, FANOUTS, gf.SamplingPolicy(pol), seed=0, root_key_base=R_base)
         for lay in s.layers:
             edges += int(lay.neighbors.numel())
@@ -363,6 +391,17 @@ def bench_ours(args, cfg, world, rank, local):
         e2e = {"value": round(e2e_total / (e2e_ms / 1e3), 1), "unit": "sampled edges/s", "h2d_bytes_per_step": bi,
                "d2h_bytes_per_step": bo}
 
+    # secondary numbers (rank-local, not the headline): each policy alone, and the replay root set
+    per_policy = {}
+    for pol in POLICIES:
+        pms, pe = timed_steps(g, roots, rts, key_base, 3, (pol,))
+        per_policy[pol] = {"value": round(pe / (pms / 1e3), 1), "ms_per_step": round(pms / 3, 4)}
+    rroots, rrts = replay_roots_for_rank(src, dst, ts, R, rank)
+    rms, re_ = timed_steps(g, rroots, rrts, key_base, 3)
+    replay = {"value": round(re_ / (rms / 1e3), 1), "unit": "sampled edges/s", "ms_per_step": round(rms / 3, 4),
+              "roots": "R/2 uniformly drawn edges (seed 1+rank), src+dst at own ts (SURVEY.md 8(d)(ii))"}
+    del rroots, rrts
+
     ingest_eps = cfg["edges"] / (max_over_ranks(ingest_ms, world) / 1e3)
     info = g.info()
     cpu = None
@@ -401,6 +440,8 @@ def bench_ours(args, cfg, world, rank, local):
                          "pipeline_gbs": round(pipe_gbs, 1) if pipe_gbs else None,
                          "pipeline_frac": round(pipe_gbs / pk["hbm_gbs"], 4) if pipe_gbs else None},
             "kernels": kernels,
+            "per_policy": per_policy,
+            "replay": replay,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

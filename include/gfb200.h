@@ -207,6 +207,10 @@ gf_status gf_ftable_put(gf_ftable* t, const int64_t* d_ids, int64_t n, const flo
 gf_status gf_ftable_get(gf_ftable* t, const int64_t* d_ids, int64_t n, float* d_rows, uint8_t* d_found,
                         void* stream);
 gf_status gf_ftable_size(gf_ftable* t, int64_t* h_n);
+/* Stored ids in ascending order (NodeFeatureTable.ids_sorted, features.py:60-61;
+ * EdgeFeatureTable.ids, features.py:76-78) into d_ids[cap]; *h_n = the count.
+ * GF_ERANGE (with *h_n set) when cap is too small.  Used by save_*_features. */
+gf_status gf_ftable_ids(gf_ftable* t, int64_t* d_ids, int64_t cap, int64_t* h_n, void* stream);
 
 /* Harness fetch block (harness.py:438-446): cache.fetch(keys) -> table.get(miss)
  * -> cache.insert_batch(found rows).  d_values [n x dim] receives cached rows

@@ -40,7 +40,30 @@ from .sampling import (  # noqa: F401
     sample_layer,
 )
 from .cache import CacheSnapshot, VectorCache, load_cache  # noqa: F401
-from .features import EdgeFeatureTable, NodeFeatureTable, fetch_features  # noqa: F401
-from .synth import generate_synthetic_arrays, generate_synthetic_device  # noqa: F401
+from .features import (  # noqa: F401
+    EdgeFeatureTable,
+    FeatureFormatError,
+    NodeFeatureTable,
+    NodeMemoryTable,
+    fetch_features,
+    load_feature_table,
+    save_edge_features,
+    save_node_features,
+)
+from .synth import generate_synthetic, generate_synthetic_arrays, generate_synthetic_device  # noqa: F401
+from .metrics import access_distribution, coefficient_of_variation, jaccard  # noqa: F401
+from .partition import BalanceStats, PartitionSpec, assign, balance_stats, dispatch  # noqa: F401
+from .cluster import ClusterSim, ClusterSpec, Origin, RemoteRequestError, measure_cv, route  # noqa: F401
+from .harness import (  # noqa: F401
+    CacheConfig,
+    IngestFormatError,
+    RoundReport,
+    RunConfig,
+    bench,
+    load_config,
+    load_edge_csv,
+    run_continuous,
+    save_edge_csv,
+)
 
 __version__ = "0.1.0"

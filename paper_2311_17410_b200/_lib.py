@@ -76,6 +76,7 @@ _SIGS = {
     "gf_ftable_put": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "gf_ftable_get": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "gf_ftable_size": (c_int, [c_vp, P_i64]),
+    "gf_ftable_ids": (c_int, [c_vp, c_vp, c_i64, P_i64, c_vp]),
     "gf_fetch_features": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P_i64, P_i64, c_vp]),
     "gf_gather_rows": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp]),
 }

@@ -739,6 +739,32 @@ gf_status gf_ftable_size(gf_ftable* t, int64_t* h_n) {
   return GF_OK;
 }
 
+gf_status gf_ftable_ids(gf_ftable* t, int64_t* d_ids, int64_t cap, int64_t* h_n, void* stream) {
+  if (!t || !h_n) return fail(GF_EINVAL, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = t->kind == 0 ? t->count : t->n;
+  *h_n = n;
+  if (n > cap) return fail(GF_ERANGE, "id buffer too small");
+  if (n == 0) return GF_OK;
+  if (!d_ids) return fail(GF_EINVAL, "NULL id buffer");
+  DeviceGuard dg(t->device);
+  if (t->kind == 1) {
+    GF_CUDA(cudaMemcpyAsync(d_ids, t->ids, 8 * n, cudaMemcpyDeviceToDevice, s));
+  } else {
+    // ascending ids whose present flag is set (stable selection over 0..cap-1)
+    Scratch sb(s);
+    size_t tmp = 0;
+    GF_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, cub::CountingInputIterator<int64_t>(0), t->present, d_ids,
+                                       (int64_t*)nullptr, t->cap, s));
+    GF_TRY(sb.alloc(tmp + 64));
+    int64_t* nsel = sb.as<int64_t>();
+    GF_CUDA(cub::DeviceSelect::Flagged((char*)sb.p + 64, tmp, cub::CountingInputIterator<int64_t>(0), t->present,
+                                       d_ids, nsel, t->cap, s));
+  }
+  GF_CUDA(cudaStreamSynchronize(s));
+  return GF_OK;
+}
+
 gf_status gf_ftable_put(gf_ftable* t, const int64_t* d_ids, int64_t n, const float* d_rows, void* stream) {
   if (!t) return fail(GF_EINVAL, "NULL argument");
   if (n == 0) return GF_OK;

@@ -1,17 +1,30 @@
-"""Device feature tables and the harness fetch block.
+"""Device feature tables, the harness fetch block, and the TGFF feature file.
 
-``NodeFeatureTable`` / ``EdgeFeatureTable`` mirror
-/root/reference/pkg/src/ctdg/features.py:27-120 (same names, zeros + found
+``NodeFeatureTable`` / ``EdgeFeatureTable`` / ``NodeMemoryTable`` mirror
+/root/reference/pkg/src/ctdg/features.py:27-157 (same names, zeros + found
 mask for unknown ids, strictly increasing edge ids) with rows in HBM.
 ``fetch_features`` is the per-minibatch block of harness.py:438-446:
 cache.fetch -> table.get(miss) -> cache.insert_batch(found), in one call.
+``save_features`` / ``load_features`` / ``load_feature_table`` write and read the
+reference's TGFF byte format (features.py:159-207), byte for byte.
 """
 
 from __future__ import annotations
 
+import csv
 import ctypes
+import struct
 
 import numpy as np
+
+FEATURE_MAGIC = b"TGFF"  # features.py:17-20
+FEATURE_VERSION = 1
+KIND_NODE = 0
+KIND_EDGE = 1
+
+
+class FeatureFormatError(ValueError):
+    """Raised for malformed feature files (features.py:23-24)."""
 
 from ._lib import check, load, ptr, stream_ptr
 
@@ -48,6 +61,16 @@ class _DeviceTable:
         n = ctypes.c_int64()
         check(load().gf_ftable_size(self._h, ctypes.byref(n)))
         return int(n.value)
+
+    def _stored_ids(self):
+        """Stored ids ascending, as a device tensor (gf_ftable_ids)."""
+        import torch
+
+        n = len(self)
+        out = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+        got = ctypes.c_int64()
+        check(load().gf_ftable_ids(self._h, ptr(out), n, ctypes.byref(got), stream_ptr()))
+        return out[: got.value]
 
     def _put(self, ids, rows):
         import torch
@@ -93,6 +116,13 @@ class NodeFeatureTable(_DeviceTable):
     def set_many(self, ids, rows) -> None:
         self._put(ids, rows)
 
+    def __contains__(self, node: int) -> bool:
+        return bool(self.get([int(node)])[1][0])
+
+    def ids_sorted(self) -> np.ndarray:
+        """features.py:60-61."""
+        return self._stored_ids().cpu().numpy()
+
 
 class EdgeFeatureTable(_DeviceTable):
     """features.py:64-120 (append-only, strictly increasing ids; binary-search lookup)."""
@@ -101,6 +131,40 @@ class EdgeFeatureTable(_DeviceTable):
 
     def append(self, ids, rows) -> None:
         self._put(ids, rows)
+
+    @property
+    def ids(self) -> np.ndarray:
+        """features.py:76-78."""
+        return self._stored_ids().cpu().numpy()
+
+    @property
+    def values(self) -> np.ndarray:
+        """features.py:80-82 (rows in id order)."""
+        ids = self._stored_ids()
+        if ids.numel() == 0:
+            return np.zeros((0, self.dim), dtype=np.float32)
+        return self.get(ids)[0].cpu().numpy()
+
+
+class NodeMemoryTable(NodeFeatureTable):
+    """features.py:123-156: per-node state rows in HBM (upsert) plus the host-side
+    ``last_update`` map the reference exposes."""
+
+    def __init__(self, dim: int, device=None):
+        super().__init__(dim, device)
+        self.last_update: dict[int, int] = {}
+
+    def update(self, ids, rows, timestamps) -> None:
+        ids_np = np.asarray(ids.cpu() if hasattr(ids, "cpu") else ids, dtype=np.int64)
+        shape = tuple(rows.shape) if hasattr(rows, "shape") else np.asarray(rows).shape
+        if shape != (len(ids_np), self.dim):
+            raise ValueError(f"rows must be ({len(ids_np)}, {self.dim}), got {shape}")
+        if len(ids_np) == 0:
+            return
+        self._put(ids, rows)
+        ts_np = np.asarray(timestamps.cpu() if hasattr(timestamps, "cpu") else timestamps, dtype=np.int64)
+        for node, t in zip(ids_np.tolist(), ts_np.tolist()):
+            self.last_update[node] = t
 
 
 def fetch_features(cache, table, keys, stream=None):
@@ -120,3 +184,79 @@ def fetch_features(cache, table, keys, stream=None):
     check(load().gf_fetch_features(cache.handle, table.handle, ptr(k), n, ptr(values), ptr(hit), ctypes.byref(nm),
                                    ctypes.byref(adm), stream_ptr(stream)))
     return values, hit[:n].bool(), int(nm.value), int(adm.value)
+
+
+# ---------------------------------------------------------------------------
+# TGFF feature files (features.py:159-221); host byte format, identical bytes
+# ---------------------------------------------------------------------------
+
+_HDR = "<IBIQ"
+
+
+def save_features(sink, kind: int, dim: int, ids, rows) -> None:
+    """features.py:159-166: magic, version, kind, dim, count, ids (u64), f32 rows."""
+    ids = np.asarray(ids, dtype="<i8")
+    rows = np.ascontiguousarray(rows, dtype="<f4")
+    sink.write(FEATURE_MAGIC)
+    sink.write(struct.pack(_HDR, FEATURE_VERSION, kind, dim, len(ids)))
+    sink.write(ids.astype("<u8").tobytes())
+    sink.write(rows.tobytes())
+
+
+def load_features(source):
+    """features.py:169-184 -> (kind, dim, ids int64, rows f32 [count, dim])."""
+    data = source.read() if hasattr(source, "read") else bytes(source)
+    if data[:4] != FEATURE_MAGIC:
+        raise FeatureFormatError("bad feature-file magic")
+    version, kind, dim, count = struct.unpack_from(_HDR, data, 4)
+    if version != FEATURE_VERSION:
+        raise FeatureFormatError(f"unsupported feature-file version {version}")
+    pos = 4 + struct.calcsize(_HDR)
+    if len(data) != pos + count * 8 + count * dim * 4:
+        raise FeatureFormatError("feature file length mismatch")
+    ids = np.frombuffer(data, dtype="<u8", count=count, offset=pos).astype(np.int64)
+    rows = np.frombuffer(data, dtype="<f4", count=count * dim, offset=pos + count * 8)
+    return kind, dim, ids, rows.reshape(count, dim).copy()
+
+
+def save_node_features(table: NodeFeatureTable, sink) -> None:
+    """features.py:187-190 (ids ascending)."""
+    ids = table._stored_ids()
+    rows = table.get(ids)[0].cpu().numpy() if ids.numel() else np.zeros((0, table.dim), np.float32)
+    save_features(sink, KIND_NODE, table.dim, ids.cpu().numpy(), rows)
+
+
+def save_edge_features(table: EdgeFeatureTable, sink) -> None:
+    """features.py:193-194."""
+    save_features(sink, KIND_EDGE, table.dim, table.ids, table.values)
+
+
+def load_feature_table(source, device=None):
+    """features.py:197-207: a device table of the file's kind."""
+    kind, dim, ids, rows = load_features(source)
+    if kind == KIND_NODE:
+        table = NodeFeatureTable(dim, device)
+        if len(ids):
+            table.set_many(ids, rows)
+        return table
+    if kind == KIND_EDGE:
+        table = EdgeFeatureTable(dim, device)
+        if len(ids):
+            table.append(ids, rows)
+        return table
+    raise FeatureFormatError(f"unknown feature kind {kind}")
+
+
+def load_features_csv(path, dim: int):
+    """features.py:210-221: id,v0,v1,... per line -> (ids int64, rows f32)."""
+    ids, rows = [], []
+    with open(path, newline="") as fh:
+        for row in csv.reader(fh):
+            if not row or row[0].startswith("#"):
+                continue
+            ids.append(int(row[0]))
+            vals = [float(x) for x in row[1:]]
+            if len(vals) != dim:
+                raise FeatureFormatError(f"expected {dim} values, got {len(vals)}")
+            rows.append(vals)
+    return np.array(ids, dtype=np.int64), np.array(rows, dtype=np.float32)

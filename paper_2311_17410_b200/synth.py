@@ -75,3 +75,10 @@ def generate_synthetic_device(nodes: int, edges: int, skew: float = 2.2, time_sp
         loops = loops[src[loops] == dst[loops]]
     ts = torch.sort(torch.randint(0, time_span, (edges,), device=device, generator=gen)).values
     return src.to(torch.int64), dst.to(torch.int64), ts.to(torch.int64)
+
+
+def generate_synthetic(nodes: int, edges: int, skew: float = 2.2, time_span: int = 1_000_000, seed: int = 0,
+                       src_skew: float | None = None) -> list[tuple[int, int, int]]:
+    """synth.py:15-53 signature and return type: the stream as (src, dst, ts) tuples."""
+    s, d, t = generate_synthetic_arrays(nodes, edges, skew, time_span, seed, src_skew)
+    return list(zip(s.tolist(), d.tolist(), t.tolist()))
