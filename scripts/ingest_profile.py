@@ -1,0 +1,56 @@
+"""Where ingest time goes: GDELT-law stream, 100K-edge batches through gf_graph_add_edges.
+
+Prints edges/s (device events around the loop), the per-kernel device time from the library's
+launch profiler, and host wall time per batch.  Usage: python scripts/ingest_profile.py [edges] [batch]
+"""
+
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2311_17410_b200 as gf  # noqa: E402
+from paper_2311_17410_b200 import _lib  # noqa: E402
+
+E = int(sys.argv[1]) if len(sys.argv) > 1 else 20_000_000
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
+dev = torch.device("cuda", 0)
+src, dst, ts = gf.generate_synthetic_device(17_000, E, 2.2, 175_200, seed=0, src_skew=2.2, device=dev)
+g = gf.DynamicGraph(directed=True, tau=8192, device=dev)
+g.reserve(17_000, 17_000 * 16 + E // 8192 + 1024, E + min(17_000 * 8192, E // 2))
+half = E // 2
+for lo in range(0, half, B):  # warm half
+    g.add_edges_arrays(src[lo:lo + B], dst[lo:lo + B], ts[lo:lo + B])
+torch.cuda.synchronize()
+_lib.profile_enable(True)
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+t0 = time.perf_counter()
+a.record()
+nb = 0
+for lo in range(half, E, B):
+    g.add_edges_arrays(src[lo:lo + B], dst[lo:lo + B], ts[lo:lo + B])
+    nb += 1
+b.record()
+torch.cuda.synchronize()
+wall = time.perf_counter() - t0
+prof = _lib.profile_summary()
+_lib.profile_enable(False)
+ms = a.elapsed_time(b)
+print(f"profiled: {nb} batches of {B}: {ms:.1f} ms device, {wall * 1e3:.1f} ms wall -> {(E - half) / (ms / 1e3) / 1e6:.1f} M edges/s"
+      f" ({ms / nb * 1e3:.0f} us/batch)")
+tot = sum(v[1] for v in prof.values())
+for k, (c, kms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+    print(f"  {k:40s} {c:6d} launches {kms:8.2f} ms  {kms / nb * 1e3:7.1f} us/batch")
+print(f"  kernel sum {tot:.1f} ms = {tot / nb * 1e3:.0f} us/batch")
+# unprofiled rate
+torch.cuda.synchronize()
+g2 = gf.DynamicGraph(directed=True, tau=8192, device=dev)
+g2.reserve(17_000, 17_000 * 16 + E // 8192 + 1024, E + min(17_000 * 8192, E // 2))
+a.record()
+for lo in range(0, E, B):
+    g2.add_edges_arrays(src[lo:lo + B], dst[lo:lo + B], ts[lo:lo + B])
+b.record()
+torch.cuda.synchronize()
+print(f"unprofiled: {E / (a.elapsed_time(b) / 1e3) / 1e6:.1f} M edges/s, {a.elapsed_time(b) / (E // B) * 1e3:.0f} us/batch")
