@@ -336,9 +336,10 @@ def bench_ours(args, cfg, world, rank, local):
         tag = name[len(raw) + 1:-1] if "[" in name else None
         base = re.sub(r"[()]|<.*>", "", raw).strip()
         ent = {"launches": cnt, "ms": round(kms, 4), "share": round(kms / tot_ms, 4) if tot_ms else None}
-        if tag in layer_qs and (base.startswith("k_count") or base.startswith("k_write")):
+        if tag in layer_qs and base.startswith(("k_count", "k_write", "k_sample_fused")):
             q_l, s_l = layer_qs[tag]
-            b = BYTES_PER_QUERY * q_l if base.startswith("k_count") else BYTES_PER_EDGE * s_l
+            b = (BYTES_PER_QUERY * q_l if base.startswith("k_count") else
+                 BYTES_PER_EDGE * s_l if base.startswith("k_write") else BYTES_PER_QUERY * q_l + BYTES_PER_EDGE * s_l)
             ent["alg_bytes"] = b
             ent["achieved_gbs"] = round(b / (kms / 1e3) / 1e9, 1) if kms > 0 else None
             base_bytes[base] = base_bytes.get(base, 0) + b
@@ -347,7 +348,7 @@ def bench_ours(args, cfg, world, rank, local):
     dom_name = max(base_bytes, key=lambda k: base_ms[k])
     achieved = base_bytes[dom_name] / (base_ms[dom_name] / 1e3) / 1e9
     traffic = load_traffic().get(dom_name)
-    pipe_ms = sum(v for k, v in base_ms.items() if k.startswith(("k_count", "k_write", "k_total", "cub_scan")))
+    pipe_ms = sum(v for k, v in base_ms.items() if k.startswith(("k_count", "k_write", "k_total", "cub_scan", "k_sample_fused")))
     pipe_gbs = (BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p) / (pipe_ms / 1e3) / 1e9 if pipe_ms else None
 
     # e2e through the public API with host (pinned) buffers: H2D roots, sample, D2H every layer
@@ -436,7 +437,7 @@ def bench_ours(args, cfg, world, rank, local):
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
                          "peak_source": pk["source"],
-                         "alg_bytes": f"count kernel {BYTES_PER_QUERY} B/query, write kernel {BYTES_PER_EDGE} B/sampled edge (SURVEY.md 8(d))",
+                         "alg_bytes": f"{BYTES_PER_QUERY} B/query + {BYTES_PER_EDGE} B/sampled edge (SURVEY.md 8(d)); fused kernel = both",
                          "pipeline_gbs": round(pipe_gbs, 1) if pipe_gbs else None,
                          "pipeline_frac": round(pipe_gbs / pk["hbm_gbs"], 4) if pipe_gbs else None},
             "kernels": kernels,

@@ -545,6 +545,225 @@ __global__ void __launch_bounds__(THREADS) k_write_coop(GraphView GV, QueryIn Q,
   }
 }
 
+// ===================== fused single-pass layer (fast path) ====================
+// k_count_lane + scan + k_write_coop in one kernel: each CTA takes the next
+// 256-query tile by ticket (so every lower tile is already resident), runs the
+// lane-per-query window search, scans its counts, publishes the tile aggregate,
+// selects its slots into shared memory, resolves its output base by decoupled
+// look-back over the predecessors' published aggregates, then gathers and
+// stores the tile's CSR range.  The per-query search state never leaves
+// registers (no QState round trip), offsets are written once, and the
+// latency-bound search of one tile overlaps the bandwidth-bound gather of
+// others on the same SM.
+
+constexpr uint64_t TS_AGG = 1ull << 62, TS_INC = 2ull << 62, TS_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct TileCtl {
+  uint64_t* status;  // per tile: flag (bits 63..62) | value; zeroed before the launch
+  unsigned* ticket;  // zeroed before the launch
+  int64_t* total;    // layer total (written by the tile holding the last query)
+};
+
+// list position -> pool slot for a selected position (regular lists: closed form; else directory)
+__device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
+  const int64_t* dd = GV.dir + d0 * DIRW;
+  int64_t b, cum;
+  if (irregular) {
+    b = dir_block_of(GV, d0, nb, p);
+    cum = __ldg(dd + b * DIRW + 1);
+  } else {
+    b = law_block(GV.law, p);
+    cum = law_cum(GV.law, b);
+  }
+  return (uint32_t)(__ldg(dd + b * DIRW + 2) + (p - cum));
+}
+
+#ifndef GF_FUSED_MINB
+#define GF_FUSED_MINB 4
+#endif
+#ifndef GF_GATHER_UNROLL
+#define GF_GATHER_UNROLL 2
+#endif
+
+__global__ void __launch_bounds__(THREADS, GF_FUSED_MINB) k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
+  constexpr int NW = THREADS / 32;
+  __shared__ uint32_t s_sel[NW][32][KMAX];
+  __shared__ uint8_t s_owner[NW][32 * KMAX];
+  __shared__ uint64_t s_key[NW][32];
+  __shared__ int32_t s_pre[NW][32];
+  __shared__ int32_t s_wsum[NW];
+  __shared__ unsigned s_tile;
+  __shared__ int64_t s_base;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(C.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t n = query_count(Q);
+  if (tile * THREADS >= n) return;
+  const int64_t q = tile * THREADS + threadIdx.x;
+
+  // ---- window search (k_count_lane) ----
+  int k = 0;
+  int64_t lo = 0, hi = 0, slot_hi = 0, cum = 0, d0 = 0, nb = 0;
+  bool irregular = false;
+  uint64_t qkey = 0;
+  if (q < n) {
+    const int64_t v = Q.src[q];
+    const int64_t te = Q.t_end[q];
+    qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
+    if (v >= 0 && v < GV.num_nodes) {
+      const int64_t* r = GV.nrec + v * NREC;
+      LaneNode N;
+      int64_t w2, w3;
+      ld256(r, N.d0, N.ns, w2, N.first);
+      ld256(r + 4, N.tcum, N.tbase, N.ttmin, N.tmax);
+      ld256(r + 8, N.htmin, w3, w3, w3);
+      N.nb = w2 & 0xffffffffll;
+      N.valid = (w2 & NREC_VALID) != 0;
+      N.irregular = (w2 & NREC_IRREG) != 0;
+      if (N.valid && N.nb > 0) {  // sampling.py:153-155
+        const LaneBnd h = lane_list_lower_bound(GV, N, te);
+        const int64_t tsr = t_start_of(Q, q, te);
+        lo = (tsr == GF_TS_MIN) ? N.first : lane_list_lower_bound(GV, N, tsr).pos;
+        if (h.pos > lo) {
+          k = (int)min(h.pos - lo, Q.fanout);
+          hi = h.pos;
+          slot_hi = h.base + (h.pos - 1 - h.cum);
+          cum = h.cum;
+          d0 = N.d0;
+          nb = N.nb;
+          irregular = N.irregular;
+        }
+      }
+    }
+  }
+
+  // ---- tile scan of the counts; publish the aggregate ----
+  int incl = k;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[w] = incl;
+  __syncthreads();
+  int wpre = 0, agg = 0;
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const int x = s_wsum[i];
+    wpre += (i < w) ? x : 0;
+    agg += x;
+  }
+  if (threadIdx.x == 0) st_relaxed(C.status + tile, (tile == 0 ? TS_INC : TS_AGG) | (uint64_t)agg);
+
+  // ---- selection into shared memory (independent of the output base) ----
+  const int pre = incl - k;
+  s_pre[w][lane] = pre;
+  s_key[w][lane] = qkey;
+  for (int i = 0; i < k; i++) s_owner[w][pre + i] = (uint8_t)lane;
+  if (k > 0) {
+    const int64_t nv = hi - lo;
+    if (Q.policy == GF_POLICY_RECENT || k == nv) {
+      // newest first: output r is list position hi-1-r (sampling.py:188-190)
+      const int64_t inblk = hi - cum;
+#pragma unroll
+      for (int r = 0; r < KMAX; r++) {
+        if (r < k) s_sel[w][lane][r] = (r < inblk) ? (uint32_t)(slot_hi - r) : pool_slot_of(GV, true, d0, nb, hi - 1 - r);
+      }
+    } else {
+      // uniform / time_window (k < nv): Floyd over candidate indices 0..nv-1,
+      // draws t_i in [0, nv-k+i] from Philox block i/2 (two draws per block)
+      int32_t pick[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; i += 2) {
+        if (i < k) {
+          uint32_t c[4] = {(uint32_t)(i >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+          philox4x32_10(c, (uint32_t)Q.seed, (uint32_t)(Q.seed >> 32));
+          const int64_t t0 = (int64_t)bounded64((uint64_t)c[0] | ((uint64_t)c[1] << 32), (uint64_t)(nv - k + i + 1));
+          bool dup0 = false;
+#pragma unroll
+          for (int j = 0; j < KMAX; j++) dup0 |= (j < i) && pick[j] == (int32_t)t0;
+          pick[i] = dup0 ? (int32_t)(nv - k + i) : (int32_t)t0;
+          if (i + 1 < k) {
+            const int64_t t1 = (int64_t)bounded64((uint64_t)c[2] | ((uint64_t)c[3] << 32), (uint64_t)(nv - k + i + 2));
+            bool dup1 = false;
+#pragma unroll
+            for (int j = 0; j < KMAX; j++) dup1 |= (j < i + 1) && pick[j] == (int32_t)t1;
+            pick[i + 1] = dup1 ? (int32_t)(nv - k + i + 1) : (int32_t)t1;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < KMAX; i++)
+        if (i < k) s_sel[w][lane][i] = pool_slot_of(GV, irregular, d0, nb, lo + pick[i]);
+    }
+  }
+
+  // ---- decoupled look-back: output base of this tile ----
+  if (w == 0) {
+    int64_t excl = 0;
+    if (tile > 0) {
+      int64_t end = tile - 1;
+      while (true) {
+        const int64_t idx = end - lane;  // lane 0 = nearest predecessor
+        uint64_t st;
+        do {
+          st = idx >= 0 ? ld_relaxed(C.status + idx) : TS_INC;
+        } while (__any_sync(0xffffffffu, (st >> 62) == 0));
+        const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        const int first = inc ? __ffs(inc) - 1 : 31;
+        int64_t v = lane <= first ? (int64_t)(st & TS_VAL) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+        end -= 32;
+      }
+      if (lane == 0) st_relaxed(C.status + tile, TS_INC | (uint64_t)(excl + agg));
+    }
+    if (lane == 0) s_base = excl;
+  }
+  __syncthreads();
+  const int64_t base = s_base;
+  const int64_t out = base + wpre + pre;
+  if (q < n) {
+    const_cast<int64_t*>(O.offsets)[q + 1] = out + k;
+    if (q == n - 1) *C.total = out + k;
+  }
+
+  // ---- cooperative gather + CSR store of the warp's contiguous range ----
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const int64_t out0 = base + wpre;
+  __syncwarp();
+  int e = lane;
+  for (; e + 32 * (GF_GATHER_UNROLL - 1) < total; e += 32 * GF_GATHER_UNROLL) {
+    Slot s[GF_GATHER_UNROLL];
+    int j[GF_GATHER_UNROLL];
+#pragma unroll
+    for (int u = 0; u < GF_GATHER_UNROLL; u++) {
+      j[u] = s_owner[w][e + 32 * u];
+      s[u] = load_slot(GV.slots + s_sel[w][j[u]][e + 32 * u - s_pre[w][j[u]]]);
+    }
+#pragma unroll
+    for (int u = 0; u < GF_GATHER_UNROLL; u++)
+      store_out(O, out0 + e + 32 * u, s[u], s_key[w][j[u]], e + 32 * u - s_pre[w][j[u]]);
+  }
+  for (; e < total; e += 32) {
+    const int jj = s_owner[w][e];
+    const int i = e - s_pre[w][jj];
+    store_out(O, out0 + e, load_slot(GV.slots + s_sel[w][jj][i]), s_key[w][jj], i);
+  }
+}
+
 // ========================== general path (deletions) =========================
 
 __device__ __forceinline__ bool node_ok(const GraphView& G_, int64_t v) {
@@ -750,6 +969,11 @@ int64_t grid_for_queries(int64_t cap_q, int per_query_threads) {
 
 // One layer: count -> scan -> total -> write.  cap_q bounds the query count
 // (exact when Q.n_dev is NULL).  total: device slot for this layer's total.
+bool fused_enabled() {
+  static const bool on = getenv("GF_NO_FUSED") == nullptr;
+  return on;
+}
+
 gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_offsets, const LayerOut& O, int64_t* total,
                        cudaStream_t s) {
   GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
@@ -759,13 +983,22 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   }
   Scratch sb(s);
   Arena A;
-  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + 4096));
+  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + (size_t)cap_q / 32 + 8192));
   A.base = sb.as<char>();
   QState S{A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q),
            A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q)};
   int64_t* counts = A.take<int64_t>(cap_q);
   GraphView GV = view_of(g);
   const bool fast = !g->any_deleted;
+  if (fast && Q.fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled()) {
+    const int64_t tiles = (cap_q + THREADS - 1) / THREADS;
+    TileCtl C{reinterpret_cast<uint64_t*>(A.take<int64_t>(tiles + 1)), nullptr, total};
+    C.ticket = reinterpret_cast<unsigned*>(C.status + tiles);
+    GF_CUDA(cudaMemsetAsync(C.status, 0, sizeof(uint64_t) * (tiles + 1), s));
+    GF_CUDA(cudaMemsetAsync(total, 0, sizeof(int64_t), s));
+    GF_LAUNCH(k_sample_fused, tiles, THREADS, 0, s, GV, Q, O, C);
+    return GF_OK;
+  }
   if (fast) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
   else GF_LAUNCH(k_count_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, counts, cap_q);
   cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
