@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <vector>
 
 #include "gf_graph.cuh"
@@ -30,7 +31,9 @@ struct IngestCounters {
   long long new_slots;    // slots to allocate
   long long dir_need;     // directory entries to allocate
   long long max_eid;      // max preassigned accepted id
+  long long abort;        // sync-free path: ABORT_* bits, nothing was mutated
 };
+constexpr long long ABORT_NODES = 1, ABORT_CAP = 2;
 
 template <class T>
 gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
@@ -84,7 +87,8 @@ __global__ void k_minmax(const int64_t* __restrict__ src, const int64_t* __restr
 
 // one event per (edge, stored endpoint), in the reference's append order
 __global__ void k_make_events(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n, int directed,
-                              uint32_t* keys, uint32_t* vals) {
+                              uint32_t* keys, uint32_t* vals, const IngestCounters* c) {
+  if (c->abort) return;
   int64_t E = directed ? n : 2 * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t j = directed ? e : (e >> 1);
@@ -111,6 +115,7 @@ __global__ void k_heads(const uint32_t* __restrict__ keys, int64_t E, int32_t* h
 __global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl,
                            int64_t E, int directed, const int64_t* __restrict__ ts, const int64_t* tail, const int64_t* bsize,
                            const int64_t* btmax, int64_t* seg_start, IngestCounters* c) {
+  if (c->abort) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t s = incl[i] - 1;
     bool head = (i == 0) || keys[i] != keys[i - 1];
@@ -128,13 +133,14 @@ __global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __
 }
 
 __global__ void k_accept_all(uint8_t* acc, int64_t n, const IngestCounters* c) {
-  if (c->viol) return;
+  if (c->viol || c->abort) return;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
 }
 
 __global__ void k_tmax_init(int64_t* tm, int64_t num_nodes, const int64_t* tail, const int64_t* bsize, const int64_t* btmax,
                             const IngestCounters* c) {
-  if (!c->viol) return;
+  if (!c->viol || c->abort) return;
+  if (c->maxv + 1 > num_nodes) num_nodes = c->maxv + 1;  // nodes this batch creates have no tail
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < num_nodes; v += (int64_t)gridDim.x * blockDim.x)
     tm[v] = node_tmax(tail, bsize, btmax, v);
 }
@@ -142,7 +148,7 @@ __global__ void k_tmax_init(int64_t* tm, int64_t num_nodes, const int64_t* tail,
 // Sequential chronology resolve (storage.py:426-437): only when a batch may reject.
 __global__ void k_accept_serial(const int64_t* src, const int64_t* dst, const int64_t* ts, int64_t n, int directed,
                                 int64_t* tm, uint8_t* acc, const IngestCounters* c) {
-  if (!c->viol || threadIdx.x || blockIdx.x) return;
+  if (!c->viol || c->abort || threadIdx.x || blockIdx.x) return;
   for (int64_t j = 0; j < n; j++) {
     int64_t s = src[j], d = dst[j], t = ts[j];
     bool ok = t >= tm[s] && (directed || t >= tm[d]);
@@ -155,7 +161,8 @@ __global__ void k_accept_serial(const int64_t* src, const int64_t* dst, const in
 }
 
 __global__ void k_keep(const uint32_t* __restrict__ vals, int64_t E, int directed, const uint8_t* __restrict__ acc,
-                       int64_t* keep) {
+                       int64_t* keep, const IngestCounters* c) {
+  if (c->abort) return;  // vals may be uninitialised (no events were made)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x)
     keep[i] = acc[ev_edge(vals[i], directed)];
   if (blockIdx.x == 0 && threadIdx.x == 0) keep[E] = 0;
@@ -181,6 +188,7 @@ __global__ void k_eids(const uint8_t* __restrict__ acc, const int64_t* __restric
 __global__ void k_compact(const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl, const int64_t* __restrict__ cpos,
                           const int64_t* __restrict__ keep, const int64_t* __restrict__ seg_start, int64_t E,
                           const IngestCounters* c, uint32_t* ce_ev, int64_t* ce_pend, int32_t* ce_seg) {
+  if (c->abort) return;
   int64_t nseg = c->num_segs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
     if (!keep[i]) continue;
@@ -214,7 +222,8 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
                        const int64_t* __restrict__ cpos, const int64_t* __restrict__ ce_pend, int64_t E,
                        const IngestCounters* c, const int64_t* tail, const int64_t* bsize, const int64_t* bcap,
                        const int64_t* degree, const int64_t* num_blocks, const int64_t* dir_cap, int kind, int64_t tau,
-                       int64_t param, SegPlan P, const int64_t* nslots, uint8_t* nflags) {
+                       int64_t param, SegPlan P, const int64_t* nslots) {
+  if (c->abort) return;
   int64_t nseg = c->num_segs;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     int64_t st = seg_start[s], en = (s + 1 < nseg) ? seg_start[s + 1] : E;
@@ -242,9 +251,6 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
     }
     P.nb_new[s] = blocks;
     P.slots_new[s] = slots;
-    // a block allocated while live degree != slots written (a deletion happened) or by
-    // batch sizing leaves the closed-form position -> block law (SizingLaw)
-    if (blocks > 0 && (kind == GF_SIZING_BATCH || degree[v] != nslots[v])) nflags[v] |= 1;
     int64_t need = num_blocks[v] + blocks;
     int64_t dc = dir_cap[v];
     if (need > dc) {
@@ -258,10 +264,20 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
 }
 
 __global__ void k_totals(const int64_t* blkoff, const int64_t* slotsoff, const int64_t* diroff, int64_t E, IngestCounters* c) {
-  if (threadIdx.x || blockIdx.x) return;
+  if (threadIdx.x || blockIdx.x || c->abort) return;
   c->new_blocks = blkoff[E];
   c->new_slots = slotsoff[E];
   c->dir_need = diroff[E];
+}
+
+// sync-free path: totals + capacity check against the host-known pool state
+__global__ void k_totals_check(const int64_t* blkoff, const int64_t* slotsoff, const int64_t* diroff, int64_t E,
+                               int64_t slots_free, int64_t dir_free, IngestCounters* c) {
+  if (threadIdx.x || blockIdx.x || c->abort) return;
+  c->new_blocks = blkoff[E];
+  c->new_slots = slotsoff[E];
+  c->dir_need = diroff[E];
+  if (c->new_slots > slots_free || c->dir_need > dir_free) c->abort |= ABORT_CAP;
 }
 
 struct Recs {
@@ -277,7 +293,8 @@ struct Recs {
 __global__ void k_enumerate(const int64_t* __restrict__ ce_pend, const uint32_t* __restrict__ ce_ev, const IngestCounters* c,
                             const int64_t* __restrict__ blkoff, const int64_t* __restrict__ keys_node_of_seg_unused,
                             SegPlan P, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
-                            const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R) {
+                            const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R, longlong2* trig) {
+  if (c->abort) return;
   int64_t nseg = c->num_segs;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     int64_t nb = P.nb_new[s];
@@ -295,6 +312,7 @@ __global__ void k_enumerate(const int64_t* __restrict__ ce_pend, const uint32_t*
       R.seg[r] = (int32_t)s;
       R.key[r] = ce_ev[cs + used];
       R.idx[r] = (uint32_t)r;
+      if (trig) trig[ce_ev[cs + used]] = make_longlong2(1, cap);  // allocation order = triggering event order
       r++;
       deg += take;
       used += take;
@@ -344,7 +362,7 @@ __global__ void k_write_blocks(const uint32_t* __restrict__ perm, int64_t nrec, 
 struct NodeArrays {
   int64_t *head, *tail, *num_blocks, *degree, *nslots, *dir_off, *dir_cap;
   const uint8_t* valid;
-  const uint8_t* nflags;
+  uint8_t* nflags;
   int64_t* nrec;
 };
 struct DirArrays {
@@ -354,7 +372,8 @@ struct DirArrays {
 __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                            SegPlan P, const int64_t* __restrict__ blkoff, const int64_t* __restrict__ diroff, int64_t dir_used,
                            Recs R, const uint32_t* __restrict__ ce_ev, const int64_t* __restrict__ ts, int directed,
-                           NodeArrays N, BlockArrays B, DirArrays D) {
+                           NodeArrays N, BlockArrays B, DirArrays D, int kind) {
+  if (c->abort) return;
   int64_t nseg = c->num_segs;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     int64_t cnt = P.acc_cnt[s];
@@ -362,6 +381,9 @@ __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__
     int64_t v = keys[seg_start[s]];
     int64_t t = N.tail[v], fill = P.fill[s], nb = P.nb_new[s], cs = P.cstart[s];
     int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v];
+    // a block allocated while live degree != slots written (a deletion happened) or by
+    // batch sizing leaves the closed-form position -> block law (SizingLaw)
+    if (nb > 0 && (kind == GF_SIZING_BATCH || N.degree[v] != ns_old)) N.nflags[v] |= 1;
     if (t != GF_NO_BLOCK && fill > 0) {
       B.size[t] = P.tail_size[s] + fill;
       B.tmax[t] = ts[ev_edge(ce_ev[cs + fill - 1], directed)];
@@ -414,6 +436,7 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
                                 const int64_t* __restrict__ bbase, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
                                 const int64_t* __restrict__ ts, const int64_t* __restrict__ eids, int directed,
                                 const int64_t* __restrict__ old_tail, Slot* slots, int64_t* sts, int64_t* fts) {
+  if (c->abort) return;
   int64_t nacc_ev = 0;
   {
     int64_t nseg = c->num_segs;
@@ -454,6 +477,7 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
 
 __global__ void k_old_tail(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                            const int64_t* tail, int64_t* old_tail) {
+  if (c->abort) return;
   int64_t nseg = c->num_segs;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x)
     old_tail[s] = tail[keys[seg_start[s]]];
@@ -606,7 +630,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
 
   const int T = 256;
   const int64_t G = 8 * num_sms();
-  GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in);
+  GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc);
   int endbit = bits_for(g->num_nodes);
   GF_TRY(cub_call([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairs(t, b, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s);
@@ -624,14 +648,14 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     return cub::DeviceScan::ExclusiveSum(t, b, acc, rank, (int)n, s);
   }, s));
   GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, g->next_edge_id, eids_in, out_eids, dc);
-  GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep);
+  GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, keep, cpos, (int)(E + 1), s); }, s));
   GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
   GF_CUDA(cudaMemsetAsync(P.nb_new, 0, sizeof(int64_t) * (E + 1), s));
   GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
   GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
   GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
-            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots, g->nflags);
+            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots);
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.nb_new, blkoff, (int)(E + 1), s); }, s));
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.slots_new, slotsoff, (int)(E + 1), s); }, s));
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.dir_new, diroff, (int)(E + 1), s); }, s));
@@ -676,7 +700,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
 
   if (nrec > 0) {
     GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
-              g->degree, g->sizing_kind, g->tau, g->sizing_param, R);
+              g->degree, g->sizing_kind, g->tau, g->sizing_param, R, nullptr);
     int kb = bits_for(E + 1);
     GF_TRY(cub_call([&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, R.key, key_sorted, R.idx, perm, (int)nrec, 0, kb, s);
@@ -696,7 +720,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
                  g->nrec};
     DirArrays D{g->dir};
     GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
-              dir, N, B, D);
+              dir, N, B, D, g->sizing_kind);
     GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
               g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
   }
@@ -712,6 +736,307 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   g->total_edges_inserted += hc.n_acc;
   if (h_rej) *h_rej = n - hc.n_acc;
   GF_CUDA(cudaGetLastError());
+  return GF_OK;
+}
+
+// ---- sync-free ingest --------------------------------------------------------
+// The same plan as add_edges_impl, but every size the host needs is either bounded by the
+// batch (new blocks <= events) or checked on the device: node-table growth beyond the
+// capacity and slot/directory pool overflow set IngestCounters.abort before anything is
+// mutated, and the host grows the pools and replays the batch.  Block handles and slot bases
+// come from one scan over the events that trigger an allocation (allocation order =
+// triggering event order), so there is no sort over new blocks and no mid-call host sync:
+// one launch sequence, one synchronisation at the end (for the rejected count).
+
+__global__ void k_counters_init(IngestCounters* c) {
+  c->minv = LLONG_MAX;
+  c->maxv = LLONG_MIN;
+  c->viol = c->num_segs = c->n_acc = c->new_blocks = c->new_slots = c->dir_need = 0;
+  c->max_eid = LLONG_MIN;
+  c->abort = 0;
+}
+
+// node-table growth on the device: rows [lo, maxv + 1) when they fit the capacity
+__global__ void k_grow_nodes(IngestCounters* c, int64_t lo, int64_t cap, int64_t* head, int64_t* tail, int64_t* nb,
+                             int64_t* deg, uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap, uint8_t* nflags,
+                             int64_t* nrec) {
+  const long long hi = c->maxv + 1;
+  if (c->minv < 0 || hi > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->abort |= ABORT_NODES;
+    return;
+  }
+  for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi; v += (int64_t)gridDim.x * blockDim.x) {
+    head[v] = GF_NO_BLOCK;
+    tail[v] = GF_NO_BLOCK;
+    nb[v] = 0;
+    deg[v] = 0;
+    valid[v] = 1;
+    nslots[v] = 0;
+    doff[v] = -1;
+    dcap[v] = 0;
+    nflags[v] = 0;
+    int64_t* r = nrec + v * NREC;
+    r[0] = -1;
+    r[1] = 0;
+    r[2] = NREC_VALID;
+    for (int w = 3; w < NREC; w++) r[w] = 0;
+  }
+}
+
+struct AddLL2 {
+  __device__ __forceinline__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
+    return make_longlong2(a.x + b.x, a.y + b.y);
+  }
+};
+
+// record r (segment-major enumeration): handle = blk_used + #allocations triggered by earlier
+// events, slot base = slots_used + their capacities
+__global__ void k_handles_by_scan(const IngestCounters* c, Recs R, const longlong2* __restrict__ tscan, int64_t blk_used,
+                                  int64_t slots_used, int64_t* rbase) {
+  if (c->abort) return;
+  const int64_t nrec = c->new_blocks;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
+    const longlong2 t = tscan[R.key[r]];
+    R.handle[r] = blk_used + t.x;
+    rbase[r] = slots_used + t.y;
+  }
+}
+
+__global__ void k_write_blocks_scan(const IngestCounters* c, Recs R, const int64_t* __restrict__ rbase,
+                                    const int64_t* __restrict__ blkoff, SegPlan P, const uint32_t* __restrict__ ce_ev,
+                                    const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
+                                    const int64_t* tail, const int64_t* __restrict__ ts, int directed, BlockArrays B) {
+  if (c->abort) return;
+  const int64_t nrec = c->new_blocks;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = R.handle[r];
+    const int32_t s = R.seg[r];
+    const int64_t k = r - blkoff[s], nb = P.nb_new[s], cs = P.cstart[s];
+    const int64_t f = R.first[r], cnt = R.count[r];
+    B.cap[h] = R.cap[r];
+    B.size[h] = cnt;
+    B.tmin[h] = ts[ev_edge(ce_ev[cs + f], directed)];
+    B.tmax[h] = ts[ev_edge(ce_ev[cs + f + cnt - 1], directed)];
+    B.base[h] = rbase[r];
+    const int64_t v = keys[seg_start[s]];
+    B.prev[h] = (k == 0) ? tail[v] : R.handle[r - 1];
+    B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : R.handle[r + 1];
+  }
+}
+
+// node capacity only (rows are initialised on the device by k_grow_nodes)
+gf_status grow_node_cap(gf_graph* g, int64_t need, cudaStream_t s) {
+  if (need <= g->node_cap) return GF_OK;
+  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, g->node_cap * 2));
+  int64_t k = g->num_nodes;
+  GF_TRY(grow_array(g->head, k, nc, s));
+  GF_TRY(grow_array(g->tail, k, nc, s));
+  GF_TRY(grow_array(g->num_blocks, k, nc, s));
+  GF_TRY(grow_array(g->degree, k, nc, s));
+  GF_TRY(grow_array(g->node_valid, k, nc, s));
+  GF_TRY(grow_array(g->nslots, k, nc, s));
+  GF_TRY(grow_array(g->dir_off, k, nc, s));
+  GF_TRY(grow_array(g->dir_cap, k, nc, s));
+  GF_TRY(grow_array(g->nflags, k, nc, s));
+  GF_TRY(grow_array(g->nrec, k * NREC, nc * NREC, s));
+  g->node_cap = nc;
+  return GF_OK;
+}
+
+gf_status add_edges_fast(gf_graph* g, const int64_t* src, const int64_t* dst, const int64_t* ts, int64_t n,
+                         const int64_t* eids_in, int64_t* out_eids, int64_t* h_rej, cudaStream_t s) {
+  if (h_rej) *h_rej = 0;
+  if (n == 0) return GF_OK;
+  if (n < 0 || n >= ((int64_t)1 << 30)) return fail(GF_EINVAL, "batch size must be in [0, 2^30)");
+  const int dir = g->directed;
+  const int64_t E = dir ? n : 2 * n;
+  GF_TRY(ensure_blocks(g, g->blk_used + E, s));  // new blocks <= accepted events
+  if (g->node_cap == 0) GF_TRY(grow_node_cap(g, 1024, s));
+  const int T = 256;
+  const int64_t G = 8 * num_sms();
+  IngestCounters hc;
+  const auto t_start = std::chrono::steady_clock::now();
+  for (int attempt = 0;; attempt++) {
+    const int64_t node_cap = g->node_cap;
+    const int endbit = bits_for(node_cap);
+    // scratch layout (one persistent buffer per graph)
+    Arena A;
+    A.base = nullptr;
+    auto layout = [&](Arena& a, void** p) {
+      size_t i = 0;
+      p[i++] = a.take<IngestCounters>(1);
+      p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);
+      p[i++] = a.take<int32_t>(E); p[i++] = a.take<int32_t>(E); p[i++] = a.take<int64_t>(E + 1);
+      p[i++] = a.take<uint8_t>(n); p[i++] = a.take<int64_t>(n + 1); p[i++] = a.take<int64_t>(node_cap);
+      p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);
+      p[i++] = a.take<uint32_t>(E); p[i++] = a.take<int64_t>(E); p[i++] = a.take<int32_t>(E);
+      for (int q = 0; q < 7; q++) p[i++] = a.take<int64_t>(E + 1);
+      for (int q = 0; q < 4; q++) p[i++] = a.take<int64_t>(E + 1);
+      for (int q = 0; q < 3; q++) p[i++] = a.take<int64_t>(E + 1);  // R.first/count/cap
+      p[i++] = a.take<int32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);  // R.seg/key/idx
+      p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);  // R.handle, rbase
+      p[i++] = a.take<longlong2>(E); p[i++] = a.take<longlong2>(E);      // trig, tscan
+      return i;
+    };
+    void* P_[64];
+    size_t cub_bytes = 0;
+    {
+      size_t b = 0;
+      GF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                              (uint32_t*)nullptr, (int)E, 0, endbit, s));
+      cub_bytes = std::max(cub_bytes, b);
+      GF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int)E, s));
+      cub_bytes = std::max(cub_bytes, b);
+      GF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, (uint8_t*)nullptr, (int64_t*)nullptr, (int)n, s));
+      cub_bytes = std::max(cub_bytes, b);
+      GF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, (int)(E + 1), s));
+      cub_bytes = std::max(cub_bytes, b);
+      GF_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, b, (longlong2*)nullptr, (longlong2*)nullptr, AddLL2(),
+                                             make_longlong2(0, 0), (int)E, s));
+      cub_bytes = std::max(cub_bytes, b);
+    }
+    Arena probe;
+    layout(probe, P_);
+    void* cubtmp_off = probe.take<char>((int64_t)cub_bytes);
+    const size_t need = probe.off + 4096;
+    (void)cubtmp_off;
+    if (need > g->ing_bytes) {
+      if (g->ing_buf) cudaFreeAsync(g->ing_buf, s);
+      g->ing_buf = nullptr;
+      g->ing_bytes = 0;
+      GF_CUDA(cudaMallocAsync(&g->ing_buf, need + need / 4, s));
+      g->ing_bytes = need + need / 4;
+    }
+    A.base = (char*)g->ing_buf;
+    layout(A, P_);
+    void* cubtmp = A.take<char>((int64_t)cub_bytes);
+    int i = 0;
+    IngestCounters* dc = (IngestCounters*)P_[i++];
+    uint32_t* keys_in = (uint32_t*)P_[i++];
+    uint32_t* keys = (uint32_t*)P_[i++];
+    uint32_t* vals_in = (uint32_t*)P_[i++];
+    uint32_t* vals = (uint32_t*)P_[i++];
+    int32_t* heads = (int32_t*)P_[i++];
+    int32_t* incl = (int32_t*)P_[i++];
+    int64_t* seg_start = (int64_t*)P_[i++];
+    uint8_t* acc = (uint8_t*)P_[i++];
+    int64_t* rank = (int64_t*)P_[i++];
+    int64_t* tm = (int64_t*)P_[i++];
+    int64_t* keep = (int64_t*)P_[i++];
+    int64_t* cpos = (int64_t*)P_[i++];
+    uint32_t* ce_ev = (uint32_t*)P_[i++];
+    int64_t* ce_pend = (int64_t*)P_[i++];
+    int32_t* ce_seg = (int32_t*)P_[i++];
+    SegPlan P;
+    P.acc_cnt = (int64_t*)P_[i++];
+    P.cstart = (int64_t*)P_[i++];
+    P.fill = (int64_t*)P_[i++];
+    P.tail_size = (int64_t*)P_[i++];
+    P.nb_new = (int64_t*)P_[i++];
+    P.slots_new = (int64_t*)P_[i++];
+    P.dir_new = (int64_t*)P_[i++];
+    int64_t* blkoff = (int64_t*)P_[i++];
+    int64_t* slotsoff = (int64_t*)P_[i++];
+    int64_t* diroff = (int64_t*)P_[i++];
+    int64_t* old_tail = (int64_t*)P_[i++];
+    Recs R;
+    R.first = (int64_t*)P_[i++];
+    R.count = (int64_t*)P_[i++];
+    R.cap = (int64_t*)P_[i++];
+    R.seg = (int32_t*)P_[i++];
+    R.key = (uint32_t*)P_[i++];
+    R.idx = (uint32_t*)P_[i++];
+    R.handle = (int64_t*)P_[i++];
+    int64_t* rbase = (int64_t*)P_[i++];
+    longlong2* trig = (longlong2*)P_[i++];
+    longlong2* tscan = (longlong2*)P_[i++];
+    size_t tb = cub_bytes;
+
+    GF_LAUNCH(k_counters_init, 1, 1, 0, s, dc);
+    GF_LAUNCH(k_minmax, grid_for(n, T, 2 * num_sms()), T, 0, s, src, dst, n, dc);
+    GF_LAUNCH(k_grow_nodes, grid_for(std::min<int64_t>(2 * n, std::max<int64_t>(node_cap - g->num_nodes, 1)), T, G), T, 0,
+              s, dc, g->num_nodes, node_cap, g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots,
+              g->dir_off, g->dir_cap, g->nflags, g->nrec);
+    GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc);
+    GF_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, tb, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s));
+    GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
+    tb = cub_bytes;
+    GF_CUDA(cub::DeviceScan::InclusiveSum(cubtmp, tb, heads, incl, (int)E, s));
+    GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
+              seg_start, dc);
+    GF_LAUNCH(k_accept_all, grid_for(n, T, G), T, 0, s, acc, n, dc);
+    GF_LAUNCH(k_tmax_init, grid_for(node_cap, T, G), T, 0, s, tm, g->num_nodes, g->tail, g->bsize, g->btmax, dc);
+    GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
+    tb = cub_bytes;
+    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, acc, rank, (int)n, s));
+    GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, g->next_edge_id, eids_in, out_eids, dc);
+    GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
+    tb = cub_bytes;
+    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, cpos, (int)(E + 1), s));
+    GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
+    GF_CUDA(cudaMemsetAsync(P.nb_new, 0, sizeof(int64_t) * (E + 1), s));
+    GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
+    GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
+    GF_CUDA(cudaMemsetAsync(trig, 0, sizeof(longlong2) * E, s));
+    GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
+              g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots);
+    tb = cub_bytes;
+    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.nb_new, blkoff, (int)(E + 1), s));
+    tb = cub_bytes;
+    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.slots_new, slotsoff, (int)(E + 1), s));
+    tb = cub_bytes;
+    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.dir_new, diroff, (int)(E + 1), s));
+    GF_LAUNCH(k_totals_check, 1, 1, 0, s, blkoff, slotsoff, diroff, E, g->slot_cap - g->slots_used,
+              g->dir_cap_total - g->dir_used, dc);
+    GF_LAUNCH(k_old_tail, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, g->tail, old_tail);
+    GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
+              g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
+    tb = cub_bytes;
+    GF_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, tb, trig, tscan, AddLL2(), make_longlong2(0, 0), (int)E, s));
+    GF_LAUNCH(k_handles_by_scan, grid_for(E, T, G), T, 0, s, dc, R, tscan, g->blk_used, g->slots_used, rbase);
+    BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
+    GF_LAUNCH(k_write_blocks_scan, grid_for(E, T, G), T, 0, s, dc, R, rbase, blkoff, P, ce_ev, keys, seg_start, g->tail,
+              ts, dir, B);
+    NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid, g->nflags,
+                 g->nrec};
+    DirArrays D{g->dir};
+    GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
+              dir, N, B, D, g->sizing_kind);
+    GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
+              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
+    GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    const auto t_enq = std::chrono::steady_clock::now();
+    GF_CUDA(cudaStreamSynchronize(s));
+    if (getenv("GF_INGEST_TIMING")) {
+      static double enq = 0, tot = 0;
+      static int calls = 0;
+      const auto t_end = std::chrono::steady_clock::now();
+      enq += std::chrono::duration<double, std::micro>(t_enq - t_start).count();
+      tot += std::chrono::duration<double, std::micro>(t_end - t_start).count();
+      if (++calls % 100 == 0) fprintf(stderr, "ingest: %d calls, host enqueue %.1f us/call, total %.1f us/call\n", calls, enq / calls, tot / calls);
+    }
+    if (!hc.abort) break;
+    if (hc.minv < 0) return fail(GF_EINVAL, "node ids must be non-negative");  // storage.py:408-409
+    if (hc.maxv + 1 > ((int64_t)1 << 31)) return fail(GF_EINVAL, "node ids must be < 2^31");
+    if (attempt >= 3) return fail(GF_ECUDA, "ingest did not converge");
+    // nothing was mutated: grow what overflowed and replay the batch
+    if (hc.abort & ABORT_NODES) GF_TRY(grow_node_cap(g, hc.maxv + 1, s));
+    if (hc.abort & ABORT_CAP) {
+      GF_TRY(ensure_slots(g, g->slots_used + hc.new_slots, s));
+      GF_TRY(ensure_dir(g, g->dir_used + hc.dir_need, s));
+    }
+  }
+  if (hc.maxv + 1 > g->num_nodes) g->num_nodes = hc.maxv + 1;  // storage.py:410-412
+  g->blk_used += hc.new_blocks;
+  g->slots_used += hc.new_slots;
+  g->dir_used += hc.dir_need;
+  if (eids_in) {
+    if (hc.n_acc > 0 && hc.max_eid + 1 > g->next_edge_id) g->next_edge_id = hc.max_eid + 1;
+  } else {
+    g->next_edge_id += hc.n_acc;
+  }
+  g->total_edges_inserted += hc.n_acc;
+  if (h_rej) *h_rej = n - hc.n_acc;
   return GF_OK;
 }
 
@@ -759,7 +1084,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dir,
-                g->slots, g->sts, g->fts, g->nflags, g->nrec};
+                g->slots, g->sts, g->fts, g->nflags, g->nrec, g->ing_buf};
   for (void* p : ps)
     if (p) cudaFree(p);
 }
@@ -826,6 +1151,10 @@ gf_status gf_graph_add_edges(gf_graph* g, const int64_t* d_src, const int64_t* d
   if (!g) return fail(GF_EINVAL, "graph is NULL");
   if (n > 0 && (!d_src || !d_dst || !d_ts || !d_out_eids)) return fail(GF_EINVAL, "NULL input array");
   DeviceGuard dg(g->device);
+  static const bool slow = getenv("GF_SLOW_INGEST") != nullptr;
+  // freed handles (offload) are reused LIFO by the sorted-allocation path
+  if (g->free_handles.empty() && !slow)
+    return add_edges_fast(g, d_src, d_dst, d_ts, n, d_eids_in, d_out_eids, h_out_rejected, (cudaStream_t)stream);
   return add_edges_impl(g, d_src, d_dst, d_ts, n, d_eids_in, d_out_eids, h_out_rejected, (cudaStream_t)stream);
 }
 

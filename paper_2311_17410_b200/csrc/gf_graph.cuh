@@ -50,6 +50,9 @@ struct gf_graph {
   gf::Slot* slots = nullptr;
   int64_t* sts = nullptr;
   int64_t* fts = nullptr;
+  // persistent ingest scratch (sync-free path), sized for the largest batch seen
+  void* ing_buf = nullptr;
+  size_t ing_bytes = 0;
 };
 
 namespace gf {

@@ -217,63 +217,77 @@ struct LaneBnd {
   int64_t pos, cum, base;  // boundary; block holding pos-1: its first position and slot base
 };
 
-__device__ __forceinline__ LaneBnd lane_list_lower_bound(const GraphView& GV, const LaneNode& N, int64_t x) {
-  if (N.htmin >= x) return LaneBnd{N.first, 0, 0};  // every block starts at or after x
+// The block holding the last timestamp < x: {first list position, slot base, size, tmin, tmax}.
+// none = every block starts at or after x (no position precedes the boundary).
+struct LaneBlk {
   int64_t cum, base, size, t0, t1;
+  bool none;
+};
+
+__device__ __forceinline__ LaneBlk lane_find_block(const GraphView& GV, const LaneNode& N, int64_t x) {
+  LaneBlk B;
+  B.none = N.htmin >= x;
+  if (B.none) return B;
   if (N.ttmin < x) {  // boundary in the tail block
-    cum = N.tcum;
-    base = N.tbase;
-    size = N.ns - N.tcum;
-    t0 = N.ttmin;
-    t1 = N.tmax;
-  } else {
-    // last non-tail block with tmin < x: entries lo < b < hi, tmin[lo] < x <= tmin[hi].
-    // Each probe reads entries g and g+1 together, so an exact interpolation ends the search.
-    const int64_t* d = GV.dir + N.d0 * DIRW;
-    int64_t lo = 0, hi = N.nb - 1, tl = N.htmin, th = N.ttmin;
-    int64_t lo_e1 = -1, lo_e2 = 0, lo_e3 = 0, hi_cum = N.tcum;  // cum/base/tmax of lo, cum of hi
-    for (int step = 0; hi - lo > 1; step++) {
-      const int64_t g = probe_between(lo, hi, x, tl, th, step);
-      int64_t e0, e1, e2, e3, n0 = 0, n1 = 0, n2, n3;
-      ld256(d + g * DIRW, e0, e1, e2, e3);
-      const bool two = g + 1 < hi;
-      if (two) ld256(d + (g + 1) * DIRW, n0, n1, n2, n3);
-      if (e0 < x) {
-        lo = g;
-        tl = e0;
-        lo_e1 = e1;
-        lo_e2 = e2;
-        lo_e3 = e3;
-        if (two) {
-          if (n0 < x) {
-            lo = g + 1;
-            tl = n0;
-            lo_e1 = n1;
-            lo_e2 = n2;
-            lo_e3 = n3;
-          } else {
-            hi = g + 1;
-            th = n0;
-            hi_cum = n1;
-          }
-        }
-      } else {
-        hi = g;
-        th = e0;
-        hi_cum = e1;
-      }
-    }
-    if (lo_e1 < 0) {  // entry lo (= 0) was never probed
-      int64_t e0;
-      ld256(d + lo * DIRW, e0, lo_e1, lo_e2, lo_e3);
-    }
-    cum = lo_e1;
-    base = lo_e2;
-    t0 = tl;
-    t1 = lo_e3;
-    size = hi_cum - cum;
+    B.cum = N.tcum;
+    B.base = N.tbase;
+    B.size = N.ns - N.tcum;
+    B.t0 = N.ttmin;
+    B.t1 = N.tmax;
+    return B;
   }
-  return LaneBnd{cum + lane_block_lower_bound(GV, base, size, t0, t1, x), cum, base};
+  // last non-tail block with tmin < x: entries lo < b < hi, tmin[lo] < x <= tmin[hi].
+  // Each probe reads entries g and g+1 together, so an exact interpolation ends the search.
+  const int64_t* d = GV.dir + N.d0 * DIRW;
+  int64_t lo = 0, hi = N.nb - 1, tl = N.htmin, th = N.ttmin;
+  int64_t lo_e1 = -1, lo_e2 = 0, lo_e3 = 0, hi_cum = N.tcum;  // cum/base/tmax of lo, cum of hi
+  for (int step = 0; hi - lo > 1; step++) {
+    const int64_t g = probe_between(lo, hi, x, tl, th, step);
+    int64_t e0, e1, e2, e3, n0 = 0, n1 = 0, n2, n3;
+    ld256(d + g * DIRW, e0, e1, e2, e3);
+    const bool two = g + 1 < hi;
+    if (two) ld256(d + (g + 1) * DIRW, n0, n1, n2, n3);
+    if (e0 < x) {
+      lo = g;
+      tl = e0;
+      lo_e1 = e1;
+      lo_e2 = e2;
+      lo_e3 = e3;
+      if (two) {
+        if (n0 < x) {
+          lo = g + 1;
+          tl = n0;
+          lo_e1 = n1;
+          lo_e2 = n2;
+          lo_e3 = n3;
+        } else {
+          hi = g + 1;
+          th = n0;
+          hi_cum = n1;
+        }
+      }
+    } else {
+      hi = g;
+      th = e0;
+      hi_cum = e1;
+    }
+  }
+  if (lo_e1 < 0) {  // entry lo (= 0) was never probed
+    int64_t e0;
+    ld256(d + lo * DIRW, e0, lo_e1, lo_e2, lo_e3);
+  }
+  B.cum = lo_e1;
+  B.base = lo_e2;
+  B.t0 = tl;
+  B.t1 = lo_e3;
+  B.size = hi_cum - lo_e1;
+  return B;
+}
+
+__device__ __forceinline__ LaneBnd lane_list_lower_bound(const GraphView& GV, const LaneNode& N, int64_t x) {
+  const LaneBlk B = lane_find_block(GV, N, x);
+  if (B.none) return LaneBnd{N.first, 0, 0};
+  return LaneBnd{B.cum + lane_block_lower_bound(GV, B.base, B.size, B.t0, B.t1, x), B.cum, B.base};
 }
 
 #ifndef GF_COUNT_MINB
@@ -594,8 +608,39 @@ __device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irreg
 #define GF_GATHER_UNROLL 2
 #endif
 
-__global__ void __launch_bounds__(THREADS, GF_FUSED_MINB) k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
-  constexpr int NW = THREADS / 32;
+// tile scan of the counts; thread 0 publishes the tile aggregate (tile 0: inclusive prefix)
+template <int NW>
+__device__ __forceinline__ void tile_publish(int k, int lane, int w, int32_t* s_wsum, const TileCtl& C, int64_t tile,
+                                             int& incl, int& wpre, int& agg) {
+  incl = k;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[w] = incl;
+  __syncthreads();
+  wpre = 0;
+  agg = 0;
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const int x = s_wsum[i];
+    wpre += (i < w) ? x : 0;
+    agg += x;
+  }
+  if (threadIdx.x == 0) st_relaxed(C.status + tile, (tile == 0 ? TS_INC : TS_AGG) | (uint64_t)agg);
+}
+
+#ifndef GF_FUSED_THREADS
+#define GF_FUSED_THREADS 256
+#endif
+constexpr int FT = GF_FUSED_THREADS;  // queries per tile = threads per CTA
+
+// EARLY: publish the tile aggregate before the in-block window search when every count is
+// already known (recent policy: long lists give k = fanout once the boundary block is found)
+template <bool EARLY>
+__global__ void __launch_bounds__(FT, GF_FUSED_MINB * 256 / FT) k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
+  constexpr int NW = FT / 32;
   __shared__ uint32_t s_sel[NW][32][KMAX];
   __shared__ uint8_t s_owner[NW][32 * KMAX];
   __shared__ uint64_t s_key[NW][32];
@@ -608,21 +653,37 @@ __global__ void __launch_bounds__(THREADS, GF_FUSED_MINB) k_sample_fused(GraphVi
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t n = query_count(Q);
-  if (tile * THREADS >= n) return;
-  const int64_t q = tile * THREADS + threadIdx.x;
+  if (tile * FT >= n) return;
+  const int64_t q = tile * FT + threadIdx.x;
 
-  // ---- window search (k_count_lane) ----
+  // ---- node record + boundary block; the count is often known here already ----
   int k = 0;
-  int64_t lo = 0, hi = 0, slot_hi = 0, cum = 0, d0 = 0, nb = 0;
-  bool irregular = false;
+  int64_t lo = 0, hi = 0, slot_hi = 0, cum = 0, d0 = 0, nb = 0, te = 0, tsr = GF_TS_MIN;
+  bool irregular = false, live = false, known = true;
   uint64_t qkey = 0;
+  LaneNode N;
+  LaneBlk hb;
+  // window search inside the boundary block
+  auto finish = [&]() {
+    hi = hb.cum + lane_block_lower_bound(GV, hb.base, hb.size, hb.t0, hb.t1, te);
+    lo = (tsr == GF_TS_MIN) ? N.first : lane_list_lower_bound(GV, N, tsr).pos;
+    if (hi > lo) {
+      k = (int)min(hi - lo, Q.fanout);
+      slot_hi = hb.base + (hi - 1 - hb.cum);
+      cum = hb.cum;
+      d0 = N.d0;
+      nb = N.nb;
+      irregular = N.irregular;
+    } else {
+      k = 0;
+    }
+  };
   if (q < n) {
     const int64_t v = Q.src[q];
-    const int64_t te = Q.t_end[q];
+    te = Q.t_end[q];
     qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
     if (v >= 0 && v < GV.num_nodes) {
       const int64_t* r = GV.nrec + v * NREC;
-      LaneNode N;
       int64_t w2, w3;
       ld256(r, N.d0, N.ns, w2, N.first);
       ld256(r + 4, N.tcum, N.tbase, N.ttmin, N.tmax);
@@ -631,39 +692,38 @@ __global__ void __launch_bounds__(THREADS, GF_FUSED_MINB) k_sample_fused(GraphVi
       N.valid = (w2 & NREC_VALID) != 0;
       N.irregular = (w2 & NREC_IRREG) != 0;
       if (N.valid && N.nb > 0) {  // sampling.py:153-155
-        const LaneBnd h = lane_list_lower_bound(GV, N, te);
-        const int64_t tsr = t_start_of(Q, q, te);
-        lo = (tsr == GF_TS_MIN) ? N.first : lane_list_lower_bound(GV, N, tsr).pos;
-        if (h.pos > lo) {
-          k = (int)min(h.pos - lo, Q.fanout);
-          hi = h.pos;
-          slot_hi = h.base + (h.pos - 1 - h.cum);
-          cum = h.cum;
-          d0 = N.d0;
-          nb = N.nb;
-          irregular = N.irregular;
+        tsr = t_start_of(Q, q, te);
+        if (EARLY) {
+          hb = lane_find_block(GV, N, te);
+          live = !hb.none;
+          // position hb.cum (tmin < te) is a candidate, so with t_start = TS_MIN there are
+          // at least hb.cum + 1 - first of them
+          if (live) {
+            if (tsr == GF_TS_MIN && hb.cum + 1 - N.first >= Q.fanout) k = (int)Q.fanout;
+            else known = false;
+          }
+        } else {
+          const LaneBnd h = lane_list_lower_bound(GV, N, te);
+          lo = (tsr == GF_TS_MIN) ? N.first : lane_list_lower_bound(GV, N, tsr).pos;
+          if (h.pos > lo) {
+            k = (int)min(h.pos - lo, Q.fanout);
+            hi = h.pos;
+            slot_hi = h.base + (h.pos - 1 - h.cum);
+            cum = h.cum;
+            d0 = N.d0;
+            nb = N.nb;
+            irregular = N.irregular;
+          }
         }
       }
     }
   }
+  int incl = 0, wpre = 0, agg = 0;
+  const bool early = EARLY && __syncthreads_and(known);
+  if (early) tile_publish<NW>(k, lane, w, s_wsum, C, tile, incl, wpre, agg);
 
-  // ---- tile scan of the counts; publish the aggregate ----
-  int incl = k;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) s_wsum[w] = incl;
-  __syncthreads();
-  int wpre = 0, agg = 0;
-#pragma unroll
-  for (int i = 0; i < NW; i++) {
-    const int x = s_wsum[i];
-    wpre += (i < w) ? x : 0;
-    agg += x;
-  }
-  if (threadIdx.x == 0) st_relaxed(C.status + tile, (tile == 0 ? TS_INC : TS_AGG) | (uint64_t)agg);
+  if (EARLY && live) finish();
+  if (!early) tile_publish<NW>(k, lane, w, s_wsum, C, tile, incl, wpre, agg);
 
   // ---- selection into shared memory (independent of the output base) ----
   const int pre = incl - k;
@@ -983,7 +1043,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   }
   Scratch sb(s);
   Arena A;
-  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + (size_t)cap_q / 32 + 8192));
+  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + (size_t)cap_q / 4 + 8192));
   A.base = sb.as<char>();
   QState S{A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q),
            A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q)};
@@ -991,12 +1051,13 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   GraphView GV = view_of(g);
   const bool fast = !g->any_deleted;
   if (fast && Q.fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled()) {
-    const int64_t tiles = (cap_q + THREADS - 1) / THREADS;
+    const int64_t tiles = (cap_q + FT - 1) / FT;
     TileCtl C{reinterpret_cast<uint64_t*>(A.take<int64_t>(tiles + 1)), nullptr, total};
     C.ticket = reinterpret_cast<unsigned*>(C.status + tiles);
     GF_CUDA(cudaMemsetAsync(C.status, 0, sizeof(uint64_t) * (tiles + 1), s));
     GF_CUDA(cudaMemsetAsync(total, 0, sizeof(int64_t), s));
-    GF_LAUNCH(k_sample_fused, tiles, THREADS, 0, s, GV, Q, O, C);
+    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, FT, 0, s, GV, Q, O, C);
+    else GF_LAUNCH(k_sample_fused<false>, tiles, FT, 0, s, GV, Q, O, C);
     return GF_OK;
   }
   if (fast) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
