@@ -12,6 +12,8 @@
 //   scan in handle order -> metadata/directory/slot writes.
 #include <cub/cub.cuh>
 
+#include <string.h>
+
 #include <algorithm>
 #include <chrono>
 #include <vector>
@@ -34,6 +36,14 @@ struct IngestCounters {
   long long abort;        // sync-free path: ABORT_* bits, nothing was mutated
 };
 constexpr long long ABORT_NODES = 1, ABORT_CAP = 2;
+
+// per-call values of the sync-free path, read on the device so that its captured launch
+// sequence can be replayed unchanged (one H2D copy of this struct per call)
+struct IngestScalars {
+  const int64_t *src, *dst, *ts, *eids_in;
+  int64_t* out_eids;
+  int64_t num_nodes, blk_used, slots_used, dir_used, next_edge_id, slots_free, dir_free;
+};
 
 template <class T>
 gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
@@ -138,8 +148,9 @@ __global__ void k_accept_all(uint8_t* acc, int64_t n, const IngestCounters* c) {
 }
 
 __global__ void k_tmax_init(int64_t* tm, int64_t num_nodes, const int64_t* tail, const int64_t* bsize, const int64_t* btmax,
-                            const IngestCounters* c) {
+                            const IngestCounters* c, const IngestScalars* S) {
   if (!c->viol || c->abort) return;
+  if (S) num_nodes = S->num_nodes;
   if (c->maxv + 1 > num_nodes) num_nodes = c->maxv + 1;  // nodes this batch creates have no tail
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < num_nodes; v += (int64_t)gridDim.x * blockDim.x)
     tm[v] = node_tmax(tail, bsize, btmax, v);
@@ -169,7 +180,9 @@ __global__ void k_keep(const uint32_t* __restrict__ vals, int64_t E, int directe
 }
 
 __global__ void k_eids(const uint8_t* __restrict__ acc, const int64_t* __restrict__ rank, int64_t n, int64_t next_id,
-                       const int64_t* __restrict__ eids_in, int64_t* out_eids, IngestCounters* c) {
+                       const int64_t* __restrict__ eids_in, int64_t* out_eids, IngestCounters* c,
+                       const IngestScalars* S) {
+  if (S) next_id = S->next_edge_id;
   long long mx = LLONG_MIN;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     int64_t e = -1;
@@ -272,12 +285,12 @@ __global__ void k_totals(const int64_t* blkoff, const int64_t* slotsoff, const i
 
 // sync-free path: totals + capacity check against the host-known pool state
 __global__ void k_totals_check(const int64_t* blkoff, const int64_t* slotsoff, const int64_t* diroff, int64_t E,
-                               int64_t slots_free, int64_t dir_free, IngestCounters* c) {
+                               const IngestScalars* S, IngestCounters* c) {
   if (threadIdx.x || blockIdx.x || c->abort) return;
   c->new_blocks = blkoff[E];
   c->new_slots = slotsoff[E];
   c->dir_need = diroff[E];
-  if (c->new_slots > slots_free || c->dir_need > dir_free) c->abort |= ABORT_CAP;
+  if (c->new_slots > S->slots_free || c->dir_need > S->dir_free) c->abort |= ABORT_CAP;
 }
 
 struct Recs {
@@ -372,8 +385,9 @@ struct DirArrays {
 __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                            SegPlan P, const int64_t* __restrict__ blkoff, const int64_t* __restrict__ diroff, int64_t dir_used,
                            Recs R, const uint32_t* __restrict__ ce_ev, const int64_t* __restrict__ ts, int directed,
-                           NodeArrays N, BlockArrays B, DirArrays D, int kind) {
+                           NodeArrays N, BlockArrays B, DirArrays D, int kind, const IngestScalars* S) {
   if (c->abort) return;
+  if (S) dir_used = S->dir_used;
   int64_t nseg = c->num_segs;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     int64_t cnt = P.acc_cnt[s];
@@ -503,6 +517,7 @@ gf_status ensure_nodes(gf_graph* g, int64_t need, cudaStream_t s) {
   if (need <= g->num_nodes) return GF_OK;
   if (need > ((int64_t)1 << 31)) return fail(GF_EINVAL, "node ids must be < 2^31");
   if (need > g->node_cap) {
+    g->gen++;
     int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, g->node_cap * 2));
     int64_t k = g->num_nodes;
     GF_TRY(grow_array(g->head, k, nc, s));
@@ -526,6 +541,7 @@ gf_status ensure_nodes(gf_graph* g, int64_t need, cudaStream_t s) {
 
 gf_status ensure_blocks(gf_graph* g, int64_t need, cudaStream_t s) {
   if (need <= g->blk_cap) return GF_OK;
+  g->gen++;
   int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, g->blk_cap * 2));
   int64_t k = g->blk_used;
   GF_TRY(grow_array(g->bcap, k, nc, s));
@@ -541,6 +557,7 @@ gf_status ensure_blocks(gf_graph* g, int64_t need, cudaStream_t s) {
 
 gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
   if (need <= g->slot_cap) return GF_OK;
+  g->gen++;
   int64_t nc = std::max<int64_t>(need, std::max<int64_t>(4096, g->slot_cap + g->slot_cap / 2));
   int64_t old = g->slot_cap;
   GF_TRY(grow_array(g->slots, g->slots_used, nc, s));
@@ -554,6 +571,7 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
 
 gf_status ensure_dir(gf_graph* g, int64_t need, cudaStream_t s) {
   if (need <= g->dir_cap_total) return GF_OK;
+  g->gen++;
   int64_t nc = std::max<int64_t>(need, std::max<int64_t>(4096, g->dir_cap_total * 2));
   GF_TRY(grow_array(g->dir, g->dir_used * DIRW, nc * DIRW, s));
   g->dir_cap_total = nc;
@@ -641,13 +659,13 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
             seg_start, dc);
   // chronology: accept all unless some stored endpoint sees a decreasing timestamp
   GF_LAUNCH(k_accept_all, grid_for(n, T, G), T, 0, s, acc, n, dc);
-  GF_LAUNCH(k_tmax_init, grid_for(g->num_nodes, T, G), T, 0, s, tm, g->num_nodes, g->tail, g->bsize, g->btmax, dc);
+  GF_LAUNCH(k_tmax_init, grid_for(g->num_nodes, T, G), T, 0, s, tm, g->num_nodes, g->tail, g->bsize, g->btmax, dc, nullptr);
   GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
   // edge ids by scan (storage.py:438-442)
   GF_TRY(cub_call([&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, acc, rank, (int)n, s);
   }, s));
-  GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, g->next_edge_id, eids_in, out_eids, dc);
+  GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, g->next_edge_id, eids_in, out_eids, dc, nullptr);
   GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, keep, cpos, (int)(E + 1), s); }, s));
   GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
@@ -720,7 +738,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
                  g->nrec};
     DirArrays D{g->dir};
     GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
-              dir, N, B, D, g->sizing_kind);
+              dir, N, B, D, g->sizing_kind, nullptr);
     GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
               g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
   }
@@ -757,9 +775,10 @@ __global__ void k_counters_init(IngestCounters* c) {
 }
 
 // node-table growth on the device: rows [lo, maxv + 1) when they fit the capacity
-__global__ void k_grow_nodes(IngestCounters* c, int64_t lo, int64_t cap, int64_t* head, int64_t* tail, int64_t* nb,
-                             int64_t* deg, uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap, uint8_t* nflags,
-                             int64_t* nrec) {
+__global__ void k_grow_nodes(IngestCounters* c, const IngestScalars* S, int64_t cap, int64_t* head, int64_t* tail,
+                             int64_t* nb, int64_t* deg, uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap,
+                             uint8_t* nflags, int64_t* nrec) {
+  const int64_t lo = S->num_nodes;
   const long long hi = c->maxv + 1;
   if (c->minv < 0 || hi > cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) c->abort |= ABORT_NODES;
@@ -791,9 +810,10 @@ struct AddLL2 {
 
 // record r (segment-major enumeration): handle = blk_used + #allocations triggered by earlier
 // events, slot base = slots_used + their capacities
-__global__ void k_handles_by_scan(const IngestCounters* c, Recs R, const longlong2* __restrict__ tscan, int64_t blk_used,
-                                  int64_t slots_used, int64_t* rbase) {
+__global__ void k_handles_by_scan(const IngestCounters* c, Recs R, const longlong2* __restrict__ tscan,
+                                  const IngestScalars* S, int64_t* rbase) {
   if (c->abort) return;
+  const int64_t blk_used = S->blk_used, slots_used = S->slots_used;
   const int64_t nrec = c->new_blocks;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
     const longlong2 t = tscan[R.key[r]];
@@ -824,9 +844,26 @@ __global__ void k_write_blocks_scan(const IngestCounters* c, Recs R, const int64
   }
 }
 
+// batch inputs -> fixed staging buffers (the captured sequence always reads the same addresses)
+__global__ void k_stage(const IngestScalars* S, int64_t n, int64_t* src, int64_t* dst, int64_t* ts, int64_t* eids) {
+  const bool has_eids = S->eids_in != nullptr;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    src[j] = S->src[j];
+    dst[j] = S->dst[j];
+    ts[j] = S->ts[j];
+    if (has_eids) eids[j] = S->eids_in[j];
+  }
+}
+
+__global__ void k_unstage(const IngestScalars* S, int64_t n, const int64_t* out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    S->out_eids[j] = out[j];
+}
+
 // node capacity only (rows are initialised on the device by k_grow_nodes)
 gf_status grow_node_cap(gf_graph* g, int64_t need, cudaStream_t s) {
   if (need <= g->node_cap) return GF_OK;
+  g->gen++;
   int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, g->node_cap * 2));
   int64_t k = g->num_nodes;
   GF_TRY(grow_array(g->head, k, nc, s));
@@ -843,8 +880,8 @@ gf_status grow_node_cap(gf_graph* g, int64_t need, cudaStream_t s) {
   return GF_OK;
 }
 
-gf_status add_edges_fast(gf_graph* g, const int64_t* src, const int64_t* dst, const int64_t* ts, int64_t n,
-                         const int64_t* eids_in, int64_t* out_eids, int64_t* h_rej, cudaStream_t s) {
+gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_in, const int64_t* ts_in, int64_t n,
+                         const int64_t* eids_user, int64_t* out_user, int64_t* h_rej, cudaStream_t s) {
   if (h_rej) *h_rej = 0;
   if (n == 0) return GF_OK;
   if (n < 0 || n >= ((int64_t)1 << 30)) return fail(GF_EINVAL, "batch size must be in [0, 2^30)");
@@ -852,6 +889,10 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src, const int64_t* dst, co
   const int64_t E = dir ? n : 2 * n;
   GF_TRY(ensure_blocks(g, g->blk_used + E, s));  // new blocks <= accepted events
   if (g->node_cap == 0) GF_TRY(grow_node_cap(g, 1024, s));
+  if (!g->ing_host) GF_CUDA(cudaMallocHost(&g->ing_host, 4096));
+  IngestScalars* hs = (IngestScalars*)g->ing_host;
+  IngestCounters* hcp = (IngestCounters*)((char*)g->ing_host + 2048);
+  static const bool no_graph = getenv("GF_INGEST_NO_GRAPH") != nullptr;
   const int T = 256;
   const int64_t G = 8 * num_sms();
   IngestCounters hc;
@@ -859,26 +900,6 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src, const int64_t* dst, co
   for (int attempt = 0;; attempt++) {
     const int64_t node_cap = g->node_cap;
     const int endbit = bits_for(node_cap);
-    // scratch layout (one persistent buffer per graph)
-    Arena A;
-    A.base = nullptr;
-    auto layout = [&](Arena& a, void** p) {
-      size_t i = 0;
-      p[i++] = a.take<IngestCounters>(1);
-      p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);
-      p[i++] = a.take<int32_t>(E); p[i++] = a.take<int32_t>(E); p[i++] = a.take<int64_t>(E + 1);
-      p[i++] = a.take<uint8_t>(n); p[i++] = a.take<int64_t>(n + 1); p[i++] = a.take<int64_t>(node_cap);
-      p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);
-      p[i++] = a.take<uint32_t>(E); p[i++] = a.take<int64_t>(E); p[i++] = a.take<int32_t>(E);
-      for (int q = 0; q < 7; q++) p[i++] = a.take<int64_t>(E + 1);
-      for (int q = 0; q < 4; q++) p[i++] = a.take<int64_t>(E + 1);
-      for (int q = 0; q < 3; q++) p[i++] = a.take<int64_t>(E + 1);  // R.first/count/cap
-      p[i++] = a.take<int32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);  // R.seg/key/idx
-      p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);  // R.handle, rbase
-      p[i++] = a.take<longlong2>(E); p[i++] = a.take<longlong2>(E);      // trig, tscan
-      return i;
-    };
-    void* P_[64];
     size_t cub_bytes = 0;
     {
       size_t b = 0;
@@ -895,23 +916,49 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src, const int64_t* dst, co
                                              make_longlong2(0, 0), (int)E, s));
       cub_bytes = std::max(cub_bytes, b);
     }
+    // scratch layout (one persistent buffer per graph)
+    auto layout = [&](Arena& a, void** p) {
+      size_t i = 0;
+      p[i++] = a.take<IngestCounters>(1);
+      p[i++] = a.take<IngestScalars>(1);
+      for (int q = 0; q < 5; q++) p[i++] = a.take<int64_t>(n);  // staged src, dst, ts, eids_in, out_eids
+      p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);
+      p[i++] = a.take<int32_t>(E); p[i++] = a.take<int32_t>(E); p[i++] = a.take<int64_t>(E + 1);
+      p[i++] = a.take<uint8_t>(n); p[i++] = a.take<int64_t>(n + 1); p[i++] = a.take<int64_t>(node_cap);
+      p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);
+      p[i++] = a.take<uint32_t>(E); p[i++] = a.take<int64_t>(E); p[i++] = a.take<int32_t>(E);
+      for (int q = 0; q < 7; q++) p[i++] = a.take<int64_t>(E + 1);
+      for (int q = 0; q < 4; q++) p[i++] = a.take<int64_t>(E + 1);
+      for (int q = 0; q < 3; q++) p[i++] = a.take<int64_t>(E + 1);  // R.first/count/cap
+      p[i++] = a.take<int32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);  // R.seg/key/idx
+      p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);  // R.handle, rbase
+      p[i++] = a.take<longlong2>(E); p[i++] = a.take<longlong2>(E);      // trig, tscan
+      p[i++] = a.take<char>((int64_t)cub_bytes);
+      return i;
+    };
+    void* P_[64];
     Arena probe;
     layout(probe, P_);
-    void* cubtmp_off = probe.take<char>((int64_t)cub_bytes);
     const size_t need = probe.off + 4096;
-    (void)cubtmp_off;
     if (need > g->ing_bytes) {
-      if (g->ing_buf) cudaFreeAsync(g->ing_buf, s);
+      if (g->ing_buf) GF_CUDA(cudaFreeAsync(g->ing_buf, s));
       g->ing_buf = nullptr;
       g->ing_bytes = 0;
       GF_CUDA(cudaMallocAsync(&g->ing_buf, need + need / 4, s));
       g->ing_bytes = need + need / 4;
     }
+    Arena A;
     A.base = (char*)g->ing_buf;
     layout(A, P_);
-    void* cubtmp = A.take<char>((int64_t)cub_bytes);
     int i = 0;
     IngestCounters* dc = (IngestCounters*)P_[i++];
+    IngestScalars* ds = (IngestScalars*)P_[i++];
+    int64_t* src = (int64_t*)P_[i++];
+    int64_t* dst = (int64_t*)P_[i++];
+    int64_t* ts = (int64_t*)P_[i++];
+    int64_t* eids_st = (int64_t*)P_[i++];
+    int64_t* out_eids = (int64_t*)P_[i++];
+    const int64_t* eids_in = eids_user ? eids_st : nullptr;
     uint32_t* keys_in = (uint32_t*)P_[i++];
     uint32_t* keys = (uint32_t*)P_[i++];
     uint32_t* vals_in = (uint32_t*)P_[i++];
@@ -950,70 +997,111 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src, const int64_t* dst, co
     int64_t* rbase = (int64_t*)P_[i++];
     longlong2* trig = (longlong2*)P_[i++];
     longlong2* tscan = (longlong2*)P_[i++];
-    size_t tb = cub_bytes;
+    void* cubtmp = P_[i++];
 
-    GF_LAUNCH(k_counters_init, 1, 1, 0, s, dc);
-    GF_LAUNCH(k_minmax, grid_for(n, T, 2 * num_sms()), T, 0, s, src, dst, n, dc);
-    GF_LAUNCH(k_grow_nodes, grid_for(std::min<int64_t>(2 * n, std::max<int64_t>(node_cap - g->num_nodes, 1)), T, G), T, 0,
-              s, dc, g->num_nodes, node_cap, g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots,
-              g->dir_off, g->dir_cap, g->nflags, g->nrec);
-    GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc);
-    GF_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, tb, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s));
-    GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
-    tb = cub_bytes;
-    GF_CUDA(cub::DeviceScan::InclusiveSum(cubtmp, tb, heads, incl, (int)E, s));
-    GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
-              seg_start, dc);
-    GF_LAUNCH(k_accept_all, grid_for(n, T, G), T, 0, s, acc, n, dc);
-    GF_LAUNCH(k_tmax_init, grid_for(node_cap, T, G), T, 0, s, tm, g->num_nodes, g->tail, g->bsize, g->btmax, dc);
-    GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
-    tb = cub_bytes;
-    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, acc, rank, (int)n, s));
-    GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, g->next_edge_id, eids_in, out_eids, dc);
-    GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
-    tb = cub_bytes;
-    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, cpos, (int)(E + 1), s));
-    GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
-    GF_CUDA(cudaMemsetAsync(P.nb_new, 0, sizeof(int64_t) * (E + 1), s));
-    GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
-    GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
-    GF_CUDA(cudaMemsetAsync(trig, 0, sizeof(longlong2) * E, s));
-    GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
-              g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots);
-    tb = cub_bytes;
-    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.nb_new, blkoff, (int)(E + 1), s));
-    tb = cub_bytes;
-    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.slots_new, slotsoff, (int)(E + 1), s));
-    tb = cub_bytes;
-    GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.dir_new, diroff, (int)(E + 1), s));
-    GF_LAUNCH(k_totals_check, 1, 1, 0, s, blkoff, slotsoff, diroff, E, g->slot_cap - g->slots_used,
-              g->dir_cap_total - g->dir_used, dc);
-    GF_LAUNCH(k_old_tail, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, g->tail, old_tail);
-    GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
-              g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
-    tb = cub_bytes;
-    GF_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, tb, trig, tscan, AddLL2(), make_longlong2(0, 0), (int)E, s));
-    GF_LAUNCH(k_handles_by_scan, grid_for(E, T, G), T, 0, s, dc, R, tscan, g->blk_used, g->slots_used, rbase);
-    BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
-    GF_LAUNCH(k_write_blocks_scan, grid_for(E, T, G), T, 0, s, dc, R, rbase, blkoff, P, ce_ev, keys, seg_start, g->tail,
-              ts, dir, B);
-    NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid, g->nflags,
-                 g->nrec};
-    DirArrays D{g->dir};
-    GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
-              dir, N, B, D, g->sizing_kind);
-    GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
-              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
-    GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    // per-call values: read on the device through ds
+    *hs = IngestScalars{src_in, dst_in, ts_in, eids_user, out_user, g->num_nodes, g->blk_used, g->slots_used,
+                        g->dir_used, g->next_edge_id, g->slot_cap - g->slots_used, g->dir_cap_total - g->dir_used};
+
+    // the launch sequence: identical for every call with the same key
+    auto enqueue = [&](cudaStream_t s) -> gf_status {
+      size_t tb = cub_bytes;
+      GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
+      GF_LAUNCH(k_counters_init, 1, 1, 0, s, dc);
+      GF_LAUNCH(k_stage, grid_for(n, T, G), T, 0, s, ds, n, src, dst, ts, eids_st);
+      GF_LAUNCH(k_minmax, grid_for(n, T, 2 * num_sms()), T, 0, s, src, dst, n, dc);
+      GF_LAUNCH(k_grow_nodes, grid_for(2 * n, T, G), T, 0, s, dc, ds, node_cap, g->head, g->tail, g->num_blocks,
+                g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
+      GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc);
+      GF_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, tb, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s));
+      GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
+      tb = cub_bytes;
+      GF_CUDA(cub::DeviceScan::InclusiveSum(cubtmp, tb, heads, incl, (int)E, s));
+      GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
+                seg_start, dc);
+      GF_LAUNCH(k_accept_all, grid_for(n, T, G), T, 0, s, acc, n, dc);
+      GF_LAUNCH(k_tmax_init, grid_for(node_cap, T, G), T, 0, s, tm, 0, g->tail, g->bsize, g->btmax, dc, ds);
+      GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
+      tb = cub_bytes;
+      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, acc, rank, (int)n, s));
+      GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, 0, eids_in, out_eids, dc, ds);
+      GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
+      tb = cub_bytes;
+      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, cpos, (int)(E + 1), s));
+      GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
+      GF_CUDA(cudaMemsetAsync(P.nb_new, 0, sizeof(int64_t) * (E + 1), s));
+      GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
+      GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
+      GF_CUDA(cudaMemsetAsync(trig, 0, sizeof(longlong2) * E, s));
+      GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
+                g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots);
+      tb = cub_bytes;
+      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.nb_new, blkoff, (int)(E + 1), s));
+      tb = cub_bytes;
+      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.slots_new, slotsoff, (int)(E + 1), s));
+      tb = cub_bytes;
+      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.dir_new, diroff, (int)(E + 1), s));
+      GF_LAUNCH(k_totals_check, 1, 1, 0, s, blkoff, slotsoff, diroff, E, ds, dc);
+      GF_LAUNCH(k_old_tail, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, g->tail, old_tail);
+      GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
+                g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
+      tb = cub_bytes;
+      GF_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, tb, trig, tscan, AddLL2(), make_longlong2(0, 0), (int)E, s));
+      GF_LAUNCH(k_handles_by_scan, grid_for(E, T, G), T, 0, s, dc, R, tscan, ds, rbase);
+      BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
+      GF_LAUNCH(k_write_blocks_scan, grid_for(E, T, G), T, 0, s, dc, R, rbase, blkoff, P, ce_ev, keys, seg_start,
+                g->tail, ts, dir, B);
+      NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
+                   g->nflags, g->nrec};
+      DirArrays D{g->dir};
+      GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, 0, R, ce_ev, ts, dir, N,
+                B, D, g->sizing_kind, ds);
+      GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
+                g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
+      GF_LAUNCH(k_unstage, grid_for(n, T, G), T, 0, s, ds, n, out_eids);
+      GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
+      return GF_OK;
+    };
+
+    const bool profiling = g_profile.load(std::memory_order_relaxed) != 0;
+    if (no_graph || profiling) {
+      GF_TRY(enqueue(s));
+    } else {
+      const int64_t key[8] = {E, n, (int64_t)dir | (eids_user ? 2 : 0), node_cap, g->gen, (int64_t)(intptr_t)g->ing_buf,
+                              (int64_t)cub_bytes, 0};
+      if (!g->ing_exec || memcmp(key, g->ing_key, sizeof(key)) != 0) {
+        if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);
+        g->ing_exec = nullptr;
+        const uint64_t l0 = g_launches.load();
+        // captured on a private stream (the caller's may be the legacy default stream)
+        if (!g->cap_stream) GF_CUDA(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+        cudaGraph_t graph = nullptr;
+        GF_CUDA(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
+        gf_status st = enqueue(g->cap_stream);
+        cudaError_t ce = cudaStreamEndCapture(g->cap_stream, &graph);
+        GF_TRY(st);
+        if (ce != cudaSuccess) return fail(GF_ECUDA, std::string("ingest capture: ") + cudaGetErrorString(ce));
+        ce = cudaGraphInstantiate(&g->ing_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return fail(GF_ECUDA, std::string("ingest graph: ") + cudaGetErrorString(ce));
+        g->ing_nodes = (int64_t)(g_launches.load() - l0);
+        g_launches.fetch_sub((uint64_t)g->ing_nodes);
+        memcpy(g->ing_key, key, sizeof(key));
+      }
+      GF_CUDA(cudaGraphLaunch(g->ing_exec, s));
+      g_launches.fetch_add((uint64_t)g->ing_nodes);
+    }
     const auto t_enq = std::chrono::steady_clock::now();
     GF_CUDA(cudaStreamSynchronize(s));
+    hc = *hcp;
     if (getenv("GF_INGEST_TIMING")) {
       static double enq = 0, tot = 0;
       static int calls = 0;
       const auto t_end = std::chrono::steady_clock::now();
       enq += std::chrono::duration<double, std::micro>(t_enq - t_start).count();
       tot += std::chrono::duration<double, std::micro>(t_end - t_start).count();
-      if (++calls % 100 == 0) fprintf(stderr, "ingest: %d calls, host enqueue %.1f us/call, total %.1f us/call\n", calls, enq / calls, tot / calls);
+      if (++calls % 100 == 0)
+        fprintf(stderr, "ingest: %d calls, host enqueue %.1f us/call, total %.1f us/call\n", calls, enq / calls, tot / calls);
     }
     if (!hc.abort) break;
     if (hc.minv < 0) return fail(GF_EINVAL, "node ids must be non-negative");  // storage.py:408-409
@@ -1030,7 +1118,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src, const int64_t* dst, co
   g->blk_used += hc.new_blocks;
   g->slots_used += hc.new_slots;
   g->dir_used += hc.dir_need;
-  if (eids_in) {
+  if (eids_user) {
     if (hc.n_acc > 0 && hc.max_eid + 1 > g->next_edge_id) g->next_edge_id = hc.max_eid + 1;
   } else {
     g->next_edge_id += hc.n_acc;
@@ -1087,6 +1175,9 @@ void free_graph(gf_graph* g) {
                 g->slots, g->sts, g->fts, g->nflags, g->nrec, g->ing_buf};
   for (void* p : ps)
     if (p) cudaFree(p);
+  if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);
+  if (g->ing_host) cudaFreeHost(g->ing_host);
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
 }
 
 }  // namespace
@@ -1126,6 +1217,7 @@ gf_status gf_graph_reserve(gf_graph* g, int64_t nodes, int64_t blocks, int64_t s
   DeviceGuard dg(g->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (nodes > g->node_cap) {
+    g->gen++;
     int64_t k = g->num_nodes, nc = nodes;
     GF_TRY(grow_array(g->head, k, nc, s));
     GF_TRY(grow_array(g->tail, k, nc, s));

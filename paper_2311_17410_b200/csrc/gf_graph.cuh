@@ -53,6 +53,13 @@ struct gf_graph {
   // persistent ingest scratch (sync-free path), sized for the largest batch seen
   void* ing_buf = nullptr;
   size_t ing_bytes = 0;
+  // ingest launch sequence captured as a CUDA graph, replayed while its key holds
+  int64_t gen = 0;            // bumped whenever a pool or table is reallocated
+  void* ing_host = nullptr;   // pinned: per-call scalars (H2D) + counters (D2H)
+  cudaGraphExec_t ing_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int64_t ing_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  int64_t ing_nodes = 0;      // kernel launches per replay
 };
 
 namespace gf {
