@@ -45,6 +45,12 @@ CONFIGS = {
                    roots=1 << 16, label="REDDIT-shaped TGAT 2-hop f10 (11K nodes, 672K edges, undirected, tau 48)"),
     "wiki": dict(nodes=9_000, edges=157_000, directed=False, tau=48, skew=2.2, src_skew=None, span=2_592_000,
                  roots=8_000, label="WIKI-shaped (9K nodes, 157K edges, undirected, tau 48)"),
+    # configs[4] at one GPU's share of the 8-way partition (owner = v % 8): 1/8 of the nodes and
+    # edges of the MAG shape, GraphSAGE-temporal uniform [15, 10], 10M-edge ingest batches
+    "mag8": dict(nodes=15_250_000, edges=162_500_000, directed=True, tau=8192, skew=2.2, src_skew=2.2, span=120,
+                 roots=1 << 20, fanouts=[15, 10], policies=("uniform",), batch=10_000_000, blocks_per_node=4,
+                 label="MAG-shaped 1/8 (one GPU's share of the 8-way partition: 15.25M nodes, 162.5M edges, "
+                       "directed, tau 8192, span 120) GraphSAGE uniform [15,10]"),
 }
 FANOUTS = [10, 10]
 POLICIES = ("recent", "uniform")
@@ -64,47 +70,79 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock + throttle reasons sampled every 2 ms during the timed region (NVML in a thread;
+    falls back to `nvidia-smi -lms 200` when NVML is unavailable)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index: int):
         self.index = index
-        self.rows: list[list[str]] = []
-        self.proc = None
+        self.rows: list[tuple[float, float, list[str]]] = []
+        self.stop = threading.Event()
+        self.t = None
+        self.nv = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.sample()  # at least one sample inside the region
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+        except Exception:  # noqa: BLE001 -- NVML missing: nvidia-smi below
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def sample(self):
+        nv = self.nv
+        mhz = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.rows.append((mhz, self.max_mhz, [n for n, a in self.REASONS if mask & getattr(nv, a, 0)]))
+
+    def _loop(self):
+        while not self.stop.wait(0.002):
+            try:
+                self.sample()
+            except Exception:  # noqa: BLE001
+                return
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
+        self.stop.set()
+        if self.t is not None:
+            self.t.join(timeout=2)
+        if self.nv is not None:
             try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+                self.sample()
+            except Exception:  # noqa: BLE001
+                pass
+        else:
+            self._smi_once()
+
+    def _smi_once(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                 capture_output=True, text=True, timeout=10).stdout
+            r = [x.strip() for x in out.split(",")]
+            names = [n for n, _ in self.REASONS]
+            self.rows.append((float(r[0]), float(r[1]), [n for n, v in zip(names, r[2:6]) if v.lower() == "active"]))
+        except (OSError, ValueError, IndexError, subprocess.SubprocessError):
+            pass
 
     def summary(self) -> dict:
-        rows = [r for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        reasons = sorted({n for r in rows for n, v in zip(names, r[2:6]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(float(r[0]) for r in rows), "sm_max_mhz": float(rows[0][1]),
-                "reasons": reasons, "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.rows[0][1],
+                "reasons": sorted({n for r in self.rows for n in r[2]}), "samples": len(self.rows),
+                "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 def dist_setup(args):
@@ -181,7 +219,7 @@ def build_graph(cfg, src, dst, ts, world, rank, device):
     g = gf.DynamicGraph(directed=cfg["directed"], tau=cfg["tau"], device=device)
     n = src.numel()
     slots = n * (1 if cfg["directed"] else 2)
-    g.reserve(cfg["nodes"], cfg["nodes"] * 16 + slots // max(1, cfg["tau"]) + 1024,
+    g.reserve(cfg["nodes"], cfg["nodes"] * cfg.get("blocks_per_node", 16) + slots // max(1, cfg["tau"]) + 1024,
               slots + min(cfg["nodes"] * cfg["tau"], slots // 2))
     from paper_2311_17410_b200.distributed import ReplicatedGraph, shard_range
 
@@ -347,7 +385,7 @@ def bench_ours(args, cfg, world, rank, local):
         kernels[name] = ent
     dom_name = max(base_bytes, key=lambda k: base_ms[k])
     achieved = base_bytes[dom_name] / (base_ms[dom_name] / 1e3) / 1e9
-    traffic = load_traffic().get(dom_name)
+    traffic = load_traffic().get(dom_name) if args.config == "gdelt" else None  # ncu capture is of the gdelt step
     pipe_ms = sum(v for k, v in base_ms.items() if k.startswith(("k_count", "k_write", "k_total", "cub_scan", "k_sample_fused")))
     pipe_gbs = (BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p) / (pipe_ms / 1e3) / 1e9 if pipe_ms else None
 
@@ -433,7 +471,7 @@ def bench_ours(args, cfg, world, rank, local):
                 "parallelism": f"replicas x{world}, root sharding (dp{world})",
             },
             "ingest": {"value": round(ingest_eps, 1), "unit": "edges/s",
-                       "note": "100K-edge batches through gf_graph_add_edges, device events; N>1 includes the NCCL all-gather"},
+                       "note": f"{INGEST_BATCH // 1000}K-edge batches through gf_graph_add_edges, device events; N>1 includes the NCCL all-gather"},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
                          "peak_source": pk["source"],
@@ -523,6 +561,10 @@ def main():
     ap.add_argument("--ref-chunk", type=int, default=16)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    global FANOUTS, POLICIES, INGEST_BATCH
+    FANOUTS = list(cfg.get("fanouts", FANOUTS))
+    POLICIES = tuple(cfg.get("policies", POLICIES))
+    INGEST_BATCH = cfg.get("batch", INGEST_BATCH)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         bench_reference(args, cfg, world, rank, local)
