@@ -97,7 +97,7 @@ __global__ void k_minmax(const int64_t* __restrict__ src, const int64_t* __restr
 
 // one event per (edge, stored endpoint), in the reference's append order
 __global__ void k_make_events(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n, int directed,
-                              uint32_t* keys, uint32_t* vals, const IngestCounters* c) {
+                              uint32_t* keys, uint32_t* vals, const IngestCounters* c, longlong2* trig) {
   if (c->abort) return;
   int64_t E = directed ? n : 2 * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
@@ -105,6 +105,7 @@ __global__ void k_make_events(const int64_t* __restrict__ src, const int64_t* __
     int side = directed ? 0 : (int)(e & 1);
     keys[e] = (uint32_t)(side ? dst[j] : src[j]);
     vals[e] = (uint32_t)e;
+    if (trig) trig[e] = make_longlong2(0, 0);
   }
 }
 
@@ -142,14 +143,16 @@ __global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __
   }
 }
 
-__global__ void k_accept_all(uint8_t* acc, int64_t n, const IngestCounters* c) {
-  if (c->viol || c->abort) return;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
-}
 
-__global__ void k_tmax_init(int64_t* tm, int64_t num_nodes, const int64_t* tail, const int64_t* bsize, const int64_t* btmax,
-                            const IngestCounters* c, const IngestScalars* S) {
-  if (!c->viol || c->abort) return;
+// chronology: accept everything, unless some stored endpoint may see a decreasing timestamp,
+// in which case per-node latest timestamps are prepared for the serial resolve
+__global__ void k_accept_prep(uint8_t* acc, int64_t n, int64_t* tm, int64_t num_nodes, const int64_t* tail,
+                              const int64_t* bsize, const int64_t* btmax, const IngestCounters* c, const IngestScalars* S) {
+  if (c->abort) return;
+  if (!c->viol) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
+    return;
+  }
   if (S) num_nodes = S->num_nodes;
   if (c->maxv + 1 > num_nodes) num_nodes = c->maxv + 1;  // nodes this batch creates have no tail
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < num_nodes; v += (int64_t)gridDim.x * blockDim.x)
@@ -191,6 +194,7 @@ __global__ void k_eids(const uint8_t* __restrict__ acc, const int64_t* __restric
       mx = max(mx, (long long)e);
     }
     out_eids[j] = e;
+    if (S) S->out_eids[j] = e;
     if (j == n - 1) c->n_acc = rank[j] + acc[j];
   }
   for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -226,18 +230,25 @@ struct SegPlan {
   int64_t* cstart;    // start in the compacted event list
   int64_t* fill;      // events that go into the current tail
   int64_t* tail_size; // tail size before the batch
-  int64_t* nb_new;    // new blocks (E+1, zero padded)
-  int64_t* slots_new; // new slots (E+1)
-  int64_t* dir_new;   // new directory capacity (E+1)
+  int64_t* nb_new;    // new blocks
+  longlong4* plan4;   // {new blocks, new slots, new directory capacity, 0} per segment, zero to E (scan input)
+};
+
+struct AddLL4 {
+  __device__ __forceinline__ longlong4 operator()(const longlong4& a, const longlong4& b) const {
+    return make_longlong4(a.x + b.x, a.y + b.y, a.z + b.z, 0);
+  }
 };
 
 __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                        const int64_t* __restrict__ cpos, const int64_t* __restrict__ ce_pend, int64_t E,
                        const IngestCounters* c, const int64_t* tail, const int64_t* bsize, const int64_t* bcap,
                        const int64_t* degree, const int64_t* num_blocks, const int64_t* dir_cap, int kind, int64_t tau,
-                       int64_t param, SegPlan P, const int64_t* nslots) {
+                       int64_t param, SegPlan P, int64_t* old_tail) {
   if (c->abort) return;
-  int64_t nseg = c->num_segs;
+  const int64_t nseg = c->num_segs;
+  for (int64_t s = nseg + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= E; s += (int64_t)gridDim.x * blockDim.x)
+    P.plan4[s] = make_longlong4(0, 0, 0, 0);
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     int64_t st = seg_start[s], en = (s + 1 < nseg) ? seg_start[s + 1] : E;
     int64_t cs = cpos[st], cnt = cpos[en] - cs;
@@ -245,6 +256,7 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
     P.acc_cnt[s] = cnt;
     P.cstart[s] = cs;
     int64_t t = tail[v];
+    old_tail[s] = t;
     int64_t fill = 0, tsz = 0;
     if (t != GF_NO_BLOCK) {
       tsz = bsize[t];
@@ -263,33 +275,29 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
       rem -= take;
     }
     P.nb_new[s] = blocks;
-    P.slots_new[s] = slots;
     int64_t need = num_blocks[v] + blocks;
-    int64_t dc = dir_cap[v];
+    int64_t dc = dir_cap[v], dnew = 0;
     if (need > dc) {
-      int64_t nc = 8;
-      while (nc < need) nc <<= 1;
-      P.dir_new[s] = nc;
-    } else {
-      P.dir_new[s] = 0;
+      dnew = 8;
+      while (dnew < need) dnew <<= 1;
     }
+    P.plan4[s] = make_longlong4(blocks, slots, dnew, 0);
   }
 }
 
-__global__ void k_totals(const int64_t* blkoff, const int64_t* slotsoff, const int64_t* diroff, int64_t E, IngestCounters* c) {
+__global__ void k_totals(const longlong4* off4, int64_t E, IngestCounters* c) {
   if (threadIdx.x || blockIdx.x || c->abort) return;
-  c->new_blocks = blkoff[E];
-  c->new_slots = slotsoff[E];
-  c->dir_need = diroff[E];
+  c->new_blocks = off4[E].x;
+  c->new_slots = off4[E].y;
+  c->dir_need = off4[E].z;
 }
 
 // sync-free path: totals + capacity check against the host-known pool state
-__global__ void k_totals_check(const int64_t* blkoff, const int64_t* slotsoff, const int64_t* diroff, int64_t E,
-                               const IngestScalars* S, IngestCounters* c) {
+__global__ void k_totals_check(const longlong4* off4, int64_t E, const IngestScalars* S, IngestCounters* c) {
   if (threadIdx.x || blockIdx.x || c->abort) return;
-  c->new_blocks = blkoff[E];
-  c->new_slots = slotsoff[E];
-  c->dir_need = diroff[E];
+  c->new_blocks = off4[E].x;
+  c->new_slots = off4[E].y;
+  c->dir_need = off4[E].z;
   if (c->new_slots > S->slots_free || c->dir_need > S->dir_free) c->abort |= ABORT_CAP;
 }
 
@@ -304,7 +312,7 @@ struct Recs {
 };
 
 __global__ void k_enumerate(const int64_t* __restrict__ ce_pend, const uint32_t* __restrict__ ce_ev, const IngestCounters* c,
-                            const int64_t* __restrict__ blkoff, const int64_t* __restrict__ keys_node_of_seg_unused,
+                            const longlong4* __restrict__ off4, const int64_t* __restrict__ keys_node_of_seg_unused,
                             SegPlan P, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                             const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R, longlong2* trig) {
   if (c->abort) return;
@@ -315,7 +323,7 @@ __global__ void k_enumerate(const int64_t* __restrict__ ce_pend, const uint32_t*
     int64_t v = keys[seg_start[s]];
     int64_t cs = P.cstart[s], cnt = P.acc_cnt[s], fill = P.fill[s];
     int64_t deg = degree[v] + fill, used = fill, rem = cnt - fill;
-    int64_t r = blkoff[s];
+    int64_t r = off4[s].x;
     while (rem > 0) {
       int64_t cap = sizing_cap(kind, tau, param, deg, ce_pend[cs + used]);
       int64_t take = min(cap, rem);
@@ -350,7 +358,7 @@ struct BlockArrays {
 };
 
 __global__ void k_write_blocks(const uint32_t* __restrict__ perm, int64_t nrec, int64_t blk_used, int64_t slots_used,
-                               const int64_t* __restrict__ base_scan, Recs R, const int64_t* __restrict__ blkoff, SegPlan P,
+                               const int64_t* __restrict__ base_scan, Recs R, const longlong4* __restrict__ off4, SegPlan P,
                                const uint32_t* __restrict__ ce_ev, const uint32_t* __restrict__ keys,
                                const int64_t* __restrict__ seg_start, const int64_t* tail, const int64_t* __restrict__ ts,
                                int directed, BlockArrays B) {
@@ -358,7 +366,7 @@ __global__ void k_write_blocks(const uint32_t* __restrict__ perm, int64_t nrec, 
     uint32_t rec = perm[r];
     int64_t h = R.handle[rec];
     int32_t s = R.seg[rec];
-    int64_t k = rec - blkoff[s], nb = P.nb_new[s];
+    int64_t k = rec - off4[s].x, nb = P.nb_new[s];
     int64_t cs = P.cstart[s];
     int64_t f = R.first[rec], cnt = R.count[rec];
     B.cap[h] = R.cap[rec];
@@ -383,7 +391,7 @@ struct DirArrays {
 };
 
 __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
-                           SegPlan P, const int64_t* __restrict__ blkoff, const int64_t* __restrict__ diroff, int64_t dir_used,
+                           SegPlan P, const longlong4* __restrict__ off4, int64_t dir_used,
                            Recs R, const uint32_t* __restrict__ ce_ev, const int64_t* __restrict__ ts, int directed,
                            NodeArrays N, BlockArrays B, DirArrays D, int kind, const IngestScalars* S) {
   if (c->abort) return;
@@ -403,20 +411,21 @@ __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__
       B.tmax[t] = ts[ev_edge(ce_ev[cs + fill - 1], directed)];
     }
     if (nb > 0) {
-      int64_t h0 = R.handle[blkoff[s]];
+      const int64_t r0 = off4[s].x;
+      int64_t h0 = R.handle[r0];
       if (t == GF_NO_BLOCK) N.head[v] = h0;
       else B.next[t] = h0;
-      N.tail[v] = R.handle[blkoff[s] + nb - 1];
+      N.tail[v] = R.handle[r0 + nb - 1];
       // block directory: grow (copy) if needed, then append the new blocks
-      if (P.dir_new[s] > 0) {
-        int64_t no = dir_used + diroff[s], oo = N.dir_off[v];
+      if (P.plan4[s].z > 0) {
+        int64_t no = dir_used + off4[s].z, oo = N.dir_off[v];
         for (int64_t w = 0; w < nb_old * DIRW; w++) D.e[no * DIRW + w] = D.e[oo * DIRW + w];
         N.dir_off[v] = no;
-        N.dir_cap[v] = P.dir_new[s];
+        N.dir_cap[v] = P.plan4[s].z;
       }
       int64_t d0 = N.dir_off[v] + nb_old;
       for (int64_t k = 0; k < nb; k++) {
-        int64_t rec = blkoff[s] + k, h = R.handle[rec];
+        int64_t rec = r0 + k, h = R.handle[rec];
         int64_t* e = D.e + (d0 + k) * DIRW;
         e[0] = B.tmin[h];
         e[1] = ns_old + R.first[rec];
@@ -446,7 +455,7 @@ __global__ void k_noderec_invalidate(int64_t* nrec, int64_t v) { nrec[v * NREC +
 
 __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restrict__ ce_seg, const uint32_t* __restrict__ ce_ev,
                                 const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start, SegPlan P,
-                                const int64_t* __restrict__ blkoff, Recs R, const int64_t* tail_before_unused,
+                                const longlong4* __restrict__ off4, Recs R, const int64_t* tail_before_unused,
                                 const int64_t* __restrict__ bbase, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
                                 const int64_t* __restrict__ ts, const int64_t* __restrict__ eids, int directed,
                                 const int64_t* __restrict__ old_tail, Slot* slots, int64_t* sts, int64_t* fts) {
@@ -468,7 +477,7 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
     if (r < fill) {
       pos = bbase[old_tail[s]] + P.tail_size[s] + r;
     } else {
-      int64_t lo = blkoff[s], hi = blkoff[s] + P.nb_new[s];  // last rec with first <= r
+      int64_t lo = off4[s].x, hi = lo + P.nb_new[s];  // last rec with first <= r
       while (hi - lo > 1) {
         int64_t m = (lo + hi) >> 1;
         if (R.first[m] <= r) lo = m;
@@ -489,13 +498,6 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
   }
 }
 
-__global__ void k_old_tail(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
-                           const int64_t* tail, int64_t* old_tail) {
-  if (c->abort) return;
-  int64_t nseg = c->num_segs;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x)
-    old_tail[s] = tail[keys[seg_start[s]]];
-}
 
 template <class F>
 gf_status cub_call(F f, cudaStream_t s) {
@@ -601,54 +603,51 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   if (hc.minv < 0) return fail(GF_EINVAL, "node ids must be non-negative");  // storage.py:408-409
   GF_TRY(ensure_nodes(g, hc.maxv + 1, s));                                  // storage.py:410-412
 
-  // ---- scratch --------------------------------------------------------------
+  // ---- scratch: one carve sequence, run once to size the buffer and once to place it ----
+  uint32_t *keys_in, *keys, *vals_in, *vals, *ce_ev;
+  int32_t *heads, *incl, *ce_seg;
+  int64_t *seg_start, *rank, *tm, *keep, *cpos, *ce_pend, *old_tail;
+  uint8_t* acc;
+  longlong4* off4;
+  SegPlan P;
+  auto carve = [&](Arena& A) {
+    keys_in = A.take<uint32_t>(E);
+    keys = A.take<uint32_t>(E);
+    vals_in = A.take<uint32_t>(E);
+    vals = A.take<uint32_t>(E);
+    heads = A.take<int32_t>(E);
+    incl = A.take<int32_t>(E);
+    seg_start = A.take<int64_t>(E + 1);
+    acc = A.take<uint8_t>(n);
+    rank = A.take<int64_t>(n + 1);
+    tm = A.take<int64_t>(g->num_nodes);
+    keep = A.take<int64_t>(E + 1);
+    cpos = A.take<int64_t>(E + 1);
+    ce_ev = A.take<uint32_t>(E);
+    ce_pend = A.take<int64_t>(E);
+    ce_seg = A.take<int32_t>(E);
+    P.acc_cnt = A.take<int64_t>(E + 1);
+    P.cstart = A.take<int64_t>(E + 1);
+    P.fill = A.take<int64_t>(E + 1);
+    P.tail_size = A.take<int64_t>(E + 1);
+    P.nb_new = A.take<int64_t>(E + 1);
+    P.plan4 = A.take<longlong4>(E + 1);
+    off4 = A.take<longlong4>(E + 1);
+    old_tail = A.take<int64_t>(E + 1);
+  };
   Scratch sb(s);
-  Arena A;
-  size_t need = 0;
   {
     Arena probe;
-    probe.take<uint32_t>(E); probe.take<uint32_t>(E); probe.take<uint32_t>(E); probe.take<uint32_t>(E);
-    probe.take<int32_t>(E); probe.take<int32_t>(E); probe.take<int64_t>(E + 1);
-    probe.take<uint8_t>(n); probe.take<int64_t>(n + 1); probe.take<int64_t>(g->num_nodes);
-    probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1);
-    probe.take<uint32_t>(E); probe.take<int64_t>(E); probe.take<int32_t>(E);
-    for (int q = 0; q < 7; q++) probe.take<int64_t>(E + 1);
-    probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1); probe.take<int64_t>(E + 1);
-    need = probe.off + 4096;
+    carve(probe);
+    GF_TRY(sb.alloc(probe.off + 4096));
+    Arena A;
+    A.base = sb.as<char>();
+    carve(A);
   }
-  GF_TRY(sb.alloc(need));
-  A.base = sb.as<char>();
-  uint32_t* keys_in = A.take<uint32_t>(E);
-  uint32_t* keys = A.take<uint32_t>(E);
-  uint32_t* vals_in = A.take<uint32_t>(E);
-  uint32_t* vals = A.take<uint32_t>(E);
-  int32_t* heads = A.take<int32_t>(E);
-  int32_t* incl = A.take<int32_t>(E);
-  int64_t* seg_start = A.take<int64_t>(E + 1);
-  uint8_t* acc = A.take<uint8_t>(n);
-  int64_t* rank = A.take<int64_t>(n + 1);
-  int64_t* tm = A.take<int64_t>(g->num_nodes);
-  int64_t* keep = A.take<int64_t>(E + 1);
-  int64_t* cpos = A.take<int64_t>(E + 1);
-  uint32_t* ce_ev = A.take<uint32_t>(E);
-  int64_t* ce_pend = A.take<int64_t>(E);
-  int32_t* ce_seg = A.take<int32_t>(E);
-  SegPlan P;
-  P.acc_cnt = A.take<int64_t>(E + 1);
-  P.cstart = A.take<int64_t>(E + 1);
-  P.fill = A.take<int64_t>(E + 1);
-  P.tail_size = A.take<int64_t>(E + 1);
-  P.nb_new = A.take<int64_t>(E + 1);
-  P.slots_new = A.take<int64_t>(E + 1);
-  P.dir_new = A.take<int64_t>(E + 1);
-  int64_t* blkoff = A.take<int64_t>(E + 1);
-  int64_t* slotsoff = A.take<int64_t>(E + 1);
-  int64_t* diroff = A.take<int64_t>(E + 1);
-  int64_t* old_tail = A.take<int64_t>(E + 1);
 
   const int T = 256;
   const int64_t G = 8 * num_sms();
-  GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc);
+  GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc, nullptr);
   int endbit = bits_for(g->num_nodes);
   GF_TRY(cub_call([&](void* t, size_t& b) {
     return cub::DeviceRadixSort::SortPairs(t, b, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s);
@@ -658,8 +657,8 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
             seg_start, dc);
   // chronology: accept all unless some stored endpoint sees a decreasing timestamp
-  GF_LAUNCH(k_accept_all, grid_for(n, T, G), T, 0, s, acc, n, dc);
-  GF_LAUNCH(k_tmax_init, grid_for(g->num_nodes, T, G), T, 0, s, tm, g->num_nodes, g->tail, g->bsize, g->btmax, dc, nullptr);
+  GF_LAUNCH(k_accept_prep, grid_for(std::max(n, g->num_nodes), T, G), T, 0, s, acc, n, tm, g->num_nodes, g->tail,
+            g->bsize, g->btmax, dc, nullptr);
   GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
   // edge ids by scan (storage.py:438-442)
   GF_TRY(cub_call([&](void* t, size_t& b) {
@@ -669,16 +668,12 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
   GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, keep, cpos, (int)(E + 1), s); }, s));
   GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
-  GF_CUDA(cudaMemsetAsync(P.nb_new, 0, sizeof(int64_t) * (E + 1), s));
-  GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
-  GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
-  GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
-            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots);
-  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.nb_new, blkoff, (int)(E + 1), s); }, s));
-  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.slots_new, slotsoff, (int)(E + 1), s); }, s));
-  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, P.dir_new, diroff, (int)(E + 1), s); }, s));
-  GF_LAUNCH(k_totals, 1, 1, 0, s, blkoff, slotsoff, diroff, E, dc);
-  GF_LAUNCH(k_old_tail, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, g->tail, old_tail);
+  GF_LAUNCH(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
+            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, old_tail);
+  GF_TRY(cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveScan(t, b, P.plan4, off4, AddLL4(), make_longlong4(0, 0, 0, 0), (int)(E + 1), s);
+  }, s));
+  GF_LAUNCH(k_totals, 1, 1, 0, s, off4, E, dc);
   GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
 
@@ -717,7 +712,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   if (nfree && nrec) GF_CUDA(cudaMemcpyAsync(d_free, g->free_handles.data(), 8 * nfree, cudaMemcpyHostToDevice, s));
 
   if (nrec > 0) {
-    GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
+    GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, off4, nullptr, P, keys, seg_start,
               g->degree, g->sizing_kind, g->tau, g->sizing_param, R, nullptr);
     int kb = bits_for(E + 1);
     GF_TRY(cub_call([&](void* t, size_t& b) {
@@ -730,16 +725,16 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     }, s));
     BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
     GF_LAUNCH(k_write_blocks, grid_for(nrec, T, G), T, 0, s, perm, nrec, g->blk_used, g->slots_used, base_scan, R,
-              blkoff, P, ce_ev, keys, seg_start, g->tail, ts, dir, B);
+              off4, P, ce_ev, keys, seg_start, g->tail, ts, dir, B);
   }
   if (hc.n_acc > 0) {
     BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
     NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid, g->nflags,
                  g->nrec};
     DirArrays D{g->dir};
-    GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, g->dir_used, R, ce_ev, ts,
+    GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, off4, g->dir_used, R, ce_ev, ts,
               dir, N, B, D, g->sizing_kind, nullptr);
-    GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
+    GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, off4, R, nullptr,
               g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
   }
   g->blk_used += nfresh;
@@ -766,13 +761,6 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
 // triggering event order), so there is no sort over new blocks and no mid-call host sync:
 // one launch sequence, one synchronisation at the end (for the rejected count).
 
-__global__ void k_counters_init(IngestCounters* c) {
-  c->minv = LLONG_MAX;
-  c->maxv = LLONG_MIN;
-  c->viol = c->num_segs = c->n_acc = c->new_blocks = c->new_slots = c->dir_need = 0;
-  c->max_eid = LLONG_MIN;
-  c->abort = 0;
-}
 
 // node-table growth on the device: rows [lo, maxv + 1) when they fit the capacity
 __global__ void k_grow_nodes(IngestCounters* c, const IngestScalars* S, int64_t cap, int64_t* head, int64_t* tail,
@@ -809,43 +797,42 @@ struct AddLL2 {
 };
 
 // record r (segment-major enumeration): handle = blk_used + #allocations triggered by earlier
-// events, slot base = slots_used + their capacities
-__global__ void k_handles_by_scan(const IngestCounters* c, Recs R, const longlong2* __restrict__ tscan,
-                                  const IngestScalars* S, int64_t* rbase) {
+// events, slot base = slots_used + their capacities; neighbours' handles are recomputed locally
+__global__ void k_write_blocks_scan(const IngestCounters* c, Recs R, const longlong2* __restrict__ tscan,
+                                    const IngestScalars* S, const longlong4* __restrict__ off4, SegPlan P,
+                                    const uint32_t* __restrict__ ce_ev, const uint32_t* __restrict__ keys,
+                                    const int64_t* __restrict__ seg_start, const int64_t* tail,
+                                    const int64_t* __restrict__ ts, int directed, BlockArrays B) {
   if (c->abort) return;
-  const int64_t blk_used = S->blk_used, slots_used = S->slots_used;
-  const int64_t nrec = c->new_blocks;
+  const int64_t nrec = c->new_blocks, blk_used = S->blk_used, slots_used = S->slots_used;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
     const longlong2 t = tscan[R.key[r]];
-    R.handle[r] = blk_used + t.x;
-    rbase[r] = slots_used + t.y;
-  }
-}
-
-__global__ void k_write_blocks_scan(const IngestCounters* c, Recs R, const int64_t* __restrict__ rbase,
-                                    const int64_t* __restrict__ blkoff, SegPlan P, const uint32_t* __restrict__ ce_ev,
-                                    const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
-                                    const int64_t* tail, const int64_t* __restrict__ ts, int directed, BlockArrays B) {
-  if (c->abort) return;
-  const int64_t nrec = c->new_blocks;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t h = R.handle[r];
+    const int64_t h = blk_used + t.x;
+    R.handle[r] = h;
     const int32_t s = R.seg[r];
-    const int64_t k = r - blkoff[s], nb = P.nb_new[s], cs = P.cstart[s];
+    const int64_t k = r - off4[s].x, nb = P.nb_new[s], cs = P.cstart[s];
     const int64_t f = R.first[r], cnt = R.count[r];
     B.cap[h] = R.cap[r];
     B.size[h] = cnt;
     B.tmin[h] = ts[ev_edge(ce_ev[cs + f], directed)];
     B.tmax[h] = ts[ev_edge(ce_ev[cs + f + cnt - 1], directed)];
-    B.base[h] = rbase[r];
+    B.base[h] = slots_used + t.y;
     const int64_t v = keys[seg_start[s]];
-    B.prev[h] = (k == 0) ? tail[v] : R.handle[r - 1];
-    B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : R.handle[r + 1];
+    B.prev[h] = (k == 0) ? tail[v] : blk_used + tscan[R.key[r - 1]].x;
+    B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : blk_used + tscan[R.key[r + 1]].x;
   }
 }
 
 // batch inputs -> fixed staging buffers (the captured sequence always reads the same addresses)
-__global__ void k_stage(const IngestScalars* S, int64_t n, int64_t* src, int64_t* dst, int64_t* ts, int64_t* eids) {
+__global__ void k_stage(const IngestScalars* S, int64_t n, int64_t* src, int64_t* dst, int64_t* ts, int64_t* eids,
+                        IngestCounters* c) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c->minv = LLONG_MAX;
+    c->maxv = LLONG_MIN;
+    c->viol = c->num_segs = c->n_acc = c->new_blocks = c->new_slots = c->dir_need = 0;
+    c->max_eid = LLONG_MIN;
+    c->abort = 0;
+  }
   const bool has_eids = S->eids_in != nullptr;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     src[j] = S->src[j];
@@ -855,10 +842,6 @@ __global__ void k_stage(const IngestScalars* S, int64_t n, int64_t* src, int64_t
   }
 }
 
-__global__ void k_unstage(const IngestScalars* S, int64_t n, const int64_t* out) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    S->out_eids[j] = out[j];
-}
 
 // node capacity only (rows are initialised on the device by k_grow_nodes)
 gf_status grow_node_cap(gf_graph* g, int64_t need, cudaStream_t s) {
@@ -915,6 +898,9 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, b, (longlong2*)nullptr, (longlong2*)nullptr, AddLL2(),
                                              make_longlong2(0, 0), (int)E, s));
       cub_bytes = std::max(cub_bytes, b);
+      GF_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, b, (longlong4*)nullptr, (longlong4*)nullptr, AddLL4(),
+                                             make_longlong4(0, 0, 0, 0), (int)(E + 1), s));
+      cub_bytes = std::max(cub_bytes, b);
     }
     // scratch layout (one persistent buffer per graph)
     auto layout = [&](Arena& a, void** p) {
@@ -927,11 +913,12 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       p[i++] = a.take<uint8_t>(n); p[i++] = a.take<int64_t>(n + 1); p[i++] = a.take<int64_t>(node_cap);
       p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);
       p[i++] = a.take<uint32_t>(E); p[i++] = a.take<int64_t>(E); p[i++] = a.take<int32_t>(E);
-      for (int q = 0; q < 7; q++) p[i++] = a.take<int64_t>(E + 1);
-      for (int q = 0; q < 4; q++) p[i++] = a.take<int64_t>(E + 1);
+      for (int q = 0; q < 5; q++) p[i++] = a.take<int64_t>(E + 1);  // acc_cnt, cstart, fill, tail_size, nb_new
+      p[i++] = a.take<longlong4>(E + 1); p[i++] = a.take<longlong4>(E + 1);  // plan4, off4
+      p[i++] = a.take<int64_t>(E + 1);  // old_tail
       for (int q = 0; q < 3; q++) p[i++] = a.take<int64_t>(E + 1);  // R.first/count/cap
       p[i++] = a.take<int32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);  // R.seg/key/idx
-      p[i++] = a.take<int64_t>(E + 1); p[i++] = a.take<int64_t>(E + 1);  // R.handle, rbase
+      p[i++] = a.take<int64_t>(E + 1);  // R.handle
       p[i++] = a.take<longlong2>(E); p[i++] = a.take<longlong2>(E);      // trig, tscan
       p[i++] = a.take<char>((int64_t)cub_bytes);
       return i;
@@ -980,11 +967,8 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     P.fill = (int64_t*)P_[i++];
     P.tail_size = (int64_t*)P_[i++];
     P.nb_new = (int64_t*)P_[i++];
-    P.slots_new = (int64_t*)P_[i++];
-    P.dir_new = (int64_t*)P_[i++];
-    int64_t* blkoff = (int64_t*)P_[i++];
-    int64_t* slotsoff = (int64_t*)P_[i++];
-    int64_t* diroff = (int64_t*)P_[i++];
+    P.plan4 = (longlong4*)P_[i++];
+    longlong4* off4 = (longlong4*)P_[i++];
     int64_t* old_tail = (int64_t*)P_[i++];
     Recs R;
     R.first = (int64_t*)P_[i++];
@@ -994,7 +978,6 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     R.key = (uint32_t*)P_[i++];
     R.idx = (uint32_t*)P_[i++];
     R.handle = (int64_t*)P_[i++];
-    int64_t* rbase = (int64_t*)P_[i++];
     longlong2* trig = (longlong2*)P_[i++];
     longlong2* tscan = (longlong2*)P_[i++];
     void* cubtmp = P_[i++];
@@ -1007,20 +990,19 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     auto enqueue = [&](cudaStream_t s) -> gf_status {
       size_t tb = cub_bytes;
       GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
-      GF_LAUNCH(k_counters_init, 1, 1, 0, s, dc);
-      GF_LAUNCH(k_stage, grid_for(n, T, G), T, 0, s, ds, n, src, dst, ts, eids_st);
+      GF_LAUNCH(k_stage, grid_for(n, T, G), T, 0, s, ds, n, src, dst, ts, eids_st, dc);
       GF_LAUNCH(k_minmax, grid_for(n, T, 2 * num_sms()), T, 0, s, src, dst, n, dc);
       GF_LAUNCH(k_grow_nodes, grid_for(2 * n, T, G), T, 0, s, dc, ds, node_cap, g->head, g->tail, g->num_blocks,
                 g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
-      GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc);
+      GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc, trig);
       GF_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, tb, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s));
       GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::InclusiveSum(cubtmp, tb, heads, incl, (int)E, s));
       GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
                 seg_start, dc);
-      GF_LAUNCH(k_accept_all, grid_for(n, T, G), T, 0, s, acc, n, dc);
-      GF_LAUNCH(k_tmax_init, grid_for(node_cap, T, G), T, 0, s, tm, 0, g->tail, g->bsize, g->btmax, dc, ds);
+      GF_LAUNCH(k_accept_prep, grid_for(std::max(n, node_cap), T, G), T, 0, s, acc, n, tm, 0, g->tail, g->bsize,
+                g->btmax, dc, ds);
       GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, acc, rank, (int)n, s));
@@ -1029,36 +1011,26 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, cpos, (int)(E + 1), s));
       GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
-      GF_CUDA(cudaMemsetAsync(P.nb_new, 0, sizeof(int64_t) * (E + 1), s));
-      GF_CUDA(cudaMemsetAsync(P.slots_new, 0, sizeof(int64_t) * (E + 1), s));
-      GF_CUDA(cudaMemsetAsync(P.dir_new, 0, sizeof(int64_t) * (E + 1), s));
-      GF_CUDA(cudaMemsetAsync(trig, 0, sizeof(longlong2) * E, s));
-      GF_LAUNCH(k_plan, grid_for(E, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
-                g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, g->nslots);
+      GF_LAUNCH(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize,
+                g->bcap, g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, old_tail);
       tb = cub_bytes;
-      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.nb_new, blkoff, (int)(E + 1), s));
-      tb = cub_bytes;
-      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.slots_new, slotsoff, (int)(E + 1), s));
-      tb = cub_bytes;
-      GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, P.dir_new, diroff, (int)(E + 1), s));
-      GF_LAUNCH(k_totals_check, 1, 1, 0, s, blkoff, slotsoff, diroff, E, ds, dc);
-      GF_LAUNCH(k_old_tail, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, g->tail, old_tail);
-      GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, blkoff, nullptr, P, keys, seg_start,
+      GF_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, tb, P.plan4, off4, AddLL4(), make_longlong4(0, 0, 0, 0), (int)(E + 1),
+                                             s));
+      GF_LAUNCH(k_totals_check, 1, 1, 0, s, off4, E, ds, dc);
+      GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, off4, nullptr, P, keys, seg_start,
                 g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, tb, trig, tscan, AddLL2(), make_longlong2(0, 0), (int)E, s));
-      GF_LAUNCH(k_handles_by_scan, grid_for(E, T, G), T, 0, s, dc, R, tscan, ds, rbase);
       BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
-      GF_LAUNCH(k_write_blocks_scan, grid_for(E, T, G), T, 0, s, dc, R, rbase, blkoff, P, ce_ev, keys, seg_start,
+      GF_LAUNCH(k_write_blocks_scan, grid_for(E, T, G), T, 0, s, dc, R, tscan, ds, off4, P, ce_ev, keys, seg_start,
                 g->tail, ts, dir, B);
       NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
                    g->nflags, g->nrec};
       DirArrays D{g->dir};
-      GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, blkoff, diroff, 0, R, ce_ev, ts, dir, N,
-                B, D, g->sizing_kind, ds);
-      GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, blkoff, R, nullptr,
+      GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, off4, 0, R, ce_ev, ts, dir, N, B, D,
+                g->sizing_kind, ds);
+      GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, off4, R, nullptr,
                 g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
-      GF_LAUNCH(k_unstage, grid_for(n, T, G), T, 0, s, ds, n, out_eids);
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
     };

@@ -1,7 +1,7 @@
 """Summarise scripts/ncu_sampler.sh output into profiles/.
 
-Reads gpurun_out/prof.ncu-rep (ncu --set full, the 8 sampler launches of one step, in launch
-order recent/hop0, recent/hop1, uniform/hop0, uniform/hop1 x count/write) and
+Reads gpurun_out/prof.ncu-rep (ncu --set full, the 4 fused sampler launches of one step, in launch
+order recent/hop0, recent/hop1, uniform/hop0, uniform/hop1) and
 gpurun_out/launches.csv (the launch list), writes
   profiles/<round>_ncu_sampler_launches.json  per-launch metrics
   profiles/ncu_traffic.json                   dram read+write bytes per launch, averaged per kernel
@@ -49,12 +49,11 @@ def raw_rows(rep: str) -> list[dict]:
 def main() -> None:
     rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
     rows = raw_rows(os.path.join(ROOT, "gpurun_out", "prof.ncu-rep"))
-    summ, traffic, seen = {}, {}, {}
-    for r in rows:
-        name = r["Kernel Name"].split("(")[0].split()[-1].split("::")[-1]
-        i = seen.get(name, 0)
-        seen[name] = i + 1
-        tag = TAGS[i] if i < len(TAGS) else f"#{i}"
+    summ, traffic = {}, {}
+    for i, r in enumerate(rows):
+        # launches come in step order; the tag follows the launch index (template args stripped)
+        name = r["Kernel Name"].split("(")[0].split()[-1].split("::")[-1].split("<")[0]
+        tag = TAGS[i % len(TAGS)] if len(rows) <= len(TAGS) else f"#{i}"
         e = {
             "ms": round(to_float(r["gpu__time_duration.sum"]) / 1e6, 6),
             "dram_read_GB": round(to_float(r["dram__bytes_read.sum"]) / 1e9, 6),
