@@ -34,6 +34,7 @@ struct IngestCounters {
   long long dir_need;     // directory entries to allocate
   long long max_eid;      // max preassigned accepted id
   long long abort;        // sync-free path: ABORT_* bits, nothing was mutated
+  long long tsmin, tsmax; // timestamp range of the batch (32-bit fence validity)
 };
 constexpr long long ABORT_NODES = 1, ABORT_CAP = 2;
 
@@ -77,21 +78,27 @@ __global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tai
   }
 }
 
-__global__ void k_minmax(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n,
-                         IngestCounters* c) {
-  long long mn = LLONG_MAX, mx = LLONG_MIN;
+__global__ void k_minmax(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, const int64_t* __restrict__ ts,
+                         int64_t n, IngestCounters* c) {
+  long long mn = LLONG_MAX, mx = LLONG_MIN, tn = LLONG_MAX, tx = LLONG_MIN;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    long long a = src[i], b = dst[i];
+    long long a = src[i], b = dst[i], t = ts[i];
     mn = min(mn, min(a, b));
     mx = max(mx, max(a, b));
+    tn = min(tn, t);
+    tx = max(tx, t);
   }
   for (int o = 16; o; o >>= 1) {
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    tn = min(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+    tx = max(tx, __shfl_xor_sync(0xffffffffu, tx, o));
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMin(&c->minv, mn);
     atomicMax(&c->maxv, mx);
+    atomicMin(&c->tsmin, tn);
+    atomicMax(&c->tsmax, tx);
   }
 }
 
@@ -458,7 +465,8 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
                                 const longlong4* __restrict__ off4, Recs R, const int64_t* tail_before_unused,
                                 const int64_t* __restrict__ bbase, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
                                 const int64_t* __restrict__ ts, const int64_t* __restrict__ eids, int directed,
-                                const int64_t* __restrict__ old_tail, Slot* slots, int64_t* sts, int64_t* fts) {
+                                const int64_t* __restrict__ old_tail, Slot* slots, int64_t* sts, int64_t* fts,
+                                int32_t* fts16) {
   if (c->abort) return;
   int64_t nacc_ev = 0;
   {
@@ -495,6 +503,7 @@ __global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restri
     slots[pos] = sl;
     sts[pos] = sl.ts;
     if ((pos & (FENCE - 1)) == 0) fts[pos / FENCE] = sl.ts;
+    if ((pos & (FENCE16 - 1)) == 0) fts16[pos / FENCE16] = (int32_t)max(min(sl.ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);
   }
 }
 
@@ -565,6 +574,7 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
   GF_TRY(grow_array(g->slots, g->slots_used, nc, s));
   GF_TRY(grow_array(g->sts, g->slots_used, nc + 2 * FENCE, s));  // window loads may read past the end
   GF_TRY(grow_array(g->fts, (g->slots_used + FENCE - 1) / FENCE, nc / FENCE + 8, s));  // chunk loads read up to 3 past
+  GF_TRY(grow_array(g->fts16, (g->slots_used + FENCE16 - 1) / FENCE16, nc / FENCE16 + 16, s));  // up to 7 past
   // unused capacity slots must read as invalid (delete scans the whole pool)
   GF_CUDA(cudaMemsetAsync(g->slots + old, 0, sizeof(Slot) * (size_t)(nc - old), s));
   g->slot_cap = nc;
@@ -596,8 +606,10 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
   hc.minv = LLONG_MAX;
   hc.maxv = LLONG_MIN;
   hc.max_eid = LLONG_MIN;
+  hc.tsmin = LLONG_MAX;
+  hc.tsmax = LLONG_MIN;
   GF_CUDA(cudaMemcpyAsync(dc, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
-  GF_LAUNCH(k_minmax, grid_for(n, 256, 2 * num_sms()), 256, 0, s, src, dst, n, dc);
+  GF_LAUNCH(k_minmax, grid_for(n, 256, 2 * num_sms()), 256, 0, s, src, dst, ts, n, dc);
   GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
   if (hc.minv < 0) return fail(GF_EINVAL, "node ids must be non-negative");  // storage.py:408-409
@@ -735,7 +747,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, off4, g->dir_used, R, ce_ev, ts,
               dir, N, B, D, g->sizing_kind, nullptr);
     GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, off4, R, nullptr,
-              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
+              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts, g->fts16);
   }
   g->blk_used += nfresh;
   g->free_handles.resize(nfree - std::min(nfree, nrec));
@@ -747,6 +759,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     g->next_edge_id += hc.n_acc;
   }
   g->total_edges_inserted += hc.n_acc;
+  if (hc.tsmin < INT32_MIN || hc.tsmax > INT32_MAX) g->ts32 = 0;  // the 32-bit fence is no longer exact
   if (h_rej) *h_rej = n - hc.n_acc;
   GF_CUDA(cudaGetLastError());
   return GF_OK;
@@ -832,6 +845,8 @@ __global__ void k_stage(const IngestScalars* S, int64_t n, int64_t* src, int64_t
     c->viol = c->num_segs = c->n_acc = c->new_blocks = c->new_slots = c->dir_need = 0;
     c->max_eid = LLONG_MIN;
     c->abort = 0;
+    c->tsmin = LLONG_MAX;
+    c->tsmax = LLONG_MIN;
   }
   const bool has_eids = S->eids_in != nullptr;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -991,7 +1006,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       size_t tb = cub_bytes;
       GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
       GF_LAUNCH(k_stage, grid_for(n, T, G), T, 0, s, ds, n, src, dst, ts, eids_st, dc);
-      GF_LAUNCH(k_minmax, grid_for(n, T, 2 * num_sms()), T, 0, s, src, dst, n, dc);
+      GF_LAUNCH(k_minmax, grid_for(n, T, 2 * num_sms()), T, 0, s, src, dst, ts, n, dc);
       GF_LAUNCH(k_grow_nodes, grid_for(2 * n, T, G), T, 0, s, dc, ds, node_cap, g->head, g->tail, g->num_blocks,
                 g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
       GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc, trig);
@@ -1030,7 +1045,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, off4, 0, R, ce_ev, ts, dir, N, B, D,
                 g->sizing_kind, ds);
       GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, off4, R, nullptr,
-                g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts);
+                g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts, g->fts16);
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
     };
@@ -1096,6 +1111,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     g->next_edge_id += hc.n_acc;
   }
   g->total_edges_inserted += hc.n_acc;
+  if (hc.tsmin < INT32_MIN || hc.tsmax > INT32_MAX) g->ts32 = 0;  // the 32-bit fence is no longer exact
   if (h_rej) *h_rej = n - hc.n_acc;
   return GF_OK;
 }
@@ -1144,7 +1160,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dir,
-                g->slots, g->sts, g->fts, g->nflags, g->nrec, g->ing_buf};
+                g->slots, g->sts, g->fts, g->fts16, g->nflags, g->nrec, g->ing_buf};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);
@@ -1285,7 +1301,7 @@ gf_status gf_graph_get_info(gf_graph* g, gf_graph_info* out) {
   out->sizing_kind = g->sizing_kind;
   out->sizing_param = g->sizing_param;
   out->device_bytes = g->node_cap * (8 * 7 + 2 + 8 * NREC) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * DIRW +
-                      g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8;
+                      g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8 + (g->slot_cap / FENCE16 + 16) * 4;
   return GF_OK;
 }
 

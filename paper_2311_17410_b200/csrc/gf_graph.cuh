@@ -50,6 +50,8 @@ struct gf_graph {
   gf::Slot* slots = nullptr;
   int64_t* sts = nullptr;
   int64_t* fts = nullptr;
+  int32_t* fts16 = nullptr;  // 32-bit fence every 16 slots (valid while ts32)
+  int ts32 = 1;              // every timestamp ingested so far fits in int32
   // persistent ingest scratch (sync-free path), sized for the largest batch seen
   void* ing_buf = nullptr;
   size_t ing_bytes = 0;
@@ -64,7 +66,8 @@ struct gf_graph {
 
 namespace gf {
 
-constexpr int FENCE = 32;  // pool slots per fence entry
+constexpr int FENCE = 32;    // pool slots per fence entry (int64 fence, general path)
+constexpr int FENCE16 = 16;  // pool slots per 32-bit fence entry: a 16-timestamp window is one 128 B line
 
 // NodeRec: one 128-byte line per node, everything a sampler query needs first
 // (one coalesced load): word 0 dir_off, 1 nslots (list end), 2 num_blocks |
@@ -115,16 +118,19 @@ struct GraphView {
   const Slot* slots;
   const int64_t* sts;
   const int64_t* fts;
+  const int32_t* fts16;
   const uint8_t* nflags;
   const int64_t* nrec;
   int64_t num_nodes;
   int any_deleted;
+  int ts32;
   SizingLaw law;
 };
 
 inline GraphView view_of(const gf_graph* g) {
-  return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off, g->dir, g->slots,
-                   g->sts,        g->fts,        g->nflags, g->nrec,      g->num_nodes, g->any_deleted,
+  return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off,   g->dir,
+                   g->slots,      g->sts,        g->fts,    g->fts16,     g->nflags,
+                   g->nrec,       g->num_nodes,  g->any_deleted, g->ts32,
                    sizing_law(g->sizing_kind, g->tau, g->sizing_param)};
 }
 

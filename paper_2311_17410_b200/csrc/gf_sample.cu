@@ -177,6 +177,35 @@ __device__ __forceinline__ void bracket_search(const int64_t* __restrict__ run, 
   }
 }
 
+// bracket_search over a sorted int32 run (the 32-bit fence): 8 entries per 256-bit chunk
+__device__ __forceinline__ int64_t pick32(int64_t w0, int64_t w1, int64_t w2, int64_t w3, int i) {
+  const int64_t w = (i & 4) ? ((i & 2) ? w3 : w2) : ((i & 2) ? w1 : w0);
+  return (int64_t)(int32_t)((i & 1) ? (uint64_t)w >> 32 : (uint64_t)w);
+}
+
+__device__ __forceinline__ void bracket_search32(const int32_t* __restrict__ run, int mis, int& lo, int& hi, int64_t& tl,
+                                                 int64_t& th, int64_t x) {
+  for (int step = 0; hi - lo > 1; step++) {
+    const int g0 = ((probe_rel(lo, hi, x, tl, th, step) + mis) & ~7) - mis;
+    int64_t w0, w1, w2, w3;
+    ld256(run + g0, w0, w1, w2, w3);
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const int idx = g0 + i;
+      k += (idx <= lo || (idx < hi && pick32(w0, w1, w2, w3, i) < x)) ? 1 : 0;
+    }
+    if (k > 0 && g0 + k - 1 > lo) {
+      lo = g0 + k - 1;
+      tl = pick32(w0, w1, w2, w3, k - 1);
+    }
+    if (k < 8 && g0 + k < hi) {
+      hi = g0 + k;
+      th = pick32(w0, w1, w2, w3, k);
+    }
+  }
+}
+
 // count of timestamps < x in sts[base, base + size) whose values lie in [t0, t1]
 __device__ __forceinline__ int64_t lane_block_lower_bound(const GraphView& GV, int64_t base, int64_t size, int64_t t0,
                                                           int64_t t1, int64_t x) {
@@ -185,7 +214,24 @@ __device__ __forceinline__ int64_t lane_block_lower_bound(const GraphView& GV, i
   int lo = -1, hi = (int)size;
   int64_t tl = t0 - 1, th = t1 + 1;
 #ifndef GF_NO_FENCE
-  if (size > FENCE) {
+  if (GV.ts32 && size > FENCE16) {
+    // 32-bit fences (fts16[f] = sts[16 f], every timestamp fits in int32): 8 per probe, and the
+    // 16-timestamp window they leave is one 128 B line
+    const int64_t f0 = (base + FENCE16 - 1) / FENCE16;
+    const int nf = (int)((base + size - 1) / FENCE16 - f0) + 1;
+    int flo = -1, fhi = nf;
+    int64_t ftl = tl, fth = th;
+    bracket_search32(GV.fts16 + f0, (int)(f0 & 7), flo, fhi, ftl, fth, x);
+    const int off = (int)(f0 * FENCE16 - base);
+    if (flo >= 0) {
+      lo = off + flo * FENCE16;
+      tl = ftl;
+    }
+    if (fhi < nf) {
+      hi = off + fhi * FENCE16;
+      th = fth;
+    }
+  } else if (size > FENCE) {
     // the fences f0..f1 (fts[f] = sts[f * FENCE], a 32x smaller array that stays in L2)
     // narrow the bracket to one 32-slot segment first
     const int64_t f0 = (base + FENCE - 1) / FENCE;

@@ -76,3 +76,32 @@ def test_negative_id_batch_leaves_graph_unchanged(cuda_device):
     out, _ = g.add_edges_arrays(np.array([1, 2]), np.array([0, 1]), np.array([200, 201]))
     np.testing.assert_array_equal(out.cpu().numpy(), o.add_edges(np.array([1, 2]), np.array([0, 1]),
                                                                  np.array([200, 201])))
+
+
+@pytest.mark.parametrize("offset", [0, 1 << 40])
+def test_window_search_with_and_without_32bit_fence(cuda_device, offset):
+    """Timestamps beyond int32 switch the sampler from the 32-bit fence to the int64 one; both match the oracle."""
+    import torch
+
+    import paper_2311_17410_b200 as gf
+    from oracle import OracleGraph
+
+    src, dst, ts = gf.generate_synthetic_arrays(200, 60_000, 2.2, 5_000, seed=11, src_skew=2.2)
+    ts = ts + offset
+    g = gf.DynamicGraph(directed=True, tau=256)
+    o = OracleGraph(True, 256)
+    for lo in range(0, len(src), 20_000):
+        sl = slice(lo, lo + 20_000)
+        g.add_edges_arrays(src[sl], dst[sl], ts[sl])
+        o.add_edges(src[sl], dst[sl], ts[sl])
+    rng = np.random.default_rng(5)
+    pick = rng.integers(0, len(src), 3000)
+    roots = np.concatenate([src[pick], dst[pick]])
+    rts = np.concatenate([ts[pick], ts[pick] + rng.integers(0, 3, 3000)])
+    for policy in ("recent", "uniform"):
+        got = gf.TemporalSampler(g, [10, 10], policy, seed=1).sample(torch.from_numpy(roots).cuda(),
+                                                                     torch.from_numpy(rts).cuda())
+        ref = o.sample_khop(roots, rts, [10, 10], policy, seed=1)
+        for lay, r in zip(got.layers, ref):
+            for a, w in zip((lay.offsets, lay.neighbors, lay.edge_ids, lay.timestamps), (r[2], r[3], r[4], r[5])):
+                np.testing.assert_array_equal(a.cpu().numpy(), w)
