@@ -1166,6 +1166,7 @@ void free_graph(gf_graph* g) {
   if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);
   if (g->ing_host) cudaFreeHost(g->ing_host);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+
 }
 
 }  // namespace

@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(THREADS) k_write_coop(GraphView GV, QueryIn Q,
 // latency-bound search of one tile overlaps the bandwidth-bound gather of
 // others on the same SM.
 
+// status word: flag (bits 63..62) | value; zeroed before each launch
 constexpr uint64_t TS_AGG = 1ull << 62, TS_INC = 2ull << 62, TS_VAL = (1ull << 62) - 1;
 
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
@@ -628,9 +629,11 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
 }
 
 struct TileCtl {
-  uint64_t* status;  // per tile: flag (bits 63..62) | value; zeroed before the launch
-  unsigned* ticket;  // zeroed before the launch
-  int64_t* total;    // layer total (written by the tile holding the last query)
+  uint64_t* status;             // per tile status word
+  unsigned long long* ticket;   // next tile
+  unsigned long long base;      // ticket value at this launch's start (0: zeroed with the status words)
+  uint64_t epoch;               // tag or'ed into every status word (0)
+  int64_t* total;               // layer total (written by the tile holding the last query)
 };
 
 // list position -> pool slot for a selected position (regular lists: closed form; else directory)
@@ -674,7 +677,7 @@ __device__ __forceinline__ void tile_publish(int k, int lane, int w, int32_t* s_
     wpre += (i < w) ? x : 0;
     agg += x;
   }
-  if (threadIdx.x == 0) st_relaxed(C.status + tile, (tile == 0 ? TS_INC : TS_AGG) | (uint64_t)agg);
+  if (threadIdx.x == 0) st_relaxed(C.status + tile, (tile == 0 ? TS_INC : TS_AGG) | C.epoch | (uint64_t)agg);
 }
 
 #ifndef GF_FUSED_THREADS
@@ -695,9 +698,10 @@ __global__ void __launch_bounds__(FT, GF_FUSED_MINB * 256 / FT) k_sample_fused(G
   __shared__ unsigned s_tile;
   __shared__ int64_t s_base;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(C.ticket, 1u);
+  if (threadIdx.x == 0) s_tile = (unsigned)(atomicAdd(C.ticket, 1ull) - C.base);
   __syncthreads();
   const int64_t tile = s_tile;
+  if (tile == 0 && threadIdx.x == 0) const_cast<int64_t*>(O.offsets)[0] = 0;
   const int64_t n = query_count(Q);
   if (tile * FT >= n) return;
   const int64_t q = tile * FT + threadIdx.x;
@@ -823,7 +827,7 @@ __global__ void __launch_bounds__(FT, GF_FUSED_MINB * 256 / FT) k_sample_fused(G
         const int64_t idx = end - lane;  // lane 0 = nearest predecessor
         uint64_t st;
         do {
-          st = idx >= 0 ? ld_relaxed(C.status + idx) : TS_INC;
+          st = idx >= 0 ? ld_relaxed(C.status + idx) : (TS_INC | C.epoch);
         } while (__any_sync(0xffffffffu, (st >> 62) == 0));
         const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
         const int first = inc ? __ffs(inc) - 1 : 31;
@@ -834,7 +838,7 @@ __global__ void __launch_bounds__(FT, GF_FUSED_MINB * 256 / FT) k_sample_fused(G
         if (inc) break;
         end -= 32;
       }
-      if (lane == 0) st_relaxed(C.status + tile, TS_INC | (uint64_t)(excl + agg));
+      if (lane == 0) st_relaxed(C.status + tile, TS_INC | C.epoch | (uint64_t)(excl + agg));
     }
     if (lane == 0) s_base = excl;
   }
@@ -1080,8 +1084,24 @@ bool fused_enabled() {
   return on;
 }
 
+// total must already be zero (callers clear their totals once per call): a layer with no
+// queries launches nothing that would write it.
 gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_offsets, const LayerOut& O, int64_t* total,
                        cudaStream_t s) {
+  GraphView GV = view_of(g);
+  const bool fast = !g->any_deleted;
+  if (fast && Q.fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled() && cap_q > 0) {
+    // per-call tile state (concurrent sampling of one graph on several streams stays safe);
+    // offsets[0] is written by tile 0, which always runs
+    const int64_t tiles = (cap_q + FT - 1) / FT;
+    Scratch sb(s);
+    GF_TRY(sb.alloc(sizeof(uint64_t) * (tiles + 1)));
+    TileCtl C{sb.as<uint64_t>(), reinterpret_cast<unsigned long long*>(sb.as<uint64_t>() + tiles), 0, 0, total};
+    GF_CUDA(cudaMemsetAsync(C.status, 0, sizeof(uint64_t) * (tiles + 1), s));
+    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, FT, 0, s, GV, Q, O, C);
+    else GF_LAUNCH(k_sample_fused<false>, tiles, FT, 0, s, GV, Q, O, C);
+    return GF_OK;
+  }
   GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
   if (cap_q == 0) {
     GF_CUDA(cudaMemsetAsync(total, 0, sizeof(int64_t), s));
@@ -1089,23 +1109,11 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   }
   Scratch sb(s);
   Arena A;
-  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + (size_t)cap_q / 4 + 8192));
+  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + 8192));
   A.base = sb.as<char>();
   QState S{A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q),
            A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q)};
   int64_t* counts = A.take<int64_t>(cap_q);
-  GraphView GV = view_of(g);
-  const bool fast = !g->any_deleted;
-  if (fast && Q.fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled()) {
-    const int64_t tiles = (cap_q + FT - 1) / FT;
-    TileCtl C{reinterpret_cast<uint64_t*>(A.take<int64_t>(tiles + 1)), nullptr, total};
-    C.ticket = reinterpret_cast<unsigned*>(C.status + tiles);
-    GF_CUDA(cudaMemsetAsync(C.status, 0, sizeof(uint64_t) * (tiles + 1), s));
-    GF_CUDA(cudaMemsetAsync(total, 0, sizeof(int64_t), s));
-    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, FT, 0, s, GV, Q, O, C);
-    else GF_LAUNCH(k_sample_fused<false>, tiles, FT, 0, s, GV, Q, O, C);
-    return GF_OK;
-  }
   if (fast) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
   else GF_LAUNCH(k_count_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, counts, cap_q);
   cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;

@@ -235,12 +235,12 @@ def sample_khop_device(graph: DynamicGraph, roots, tends, fanouts, policy: Sampl
     if max(caps) > (1 << 30):
         return _khop_layerwise(graph, roots, tends, fanouts, policy, seed, root_key_base, stream)
     dev = graph.device
-    offs = []
-    nbr = [torch.empty(max(c, 1), dtype=torch.int64, device=dev) for c in caps]
-    eid = [torch.empty(max(c, 1), dtype=torch.int64, device=dev) for c in caps]
-    tss = [torch.empty(max(c, 1), dtype=torch.int64, device=dev) for c in caps]
     nq = [int(roots.numel())] + caps[:-1]
-    offs = [torch.empty(q + 1, dtype=torch.int64, device=dev) for q in nq]
+    # one allocation for every output of the call, carved into disjoint views
+    sizes = [max(c, 1) for c in caps] * 3 + [q + 1 for q in nq]
+    flat = torch.empty(sum(sizes), dtype=torch.int64, device=dev)
+    parts = list(torch.split(flat, sizes))
+    nbr, eid, tss, offs = (parts[i * n_hops:(i + 1) * n_hops] for i in range(4))
     VP = ctypes.c_void_p * n_hops
     I64 = ctypes.c_int64 * n_hops
     totals = I64()
