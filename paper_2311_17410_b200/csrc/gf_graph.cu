@@ -94,7 +94,22 @@ __global__ void k_minmax(const int64_t* __restrict__ src, const int64_t* __restr
     tn = min(tn, __shfl_xor_sync(0xffffffffu, tn, o));
     tx = max(tx, __shfl_xor_sync(0xffffffffu, tx, o));
   }
+  __shared__ long long sm[4][32];
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   if ((threadIdx.x & 31) == 0) {
+    sm[0][w] = mn;
+    sm[1][w] = mx;
+    sm[2][w] = tn;
+    sm[3][w] = tx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one set of atomics per block
+    for (int i = 1; i < nw; i++) {
+      mn = min(mn, sm[0][i]);
+      mx = max(mx, sm[1][i]);
+      tn = min(tn, sm[2][i]);
+      tx = max(tx, sm[3][i]);
+    }
     atomicMin(&c->minv, mn);
     atomicMax(&c->maxv, mx);
     atomicMin(&c->tsmin, tn);
@@ -299,14 +314,6 @@ __global__ void k_totals(const longlong4* off4, int64_t E, IngestCounters* c) {
   c->dir_need = off4[E].z;
 }
 
-// sync-free path: totals + capacity check against the host-known pool state
-__global__ void k_totals_check(const longlong4* off4, int64_t E, const IngestScalars* S, IngestCounters* c) {
-  if (threadIdx.x || blockIdx.x || c->abort) return;
-  c->new_blocks = off4[E].x;
-  c->new_slots = off4[E].y;
-  c->dir_need = off4[E].z;
-  if (c->new_slots > S->slots_free || c->dir_need > S->dir_free) c->abort |= ABORT_CAP;
-}
 
 struct Recs {
   int64_t* first;   // segment-local accepted rank of the block's first event
@@ -397,64 +404,79 @@ struct DirArrays {
   int64_t* e;  // DIRW words per entry
 };
 
+// one warp per segment: lane 0 updates the node and its tail block; the lanes copy a regrown
+// directory and append the new blocks' entries together (hub directories can be thousands long)
 __global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                            SegPlan P, const longlong4* __restrict__ off4, int64_t dir_used,
                            Recs R, const uint32_t* __restrict__ ce_ev, const int64_t* __restrict__ ts, int directed,
                            NodeArrays N, BlockArrays B, DirArrays D, int kind, const IngestScalars* S) {
   if (c->abort) return;
   if (S) dir_used = S->dir_used;
-  int64_t nseg = c->num_segs;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
-    int64_t cnt = P.acc_cnt[s];
+  const int lane = threadIdx.x & 31;
+  const int64_t nseg = c->num_segs;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < nseg; s += nwarps) {
+    const int64_t cnt = P.acc_cnt[s];
     if (!cnt) continue;
-    int64_t v = keys[seg_start[s]];
-    int64_t t = N.tail[v], fill = P.fill[s], nb = P.nb_new[s], cs = P.cstart[s];
-    int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v];
-    // a block allocated while live degree != slots written (a deletion happened) or by
-    // batch sizing leaves the closed-form position -> block law (SizingLaw)
-    if (nb > 0 && (kind == GF_SIZING_BATCH || N.degree[v] != ns_old)) N.nflags[v] |= 1;
-    if (t != GF_NO_BLOCK && fill > 0) {
-      B.size[t] = P.tail_size[s] + fill;
-      B.tmax[t] = ts[ev_edge(ce_ev[cs + fill - 1], directed)];
+    const int64_t v = keys[seg_start[s]];
+    const int64_t t = N.tail[v], fill = P.fill[s], nb = P.nb_new[s], cs = P.cstart[s];
+    const int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v], deg_old = N.degree[v], oo = N.dir_off[v];
+    const int64_t dnew = P.plan4[s].z, r0 = off4[s].x;
+    const int64_t doff = dnew > 0 ? dir_used + off4[s].z : oo;
+    const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? ts[ev_edge(ce_ev[cs + fill - 1], directed)] : 0;
+    __syncwarp();
+    // block directory: grow (copy) if needed, then append the new blocks
+    if (nb > 0 && dnew > 0)
+      for (int64_t w = lane; w < nb_old * DIRW; w += 32) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
+    __syncwarp();
+    for (int64_t k = lane; k < nb; k += 32) {
+      const int64_t rec = r0 + k, h = R.handle[rec];
+      int64_t* e = D.e + (doff + nb_old + k) * DIRW;
+      e[0] = B.tmin[h];
+      e[1] = ns_old + R.first[rec];
+      e[2] = B.base[h];
+      e[3] = B.tmax[h];
     }
-    if (nb > 0) {
-      const int64_t r0 = off4[s].x;
-      int64_t h0 = R.handle[r0];
-      if (t == GF_NO_BLOCK) N.head[v] = h0;
-      else B.next[t] = h0;
-      N.tail[v] = R.handle[r0 + nb - 1];
-      // block directory: grow (copy) if needed, then append the new blocks
-      if (P.plan4[s].z > 0) {
-        int64_t no = dir_used + off4[s].z, oo = N.dir_off[v];
-        for (int64_t w = 0; w < nb_old * DIRW; w++) D.e[no * DIRW + w] = D.e[oo * DIRW + w];
-        N.dir_off[v] = no;
-        N.dir_cap[v] = P.plan4[s].z;
+    if (lane == 0) {
+      // a block allocated while live degree != slots written (a deletion happened) or by
+      // batch sizing leaves the closed-form position -> block law (SizingLaw)
+      if (nb > 0 && (kind == GF_SIZING_BATCH || deg_old != ns_old)) N.nflags[v] |= 1;
+      if (t != GF_NO_BLOCK && fill > 0) {
+        B.size[t] = P.tail_size[s] + fill;
+        B.tmax[t] = t_tmax;
+        D.e[(doff + nb_old - 1) * DIRW + 3] = t_tmax;  // old tail grew
       }
-      int64_t d0 = N.dir_off[v] + nb_old;
-      for (int64_t k = 0; k < nb; k++) {
-        int64_t rec = r0 + k, h = R.handle[rec];
-        int64_t* e = D.e + (d0 + k) * DIRW;
-        e[0] = B.tmin[h];
-        e[1] = ns_old + R.first[rec];
-        e[2] = B.base[h];
-        e[3] = B.tmax[h];
+      int64_t tl = t;
+      if (nb > 0) {
+        if (t == GF_NO_BLOCK) N.head[v] = R.handle[r0];
+        else B.next[t] = R.handle[r0];
+        tl = R.handle[r0 + nb - 1];
+        N.tail[v] = tl;
+        if (dnew > 0) {
+          N.dir_off[v] = doff;
+          N.dir_cap[v] = dnew;
+        }
       }
+      const int64_t nbt = nb_old + nb;
+      N.num_blocks[v] = nbt;
+      N.degree[v] = deg_old + cnt;
+      N.nslots[v] = ns_old + cnt;
     }
-    if (t != GF_NO_BLOCK && fill > 0) D.e[(N.dir_off[v] + nb_old - 1) * DIRW + 3] = B.tmax[t];  // old tail grew
-    N.num_blocks[v] = nb_old + nb;
-    N.degree[v] += cnt;
-    N.nslots[v] = ns_old + cnt;
-    int64_t tl = N.tail[v], doff = N.dir_off[v], nbt = nb_old + nb;
-    int64_t* r = N.nrec + v * NREC;
-    r[0] = doff;
-    r[1] = ns_old + cnt;
-    r[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
-    r[3] = D.e[doff * DIRW + 1];
-    r[4] = D.e[(doff + nbt - 1) * DIRW + 1];
-    r[5] = B.base[tl];
-    r[6] = B.tmin[tl];
-    r[7] = B.tmax[tl];
-    r[8] = D.e[doff * DIRW];
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t nbt = nb_old + nb, tl = N.tail[v];
+      int64_t* r = N.nrec + v * NREC;
+      r[0] = doff;
+      r[1] = ns_old + cnt;
+      r[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
+      r[3] = D.e[doff * DIRW + 1];
+      r[4] = D.e[(doff + nbt - 1) * DIRW + 1];
+      r[5] = B.base[tl];
+      r[6] = B.tmin[tl];
+      r[7] = B.tmax[tl];
+      r[8] = D.e[doff * DIRW];
+    }
   }
 }
 
@@ -744,7 +766,7 @@ gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, co
     NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid, g->nflags,
                  g->nrec};
     DirArrays D{g->dir};
-    GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, off4, g->dir_used, R, ce_ev, ts,
+    GF_LAUNCH(k_finalize, grid_for(32 * E, T, G), T, 0, s, dc, keys, seg_start, P, off4, g->dir_used, R, ce_ev, ts,
               dir, N, B, D, g->sizing_kind, nullptr);
     GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, off4, R, nullptr,
               g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts, g->fts16);
@@ -803,60 +825,412 @@ __global__ void k_grow_nodes(IngestCounters* c, const IngestScalars* S, int64_t 
   }
 }
 
-struct AddLL2 {
-  __device__ __forceinline__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
-    return make_longlong2(a.x + b.x, a.y + b.y);
-  }
+// Exclusive sum scan of K-wide int64 records (the 4-wide block plan and the 2-wide allocation
+// triggers) in one pass: ticketed tiles with decoupled look-back.  Tile state (flags, ticket) is
+// zeroed by k_stage_minmax at the start of the same launch sequence.
+#ifndef GF_SCAN_ITEMS
+#define GF_SCAN_ITEMS 4
+#endif
+constexpr int SCAN_T = 256, SCAN_ITEMS = GF_SCAN_ITEMS, SCAN_TILE = SCAN_T * SCAN_ITEMS;
+
+struct ScanState {
+  int64_t* agg;   // [tiles][K]
+  int64_t* inc;   // [tiles][K]
+  int* flag;      // [tiles]: 0 none, 1 aggregate, 2 inclusive
+  unsigned* ticket;
+  int64_t tiles;
 };
 
-// record r (segment-major enumeration): handle = blk_used + #allocations triggered by earlier
-// events, slot base = slots_used + their capacities; neighbours' handles are recomputed locally
-__global__ void k_write_blocks_scan(const IngestCounters* c, Recs R, const longlong2* __restrict__ tscan,
-                                    const IngestScalars* S, const longlong4* __restrict__ off4, SegPlan P,
-                                    const uint32_t* __restrict__ ce_ev, const uint32_t* __restrict__ keys,
-                                    const int64_t* __restrict__ seg_start, const int64_t* tail,
-                                    const int64_t* __restrict__ ts, int directed, BlockArrays B) {
+__device__ __forceinline__ int ld_flag(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_flag(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(SCAN_T) k_scan_sum(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
+                                                      ScanState S, const IngestCounters* c) {
+  __shared__ unsigned s_tile;
+  __shared__ int64_t s_w[SCAN_T / 32][K];
+  __shared__ int64_t s_base[K];
   if (c->abort) return;
-  const int64_t nrec = c->new_blocks, blk_used = S->blk_used, slots_used = S->slots_used;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
-    const longlong2 t = tscan[R.key[r]];
-    const int64_t h = blk_used + t.x;
-    R.handle[r] = h;
-    const int32_t s = R.seg[r];
-    const int64_t k = r - off4[s].x, nb = P.nb_new[s], cs = P.cstart[s];
-    const int64_t f = R.first[r], cnt = R.count[r];
-    B.cap[h] = R.cap[r];
-    B.size[h] = cnt;
-    B.tmin[h] = ts[ev_edge(ce_ev[cs + f], directed)];
-    B.tmax[h] = ts[ev_edge(ce_ev[cs + f + cnt - 1], directed)];
-    B.base[h] = slots_used + t.y;
-    const int64_t v = keys[seg_start[s]];
-    B.prev[h] = (k == 0) ? tail[v] : blk_used + tscan[R.key[r - 1]].x;
-    B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : blk_used + tscan[R.key[r + 1]].x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(S.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t i0 = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  int64_t v[SCAN_ITEMS][K], run[K];
+#pragma unroll
+  for (int f = 0; f < K; f++) run[f] = 0;
+#pragma unroll
+  for (int j = 0; j < SCAN_ITEMS; j++)
+#pragma unroll
+    for (int f = 0; f < K; f++) {
+      v[j][f] = run[f];  // exclusive within the thread
+      run[f] += (i0 + j < n) ? in[(i0 + j) * K + f] : 0;
+    }
+  // warp inclusive scan of the thread totals
+  int64_t inc_[K];
+#pragma unroll
+  for (int f = 0; f < K; f++) {
+    int64_t x = run[f];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    inc_[f] = x;
+    if (lane == 31) s_w[w][f] = x;
   }
+  __syncthreads();
+  int64_t wpre[K], agg[K];
+#pragma unroll
+  for (int f = 0; f < K; f++) {
+    wpre[f] = 0;
+    agg[f] = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_T / 32; i++) {
+      wpre[f] += (i < w) ? s_w[i][f] : 0;
+      agg[f] += s_w[i][f];
+    }
+  }
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int f = 0; f < K; f++) (tile == 0 ? S.inc : S.agg)[tile * K + f] = agg[f];
+    __threadfence();
+    st_flag(S.flag + tile, tile == 0 ? 2 : 1);
+  }
+  if (w == 0) {
+    int64_t base[K];
+#pragma unroll
+    for (int f = 0; f < K; f++) base[f] = 0;
+    if (tile > 0) {
+      int64_t end = tile - 1;
+      while (true) {
+        const int64_t idx = end - lane;
+        int fl = 2;
+        if (idx >= 0) {
+          do {
+            fl = ld_flag(S.flag + idx);
+          } while (fl == 0);
+        }
+        __syncwarp();
+        __threadfence();
+        const unsigned incm = __ballot_sync(0xffffffffu, fl == 2);  // lanes before tile 0 count as inclusive 0
+        const int first = incm ? __ffs(incm) - 1 : 31;
+        const bool take = lane <= first && idx >= 0;
+#pragma unroll
+        for (int f = 0; f < K; f++) {
+          int64_t x = take ? __ldcg((fl == 2 ? S.inc : S.agg) + idx * K + f) : 0;  // L2: never a stale L1 line
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          base[f] += x;
+        }
+        if (incm) break;
+        end -= 32;
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int f = 0; f < K; f++) S.inc[tile * K + f] = base[f] + agg[f];
+        __threadfence();
+        st_flag(S.flag + tile, 2);
+      }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int f = 0; f < K; f++) s_base[f] = base[f];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < SCAN_ITEMS; j++)
+    if (i0 + j < n)
+#pragma unroll
+      for (int f = 0; f < K; f++) out[(i0 + j) * K + f] = s_base[f] + wpre[f] + inc_[f] - run[f] + v[j][f];
 }
 
-// batch inputs -> fixed staging buffers (the captured sequence always reads the same addresses)
-__global__ void k_stage(const IngestScalars* S, int64_t n, int64_t* src, int64_t* dst, int64_t* ts, int64_t* eids,
-                        IngestCounters* c) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c->minv = LLONG_MAX;
-    c->maxv = LLONG_MIN;
-    c->viol = c->num_segs = c->n_acc = c->new_blocks = c->new_slots = c->dir_need = 0;
-    c->max_eid = LLONG_MIN;
-    c->abort = 0;
-    c->tsmin = LLONG_MAX;
-    c->tsmax = LLONG_MIN;
-  }
+// ---- fused kernels of the sync-free path -------------------------------------
+// staging + batch min/max (the counters were initialised by the H2D copy that starts the sequence)
+__global__ void k_stage_minmax(const IngestScalars* S, int64_t n, int64_t* src, int64_t* dst, int64_t* ts, int64_t* eids,
+                               IngestCounters* c, int* zero, int64_t nzero) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nzero; j += (int64_t)gridDim.x * blockDim.x)
+    zero[j] = 0;  // look-back scan flags and tickets of this launch sequence
   const bool has_eids = S->eids_in != nullptr;
+  long long mn = LLONG_MAX, mx = LLONG_MIN, tn = LLONG_MAX, tx = LLONG_MIN;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    src[j] = S->src[j];
-    dst[j] = S->dst[j];
-    ts[j] = S->ts[j];
+    const long long a = S->src[j], b = S->dst[j], t = S->ts[j];
+    src[j] = a;
+    dst[j] = b;
+    ts[j] = t;
     if (has_eids) eids[j] = S->eids_in[j];
+    mn = min(mn, min(a, b));
+    mx = max(mx, max(a, b));
+    tn = min(tn, t);
+    tx = max(tx, t);
+  }
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    tn = min(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+    tx = max(tx, __shfl_xor_sync(0xffffffffu, tx, o));
+  }
+  __shared__ long long sm[4][32];
+  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sm[0][w] = mn;
+    sm[1][w] = mx;
+    sm[2][w] = tn;
+    sm[3][w] = tx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < nw; i++) {
+      mn = min(mn, sm[0][i]);
+      mx = max(mx, sm[1][i]);
+      tn = min(tn, sm[2][i]);
+      tx = max(tx, sm[3][i]);
+    }
+    if (mn != LLONG_MAX) {
+      atomicMin(&c->minv, mn);
+      atomicMax(&c->maxv, mx);
+      atomicMin(&c->tsmin, tn);
+      atomicMax(&c->tsmax, tx);
+    }
   }
 }
 
+// chronology: accept all; only when some endpoint may see a decreasing timestamp, block 0 prepares
+// the per-node latest timestamps and resolves the batch serially (storage.py:426-437)
+__global__ void k_accept(uint8_t* acc, int64_t n, int64_t* tm, const int64_t* tail, const int64_t* bsize,
+                         const int64_t* btmax, const IngestCounters* c, const IngestScalars* S, const int64_t* src,
+                         const int64_t* dst, const int64_t* ts, int directed) {
+  if (c->abort) return;
+  if (!c->viol) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
+    return;
+  }
+  if (blockIdx.x != 0) return;
+  const int64_t nn = max((int64_t)S->num_nodes, (int64_t)c->maxv + 1);
+  for (int64_t v = threadIdx.x; v < nn; v += blockDim.x) tm[v] = node_tmax(tail, bsize, btmax, v);
+  __syncthreads();
+  if (threadIdx.x) return;
+  for (int64_t j = 0; j < n; j++) {
+    const int64_t a = src[j], d = dst[j], t = ts[j];
+    const bool ok = t >= tm[a] && (directed || t >= tm[d]);
+    acc[j] = ok;
+    if (ok) {
+      tm[a] = t;
+      if (!directed) tm[d] = t;
+    }
+  }
+}
+
+// edge ids (storage.py:438-442) and per-event keep flags in one pass
+__global__ void k_eids_keep(const uint8_t* __restrict__ acc, const int64_t* __restrict__ rank, int64_t n,
+                            const int64_t* __restrict__ eids_in, int64_t* out_eids, IngestCounters* c, const IngestScalars* S,
+                            const uint32_t* __restrict__ vals, int64_t E, int directed, int64_t* keep) {
+  if (c->abort) return;
+  const int64_t next_id = S->next_edge_id;
+  long long mx = LLONG_MIN;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = -1;
+    if (acc[j]) {
+      e = eids_in ? eids_in[j] : next_id + rank[j];
+      mx = max(mx, (long long)e);
+    }
+    out_eids[j] = e;
+    S->out_eids[j] = e;
+    if (j == n - 1) c->n_acc = rank[j] + acc[j];
+  }
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx != LLONG_MIN) atomicMax(&c->max_eid, mx);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x)
+    keep[i] = acc[ev_edge(vals[i], directed)];
+  if (blockIdx.x == 0 && threadIdx.x == 0) keep[E] = 0;
+}
+
+// pool-capacity check (block 0) + enumeration of the new blocks
+__global__ void k_check_enumerate(const longlong4* __restrict__ off4, int64_t E, const IngestScalars* S, IngestCounters* c,
+                                  const int64_t* __restrict__ ce_pend, const uint32_t* __restrict__ ce_ev, SegPlan P,
+                                  const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
+                                  const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R, longlong2* trig) {
+  if (c->abort) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c->new_blocks = off4[E].x;
+    c->new_slots = off4[E].y;
+    c->dir_need = off4[E].z;
+    if (c->new_slots > S->slots_free || c->dir_need > S->dir_free) c->abort |= ABORT_CAP;  // nothing written yet
+  }
+  const int64_t nseg = c->num_segs;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nb = P.nb_new[s];
+    if (!nb) continue;
+    const int64_t v = keys[seg_start[s]];
+    const int64_t cs = P.cstart[s], cnt = P.acc_cnt[s], fill = P.fill[s];
+    int64_t deg = degree[v] + fill, used = fill, rem = cnt - fill;
+    int64_t r = off4[s].x;
+    while (rem > 0) {
+      const int64_t cap = sizing_cap(kind, tau, param, deg, ce_pend[cs + used]);
+      const int64_t take = min(cap, rem);
+      R.first[r] = used;
+      R.count[r] = take;
+      R.cap[r] = cap;
+      R.seg[r] = (int32_t)s;
+      R.key[r] = ce_ev[cs + used];
+      trig[ce_ev[cs + used]] = make_longlong2(1, cap);  // allocation order = triggering event order
+      r++;
+      deg += take;
+      used += take;
+      rem -= take;
+    }
+  }
+}
+
+// The commit: one warp per segment writes its new blocks (handle and slot base from the trigger
+// scan), the directory, the node and its NodeRec; one thread per accepted event writes its slot.
+// The capacity check ran in an earlier kernel, so a set abort flag is seen here.
+__global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const uint32_t* __restrict__ keys,
+                         const int64_t* __restrict__ seg_start, SegPlan P, const longlong4* __restrict__ off4, Recs R,
+                         const longlong2* __restrict__ tscan, const uint32_t* __restrict__ ce_ev,
+                         const int32_t* __restrict__ ce_seg, const int64_t* __restrict__ src,
+                         const int64_t* __restrict__ dst, const int64_t* __restrict__ ts, const int64_t* __restrict__ eids,
+                         int directed, const int64_t* __restrict__ old_tail, NodeArrays N, BlockArrays B, DirArrays D,
+                         int kind, Slot* slots, int64_t* sts, int64_t* fts, int32_t* fts16) {
+  if (c->abort) return;
+  const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used;
+  const int lane = threadIdx.x & 31;
+  const int64_t nseg = c->num_segs;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < nseg; s += nwarps) {
+    const int64_t cnt = P.acc_cnt[s];
+    if (!cnt) continue;
+    const int64_t v = keys[seg_start[s]];
+    const int64_t t = old_tail[s], fill = P.fill[s], nb = P.nb_new[s], cs = P.cstart[s];
+    const int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v], deg_old = N.degree[v], oo = N.dir_off[v];
+    const int64_t dnew = P.plan4[s].z, r0 = off4[s].x;
+    const int64_t doff = dnew > 0 ? dir_used + off4[s].z : oo;
+    const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? ts[ev_edge(ce_ev[cs + fill - 1], directed)] : 0;
+    __syncwarp();
+    if (nb > 0 && dnew > 0)
+      for (int64_t w = lane; w < nb_old * DIRW; w += 32) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
+    __syncwarp();
+    int64_t h_last = GF_NO_BLOCK, tmin_last = 0, tmax_last = 0, base_last = 0;
+    for (int64_t k = lane; k < nb; k += 32) {
+      const int64_t r = r0 + k;
+      const longlong2 tr = tscan[R.key[r]];
+      const int64_t h = blk_used + tr.x, base = slots_used + tr.y;
+      const int64_t f = R.first[r], n_in = R.count[r];
+      const int64_t tmin = ts[ev_edge(ce_ev[cs + f], directed)];
+      const int64_t tmax = ts[ev_edge(ce_ev[cs + f + n_in - 1], directed)];
+      B.cap[h] = R.cap[r];
+      B.size[h] = n_in;
+      B.tmin[h] = tmin;
+      B.tmax[h] = tmax;
+      B.base[h] = base;
+      B.prev[h] = (k == 0) ? t : blk_used + tscan[R.key[r - 1]].x;
+      B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : blk_used + tscan[R.key[r + 1]].x;
+      int64_t* e = D.e + (doff + nb_old + k) * DIRW;
+      e[0] = tmin;
+      e[1] = ns_old + f;
+      e[2] = base;
+      e[3] = tmax;
+      if (k == nb - 1) {
+        h_last = h;
+        tmin_last = tmin;
+        tmax_last = tmax;
+        base_last = base;
+      }
+    }
+    // the lane that wrote the last new block hands its record to lane 0
+    const unsigned who = __ballot_sync(0xffffffffu, h_last != GF_NO_BLOCK);
+    const int src_lane = who ? __ffs(who) - 1 : 0;
+    h_last = __shfl_sync(0xffffffffu, h_last, src_lane);
+    tmin_last = __shfl_sync(0xffffffffu, tmin_last, src_lane);
+    tmax_last = __shfl_sync(0xffffffffu, tmax_last, src_lane);
+    base_last = __shfl_sync(0xffffffffu, base_last, src_lane);
+    const int64_t h_first = nb > 0 ? blk_used + tscan[R.key[r0]].x : GF_NO_BLOCK;
+    __syncwarp();
+    if (lane == 0) {
+      // a block allocated while live degree != slots written (a deletion happened) or by
+      // batch sizing leaves the closed-form position -> block law (SizingLaw)
+      if (nb > 0 && (kind == GF_SIZING_BATCH || deg_old != ns_old)) N.nflags[v] |= 1;
+      int64_t tl = t, tl_tmin = 0, tl_tmax = 0, tl_base = 0;
+      if (t != GF_NO_BLOCK) {
+        tl_tmin = B.tmin[t];
+        tl_base = B.base[t];
+        tl_tmax = fill > 0 ? t_tmax : B.tmax[t];
+      }
+      if (t != GF_NO_BLOCK && fill > 0) {
+        B.size[t] = P.tail_size[s] + fill;
+        B.tmax[t] = t_tmax;
+        D.e[(doff + nb_old - 1) * DIRW + 3] = t_tmax;  // old tail grew
+      }
+      if (nb > 0) {
+        if (t == GF_NO_BLOCK) N.head[v] = h_first;
+        else B.next[t] = h_first;
+        tl = h_last;
+        tl_tmin = tmin_last;
+        tl_tmax = tmax_last;
+        tl_base = base_last;
+        N.tail[v] = tl;
+        if (dnew > 0) {
+          N.dir_off[v] = doff;
+          N.dir_cap[v] = dnew;
+        }
+      }
+      const int64_t nbt = nb_old + nb;
+      N.num_blocks[v] = nbt;
+      N.degree[v] = deg_old + cnt;
+      N.nslots[v] = ns_old + cnt;
+      int64_t* rr = N.nrec + v * NREC;
+      rr[0] = doff;
+      rr[1] = ns_old + cnt;
+      rr[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
+      rr[3] = D.e[doff * DIRW + 1];
+      rr[4] = D.e[(doff + nbt - 1) * DIRW + 1];
+      rr[5] = tl_base;
+      rr[6] = tl_tmin;
+      rr[7] = tl_tmax;
+      rr[8] = D.e[doff * DIRW];
+    }
+  }
+  // slots: one thread per accepted event
+  const int64_t nacc_ev = P.cstart[nseg - 1] + P.acc_cnt[nseg - 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nacc_ev; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t sg = ce_seg[i];
+    const int64_t r = i - P.cstart[sg];
+    const uint32_t ev = ce_ev[i];
+    const int64_t j = ev_edge(ev, directed);
+    const int side = directed ? 0 : (int)(ev & 1);
+    const int64_t fill = P.fill[sg];
+    int64_t pos;
+    if (r < fill) {
+      pos = B.base[old_tail[sg]] + P.tail_size[sg] + r;  // the old tail's base does not change
+    } else {
+      int64_t lo = off4[sg].x, hi = lo + P.nb_new[sg];  // last rec with first <= r
+      while (hi - lo > 1) {
+        const int64_t m = (lo + hi) >> 1;
+        if (R.first[m] <= r) lo = m;
+        else hi = m;
+      }
+      pos = slots_used + tscan[R.key[lo]].y + (r - R.first[lo]);
+    }
+    Slot sl;
+    sl.ts = ts[j];
+    sl.eid = eids[j];
+    sl.nbr = (int32_t)(side ? src[j] : dst[j]);
+    sl.owner = (int32_t)keys[seg_start[sg]];
+    sl.valid = 1;
+    sl.pad = 0;
+    slots[pos] = sl;
+    sts[pos] = sl.ts;
+    if ((pos & (FENCE - 1)) == 0) fts[pos / FENCE] = sl.ts;
+    if ((pos & (FENCE16 - 1)) == 0) fts16[pos / FENCE16] = (int32_t)max(min(sl.ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);
+  }
+}
 
 // node capacity only (rows are initialised on the device by k_grow_nodes)
 gf_status grow_node_cap(gf_graph* g, int64_t need, cudaStream_t s) {
@@ -889,7 +1263,11 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
   if (g->node_cap == 0) GF_TRY(grow_node_cap(g, 1024, s));
   if (!g->ing_host) GF_CUDA(cudaMallocHost(&g->ing_host, 4096));
   IngestScalars* hs = (IngestScalars*)g->ing_host;
-  IngestCounters* hcp = (IngestCounters*)((char*)g->ing_host + 2048);
+  IngestCounters* hci = (IngestCounters*)((char*)g->ing_host + 1024);  // initial counter values
+  IngestCounters* hcp = (IngestCounters*)((char*)g->ing_host + 2048);  // counters read back
+  memset(hci, 0, sizeof(IngestCounters));
+  hci->minv = hci->tsmin = LLONG_MAX;
+  hci->maxv = hci->tsmax = hci->max_eid = LLONG_MIN;
   static const bool no_graph = getenv("GF_INGEST_NO_GRAPH") != nullptr;
   const int T = 256;
   const int64_t G = 8 * num_sms();
@@ -899,6 +1277,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     const int64_t node_cap = g->node_cap;
     const int endbit = bits_for(node_cap);
     size_t cub_bytes = 0;
+    const int64_t tiles4 = (E + 1 + SCAN_TILE - 1) / SCAN_TILE, tiles2 = (E + SCAN_TILE - 1) / SCAN_TILE;
     {
       size_t b = 0;
       GF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
@@ -910,12 +1289,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       cub_bytes = std::max(cub_bytes, b);
       GF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, (int)(E + 1), s));
       cub_bytes = std::max(cub_bytes, b);
-      GF_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, b, (longlong2*)nullptr, (longlong2*)nullptr, AddLL2(),
-                                             make_longlong2(0, 0), (int)E, s));
-      cub_bytes = std::max(cub_bytes, b);
-      GF_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, b, (longlong4*)nullptr, (longlong4*)nullptr, AddLL4(),
-                                             make_longlong4(0, 0, 0, 0), (int)(E + 1), s));
-      cub_bytes = std::max(cub_bytes, b);
+
     }
     // scratch layout (one persistent buffer per graph)
     auto layout = [&](Arena& a, void** p) {
@@ -936,6 +1310,9 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       p[i++] = a.take<int64_t>(E + 1);  // R.handle
       p[i++] = a.take<longlong2>(E); p[i++] = a.take<longlong2>(E);      // trig, tscan
       p[i++] = a.take<char>((int64_t)cub_bytes);
+      p[i++] = a.take<int64_t>(tiles4 * 4); p[i++] = a.take<int64_t>(tiles4 * 4);  // plan scan agg/inc
+      p[i++] = a.take<int64_t>(tiles2 * 2); p[i++] = a.take<int64_t>(tiles2 * 2);  // trigger scan agg/inc
+      p[i++] = a.take<int>(2 + tiles4 + tiles2);                                  // tickets + flags (zeroed)
       return i;
     };
     void* P_[64];
@@ -996,6 +1373,15 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     longlong2* trig = (longlong2*)P_[i++];
     longlong2* tscan = (longlong2*)P_[i++];
     void* cubtmp = P_[i++];
+    ScanState S4{(int64_t*)P_[i], (int64_t*)P_[i + 1], nullptr, nullptr, tiles4};
+    ScanState S2{(int64_t*)P_[i + 2], (int64_t*)P_[i + 3], nullptr, nullptr, tiles2};
+    int* zero = (int*)P_[i + 4];
+    i += 5;
+    S4.ticket = (unsigned*)zero;
+    S2.ticket = (unsigned*)zero + 1;
+    S4.flag = zero + 2;
+    S2.flag = zero + 2 + tiles4;
+    const int64_t nzero = 2 + tiles4 + tiles2;
 
     // per-call values: read on the device through ds
     *hs = IngestScalars{src_in, dst_in, ts_in, eids_user, out_user, g->num_nodes, g->blk_used, g->slots_used,
@@ -1005,8 +1391,8 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     auto enqueue = [&](cudaStream_t s) -> gf_status {
       size_t tb = cub_bytes;
       GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
-      GF_LAUNCH(k_stage, grid_for(n, T, G), T, 0, s, ds, n, src, dst, ts, eids_st, dc);
-      GF_LAUNCH(k_minmax, grid_for(n, T, 2 * num_sms()), T, 0, s, src, dst, ts, n, dc);
+      GF_CUDA(cudaMemcpyAsync(dc, hci, sizeof(IngestCounters), cudaMemcpyHostToDevice, s));
+      GF_LAUNCH(k_stage_minmax, grid_for(std::max(n, nzero), T, G), T, 0, s, ds, n, src, dst, ts, eids_st, dc, zero, nzero);
       GF_LAUNCH(k_grow_nodes, grid_for(2 * n, T, G), T, 0, s, dc, ds, node_cap, g->head, g->tail, g->num_blocks,
                 g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
       GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc, trig);
@@ -1016,36 +1402,26 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_CUDA(cub::DeviceScan::InclusiveSum(cubtmp, tb, heads, incl, (int)E, s));
       GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
                 seg_start, dc);
-      GF_LAUNCH(k_accept_prep, grid_for(std::max(n, node_cap), T, G), T, 0, s, acc, n, tm, 0, g->tail, g->bsize,
-                g->btmax, dc, ds);
-      GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
+      GF_LAUNCH(k_accept, grid_for(n, T, G), T, 0, s, acc, n, tm, g->tail, g->bsize, g->btmax, dc, ds, src, dst, ts, dir);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, acc, rank, (int)n, s));
-      GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, 0, eids_in, out_eids, dc, ds);
-      GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
+      GF_LAUNCH(k_eids_keep, grid_for(std::max(n, E), T, G), T, 0, s, acc, rank, n, eids_in, out_eids, dc, ds, vals, E,
+                dir, keep);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, cpos, (int)(E + 1), s));
       GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
       GF_LAUNCH(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize,
                 g->bcap, g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, old_tail);
-      tb = cub_bytes;
-      GF_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, tb, P.plan4, off4, AddLL4(), make_longlong4(0, 0, 0, 0), (int)(E + 1),
-                                             s));
-      GF_LAUNCH(k_totals_check, 1, 1, 0, s, off4, E, ds, dc);
-      GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, off4, nullptr, P, keys, seg_start,
+      GF_LAUNCH(k_scan_sum<4>, tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc);
+      GF_LAUNCH(k_check_enumerate, grid_for(E, T, G), T, 0, s, off4, E, ds, dc, ce_pend, ce_ev, P, keys, seg_start,
                 g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
-      tb = cub_bytes;
-      GF_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, tb, trig, tscan, AddLL2(), make_longlong2(0, 0), (int)E, s));
-      BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
-      GF_LAUNCH(k_write_blocks_scan, grid_for(E, T, G), T, 0, s, dc, R, tscan, ds, off4, P, ce_ev, keys, seg_start,
-                g->tail, ts, dir, B);
+      GF_LAUNCH(k_scan_sum<2>, tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc);
       NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
                    g->nflags, g->nrec};
+      BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
       DirArrays D{g->dir};
-      GF_LAUNCH(k_finalize, grid_for(E, T, G), T, 0, s, dc, keys, seg_start, P, off4, 0, R, ce_ev, ts, dir, N, B, D,
-                g->sizing_kind, ds);
-      GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, off4, R, nullptr,
-                g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts, g->fts16);
+      GF_LAUNCH(k_commit, grid_for(32 * E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, ce_seg, src,
+                dst, ts, out_eids, dir, old_tail, N, B, D, g->sizing_kind, g->slots, g->sts, g->fts, g->fts16);
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
     };

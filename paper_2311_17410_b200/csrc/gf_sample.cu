@@ -688,7 +688,11 @@ constexpr int FT = GF_FUSED_THREADS;  // queries per tile = threads per CTA
 // EARLY: publish the tile aggregate before the in-block window search when every count is
 // already known (recent policy: long lists give k = fanout once the boundary block is found)
 template <bool EARLY>
-__global__ void __launch_bounds__(FT, GF_FUSED_MINB * 256 / FT) k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
+#ifndef GF_FUSED_MINB_RECENT
+#define GF_FUSED_MINB_RECENT GF_FUSED_MINB
+#endif
+__global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_MINB) * 256 / FT)
+    k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
   constexpr int NW = FT / 32;
   __shared__ uint32_t s_sel[NW][32][KMAX];
   __shared__ uint8_t s_owner[NW][32 * KMAX];

@@ -99,7 +99,7 @@ def test_layer_bitwise_vs_oracle(cuda_device, policy, deletions):
         t0 = np.where(rng.random(nq) < 0.5, TS_MIN, t1 - rng.integers(0, int(ts[-1]) + 1, nq))
         delta = max(1, int(ts[-1]) // 5)
         pol = gf.SamplingPolicy(policy, delta if policy == "time_window" else 0)
-        for f in (1, 5, 10, 32, 40):
+        for f in (1, 5, 10, 15, 16, 17, 32, 40):  # fused path up to 16, unfused above
             lay = gf.sample_layer(g, q, t0, t1, f, pol, seed=1234 + f)
             want = o.sample_layer(q, t0, t1, f, policy, delta, seed=1234 + f)
             for nm, w in zip(("offsets", "neighbors", "edge_ids", "timestamps"), want):
