@@ -629,10 +629,8 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
 }
 
 struct TileCtl {
-  uint64_t* status;             // per tile status word
-  unsigned long long* ticket;   // next tile
-  unsigned long long base;      // ticket value at this launch's start (0: zeroed with the status words)
-  uint64_t epoch;               // tag or'ed into every status word (0)
+  uint64_t* status;             // per tile status word (zeroed before the launch)
+  unsigned long long* ticket;   // next tile (zeroed with the status words)
   int64_t* total;               // layer total (written by the tile holding the last query)
 };
 
@@ -677,7 +675,7 @@ __device__ __forceinline__ void tile_publish(int k, int lane, int w, int32_t* s_
     wpre += (i < w) ? x : 0;
     agg += x;
   }
-  if (threadIdx.x == 0) st_relaxed(C.status + tile, (tile == 0 ? TS_INC : TS_AGG) | C.epoch | (uint64_t)agg);
+  if (threadIdx.x == 0) st_relaxed(C.status + tile, (tile == 0 ? TS_INC : TS_AGG) | (uint64_t)agg);
 }
 
 #ifndef GF_FUSED_THREADS
@@ -702,7 +700,7 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
   __shared__ unsigned s_tile;
   __shared__ int64_t s_base;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = (unsigned)(atomicAdd(C.ticket, 1ull) - C.base);
+  if (threadIdx.x == 0) s_tile = (unsigned)atomicAdd(C.ticket, 1ull);
   __syncthreads();
   const int64_t tile = s_tile;
   if (tile == 0 && threadIdx.x == 0) const_cast<int64_t*>(O.offsets)[0] = 0;
@@ -831,7 +829,7 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
         const int64_t idx = end - lane;  // lane 0 = nearest predecessor
         uint64_t st;
         do {
-          st = idx >= 0 ? ld_relaxed(C.status + idx) : (TS_INC | C.epoch);
+          st = idx >= 0 ? ld_relaxed(C.status + idx) : TS_INC;
         } while (__any_sync(0xffffffffu, (st >> 62) == 0));
         const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
         const int first = inc ? __ffs(inc) - 1 : 31;
@@ -842,7 +840,7 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
         if (inc) break;
         end -= 32;
       }
-      if (lane == 0) st_relaxed(C.status + tile, TS_INC | C.epoch | (uint64_t)(excl + agg));
+      if (lane == 0) st_relaxed(C.status + tile, TS_INC | (uint64_t)(excl + agg));
     }
     if (lane == 0) s_base = excl;
   }
@@ -1100,7 +1098,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
     const int64_t tiles = (cap_q + FT - 1) / FT;
     Scratch sb(s);
     GF_TRY(sb.alloc(sizeof(uint64_t) * (tiles + 1)));
-    TileCtl C{sb.as<uint64_t>(), reinterpret_cast<unsigned long long*>(sb.as<uint64_t>() + tiles), 0, 0, total};
+    TileCtl C{sb.as<uint64_t>(), reinterpret_cast<unsigned long long*>(sb.as<uint64_t>() + tiles), total};
     GF_CUDA(cudaMemsetAsync(C.status, 0, sizeof(uint64_t) * (tiles + 1), s));
     if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, FT, 0, s, GV, Q, O, C);
     else GF_LAUNCH(k_sample_fused<false>, tiles, FT, 0, s, GV, Q, O, C);
