@@ -441,6 +441,8 @@ def bench_ours(args, cfg, world, rank, local):
               "roots": "R/2 uniformly drawn edges (seed 1+rank), src+dst at own ts (SURVEY.md 8(d)(ii))"}
     del rroots, rrts
 
+    fetch = fetch_bench(g, src, dst, ts, cfg, device) if (args.config == "gdelt" and not args.no_fetch) else None
+
     ingest_eps = cfg["edges"] / (max_over_ranks(ingest_ms, world) / 1e3)
     info = g.info()
     cpu = None
@@ -480,6 +482,7 @@ def bench_ours(args, cfg, world, rank, local):
                          "pipeline_frac": round(pipe_gbs / pk["hbm_gbs"], 4) if pipe_gbs else None},
             "kernels": kernels,
             "per_policy": per_policy,
+            "fetch": fetch,
             "replay": replay,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -487,6 +490,80 @@ def bench_ours(args, cfg, world, rank, local):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+
+
+# GDELT feature dims and cache sizes (3% of nodes / 3 per mille of edges)
+FETCH_DV, FETCH_DE = 413, 186
+FETCH_MINIBATCH = 4000      # TGN minibatch edges -> 8,000 roots (harness.py:424-429)
+FETCH_EDGE_TABLE = 5_000_000  # edge features held for the latest 5M edges (142 GB for all 191M)
+
+
+def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 20) -> dict:
+    """Feature-cache fetch block (harness.py:432-446) on GPU: per minibatch of the latest edges,
+    2-hop recent f10 sample, then node keys = roots + last-layer neighbours through an LRU node cache
+    (d_v 413) and edge keys = every layer's edge ids through an LRU edge cache (d_e 186); misses
+    are filled from the device feature tables and inserted.  Unit: one fetched row
+    (8 B key + 1 B mask + 8*d B read+write)."""
+    import torch
+
+    import paper_2311_17410_b200 as gf
+    from paper_2311_17410_b200 import _lib
+
+    nodes = cfg["nodes"]
+    gen = torch.Generator(device=device)
+    gen.manual_seed(7)
+    ntab = gf.NodeFeatureTable(FETCH_DV, device=device)
+    ntab.set_many(torch.arange(nodes, device=device), torch.rand(nodes, FETCH_DV, device=device, generator=gen))
+    e_total = src.numel()
+    e0 = e_total - FETCH_EDGE_TABLE
+    etab = gf.EdgeFeatureTable(FETCH_DE, device=device)
+    etab.append(torch.arange(e0, e_total, device=device),
+                torch.rand(FETCH_EDGE_TABLE, FETCH_DE, device=device, generator=gen))
+    ncache = gf.VectorCache("lru", max(1, int(0.03 * nodes)), FETCH_DV, 0.2, device=device)
+    ecache = gf.VectorCache("lru", max(1, int(0.003 * e_total)), FETCH_DE, 0.2, device=device)
+    mb = []
+    for b in range(batches + 2):  # minibatches walking back from the newest edges
+        hi = e_total - b * FETCH_MINIBATCH
+        lo = hi - FETCH_MINIBATCH
+        roots = torch.cat([src[lo:hi], dst[lo:hi]]).contiguous()
+        rts = torch.cat([ts[lo:hi], ts[lo:hi]]).contiguous()
+        smp = gf.sample_khop_device(g, roots, rts, FANOUTS, gf.SamplingPolicy("recent"), seed=0)
+        nkeys = torch.cat([roots, smp.layers[-1].neighbors]).contiguous()
+        ekeys = torch.cat([lay.edge_ids for lay in smp.layers]).contiguous()
+        mb.append((nkeys, ekeys))
+    for nk, ek in mb[:2]:  # warm-up
+        gf.fetch_features(ncache, ntab, nk)
+        gf.fetch_features(ecache, etab, ek)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rows = byts = 0
+    a.record()
+    for nk, ek in mb[2:]:
+        gf.fetch_features(ncache, ntab, nk)
+        gf.fetch_features(ecache, etab, ek)
+        rows += nk.numel() + ek.numel()
+        byts += nk.numel() * (9 + 8 * FETCH_DV) + ek.numel() * (9 + 8 * FETCH_DE)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    _lib.profile_enable(True)
+    for nk, ek in mb[2:6]:
+        gf.fetch_features(ncache, ntab, nk)
+        gf.fetch_features(ecache, etab, ek)
+    prof = _lib.profile_summary()
+    _lib.profile_enable(False)
+    tot = sum(v[1] for v in prof.values())
+    gat = sum(v[1] for k, v in prof.items() if k.startswith(("k_gather_rows", "k_fetch_gather", "k_fill_from_table",
+                                                                  "k_copy_rows")))
+    pk = peaks()
+    gbs = byts / (ms / 1e3) / 1e9
+    return {"value": round(rows / (ms / 1e3), 1), "unit": "fetched rows/s", "ms_per_minibatch": round(ms / batches, 4),
+            "rows_per_minibatch": rows // batches, "achieved_gbs": round(gbs, 1), "frac": round(gbs / pk["hbm_gbs"], 4),
+            "row_copy_share": round(gat / tot, 3) if tot else None,
+            "node_hit_rate": round(ncache.stats()["hit_rate"], 4), "edge_hit_rate": round(ecache.stats()["hit_rate"], 4),
+            "config": f"GDELT TGN minibatch {FETCH_MINIBATCH} edges -> {2 * FETCH_MINIBATCH} roots, 2-hop recent f10; "
+                      f"node LRU cache 3% (d_v {FETCH_DV}), edge LRU cache 3 per mille (d_e {FETCH_DE}); "
+                      f"edge table = latest {FETCH_EDGE_TABLE // 1_000_000}M edges; {batches} minibatches"}
 
 
 def cpu_baseline(cfg, src, dst, ts, roots, rts, args):
@@ -557,6 +634,7 @@ def main():
     ap.add_argument("--roots", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fetch", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-chunk", type=int, default=16)
     args = ap.parse_args()

@@ -326,18 +326,20 @@ __global__ void k_victims(const uint32_t* sorted_slots, int64_t r, int64_t* aslo
     aslot[j] = sorted_slots[j];
 }
 
+gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int64_t u, const float* values,
+                     int64_t* h_admitted, cudaStream_t s);
+
 gf_status insert_impl(gf_cache* c, const int64_t* keys, int64_t n, const float* values, int64_t* h_admitted, cudaStream_t s) {
   *h_admitted = 0;
   if (n == 0) return GF_OK;
   const int64_t G = 8 * num_sms();
   Scratch sb(s);
   Arena A;
-  GF_TRY(sb.alloc((size_t)n * 4 + (size_t)n * 8 * 3 + 64 + 4096));
+  GF_TRY(sb.alloc((size_t)n * 4 + (size_t)n * 8 * 2 + 64 + 4096));
   A.base = sb.as<char>();
   int32_t* slots = A.take<int32_t>(n);
   int64_t* ukeys = A.take<int64_t>(n);
   int64_t* usrc = A.take<int64_t>(n);
-  int64_t* aslot = A.take<int64_t>(n);
   int* flag = A.take<int>(1);
   long long* dummy = A.take<long long>(1);
   GF_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
@@ -350,8 +352,20 @@ gf_status insert_impl(gf_cache* c, const int64_t* keys, int64_t n, const float* 
   if (already) return fail(GF_EINVAL, "a key is already cached");  // cache.py:139-140
   int64_t u = 0;
   GF_TRY(dedupe_first(keys, n, nullptr, ukeys, usrc, nullptr, &u, s));
+  return place_impl(c, ukeys, usrc, u, values, h_admitted, s);
+}
+
+// Admit the first min(u, max_update) of u distinct, uncached keys (cache.py:144-177); the row of
+// ukeys[j] is values[usrc[j]].
+gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int64_t u, const float* values,
+                     int64_t* h_admitted, cudaStream_t s) {
+  *h_admitted = 0;
+  const int64_t G = 8 * num_sms();
   int64_t na = std::min<int64_t>(u, c->max_update);  // cache.py:144
   if (na == 0) return GF_OK;
+  Scratch ab(s);
+  GF_TRY(ab.alloc((size_t)na * 8 + 256));
+  int64_t* aslot = ab.as<int64_t>();
   const int64_t new_score = (c->policy == GF_CACHE_LFU) ? 1 : 0;
   if (c->policy == GF_CACHE_FIFO) {  // cache.py:148-153
     GF_LAUNCH(k_fifo_slots, grid_for(na, 256, G), 256, 0, s, c->fifo_head, c->capacity, na, aslot);
@@ -526,6 +540,71 @@ gf_status grow(T*& p, int64_t keep, int64_t cap, cudaStream_t s, bool zero_tail 
   return GF_OK;
 }
 
+// K6 (fetch block): out[i] = cache row (slot >= 0), else table row (tidx >= 0), else zeros.  One warp
+// per row: every 128-bit load of the 16-byte-pitched source row is issued before any use, the row is
+// staged in shared memory, then written to the packed [n, dim] output with coalesced stores (any
+// dim alignment).
+constexpr int FG_V4 = 8;  // float4 per lane: rows up to 1024 floats
+__global__ void __launch_bounds__(256) k_fetch_gather(const float* __restrict__ cache, int64_t cpitch,
+                                                      const int32_t* __restrict__ slots, const float* __restrict__ table,
+                                                      int64_t tpitch, const int64_t* __restrict__ tidx, int64_t n,
+                                                      int64_t dim, float* __restrict__ out) {
+  __shared__ float4 sm[8][32 * FG_V4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int dim4 = (int)((dim + 3) >> 2);
+  const float* smf = reinterpret_cast<const float*>(sm[w]);
+  for (int64_t i = warp; i < n; i += nw) {
+    const int32_t sl = slots[i];
+    const float4* src = nullptr;
+    if (sl >= 0) src = reinterpret_cast<const float4*>(cache + (int64_t)sl * cpitch);
+    else if (tidx[i] >= 0) src = reinterpret_cast<const float4*>(table + tidx[i] * tpitch);
+    float4 v[FG_V4];
+#pragma unroll
+    for (int k = 0; k < FG_V4; k++) {
+      const int c4 = lane + 32 * k;
+      v[k] = (src && c4 < dim4) ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < FG_V4; k++)
+      if (lane + 32 * k < dim4) sm[w][lane + 32 * k] = v[k];
+    __syncwarp();
+    float* o = out + i * dim;
+    for (int64_t c = lane; c < dim; c += 32) __stcs(o + c, smf[c]);
+    __syncwarp();
+  }
+}
+
+__global__ void k_fill_from_table(const int32_t* __restrict__ slots, const float* __restrict__ table, int64_t tpitch,
+                                  const int64_t* __restrict__ tidx, int64_t n, int64_t dim, float* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nw) {
+    if (slots[i] >= 0 || tidx[i] < 0) continue;  // hit, or unknown id (zeros already written)
+    const float* r = table + tidx[i] * tpitch;
+    for (int64_t c = lane; c < dim; c += 32) out[i * dim + c] = __ldg(r + c);
+  }
+}
+
+__global__ void k_unique_found(const int64_t* __restrict__ msrc, const uint8_t* __restrict__ found, int64_t m,
+                               int64_t* flag) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    flag[j] = found[msrc[j]];
+  if (blockIdx.x == 0 && threadIdx.x == 0) flag[m] = 0;
+}
+
+__global__ void k_compact_found(const int64_t* __restrict__ flag, const int64_t* __restrict__ pos, int64_t m,
+                                const int64_t* __restrict__ miss, const int64_t* __restrict__ msrc, int64_t* okeys,
+                                int64_t* osrc) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    if (flag[j]) {
+      okeys[pos[j]] = miss[j];
+      osrc[pos[j]] = msrc[j];
+    }
+}
+
 gf_status ftable_get_idx(gf_ftable* t, const int64_t* ids, int64_t n, int64_t* idx, uint8_t* found, cudaStream_t s) {
   const int64_t G = 8 * num_sms();
   if (t->kind == 0) {
@@ -538,6 +617,20 @@ gf_status ftable_get_idx(gf_ftable* t, const int64_t* ids, int64_t n, int64_t* i
   } else {
     GF_LAUNCH(k_edge_idx, grid_for(n, 256, G), 256, 0, s, ids, n, t->ids, t->n, idx, found);
   }
+  return GF_OK;
+}
+
+gf_status fetch_gather(gf_cache* c, const int32_t* slots, gf_ftable* t, const int64_t* tidx, int64_t n, float* out,
+                       cudaStream_t s) {
+  if (c->dim == 0) return GF_OK;
+  if (c->dim > 4 * 32 * FG_V4) {  // wide rows: hits from the cache, then misses from the table
+    GF_TRY(gather(c->storage, c->pitch, nullptr, slots, n, c->dim, out, c->dim, s));
+    GF_LAUNCH(k_fill_from_table, grid_for(n * 32, 256, 8 * num_sms()), 256, 0, s, slots, t->rows, t->pitch, tidx, n,
+              c->dim, out);
+    return GF_OK;
+  }
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * 16);
+  GF_LAUNCH(k_fetch_gather, blocks, 256, 0, s, c->storage, c->pitch, slots, t->rows, t->pitch, tidx, n, c->dim, out);
   return GF_OK;
 }
 
@@ -843,35 +936,7 @@ gf_status gf_gather_rows(const float* d_table, int64_t ld, const int64_t* d_idx,
   return gather(d_table, ld, d_idx, nullptr, n, dim, d_out, dim, (cudaStream_t)stream);
 }
 
-__global__ void k_fill_misses(const int64_t* __restrict__ miss_rank, int64_t n, const float* __restrict__ miss_rows,
-                              int64_t dim, float* values) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n; i += nw) {
-    int64_t r = miss_rank[i];
-    if (r < 0) continue;
-    for (int64_t c = lane; c < dim; c += 32) values[i * dim + c] = miss_rows[r * dim + c];
-  }
-}
 
-__global__ void k_found_flags(const uint8_t* found, int64_t m, int64_t* flag) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    flag[i] = found[i];
-  if (blockIdx.x == 0 && threadIdx.x == 0) flag[m] = 0;
-}
-__global__ void k_found_scatter(const int64_t* flag, const int64_t* pos, int64_t m, const int64_t* keys, const float* rows,
-                                int64_t dim, int64_t* okeys, float* orows) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < m; i += nw) {
-    if (!flag[i]) continue;
-    int64_t p = pos[i];
-    if (lane == 0) okeys[p] = keys[i];
-    for (int64_t c = lane; c < dim; c += 32) orows[p * dim + c] = rows[i * dim + c];
-  }
-}
 
 gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, int64_t n, float* d_values, uint8_t* d_hit,
                             int64_t* h_n_miss, int64_t* h_admitted, void* stream) {
@@ -887,38 +952,55 @@ gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, in
   const int64_t dim = c->dim;
   Scratch sb(s);
   Arena A;
-  GF_TRY(sb.alloc((size_t)n * 16 + 4096));
-  A.base = sb.as<char>();
-  int64_t* miss = A.take<int64_t>(n);
-  int64_t* mrank = A.take<int64_t>(n);
-  int64_t nm = 0;
-  // cache.fetch(keys) (harness.py:438)
-  GF_TRY(fetch_impl(c, d_keys, n, d_values, d_hit, miss, &nm, mrank, s));
+  int32_t* slots;
+  int64_t *tidx, *miss, *msrc, *flag, *pos, *okeys, *osrc;
+  uint8_t* found;
+  float* values = d_values;
+  auto carve = [&](Arena& a) {
+    slots = a.take<int32_t>(n);
+    tidx = a.take<int64_t>(n);
+    found = a.take<uint8_t>(n);
+    miss = a.take<int64_t>(n);
+    msrc = a.take<int64_t>(n);
+    flag = a.take<int64_t>(n + 1);
+    pos = a.take<int64_t>(n + 1);
+    okeys = a.take<int64_t>(n);
+    osrc = a.take<int64_t>(n);
+    if (!d_values) values = a.take<float>(n * dim);  // rows are still needed for the insert
+  };
+  {
+    Arena probe;
+    carve(probe);
+    GF_TRY(sb.alloc(probe.off + 4096));
+    A.base = sb.as<char>();
+    carve(A);
+  }
+  // cache.fetch(keys) (harness.py:438, cache.py:85-121): probe, score event, miss counting
+  GF_LAUNCH(k_lookup, grid_for(n, 256, G), 256, 0, s, d_keys, n, c->hkeys, c->hslots, c->tsize - 1, slots, d_hit,
+            c->counters);
+  // store.get(miss) (harness.py:440): table row of every occurrence; hits and misses are then
+  // copied to the output in one pass, each row once
+  GF_TRY(ftable_get_idx(t, d_keys, n, tidx, found, s));
+  GF_TRY(fetch_gather(c, slots, t, tidx, n, values, s));
+  if (c->policy == GF_CACHE_LRU) {
+    GF_LAUNCH(k_lru_decay, grid_for(c->capacity, 256, G), 256, 0, s, c->keys, c->scores, c->capacity);
+    GF_LAUNCH(k_score_hits, grid_for(n, 256, G), 256, 0, s, slots, n, c->scores, 0);
+  } else if (c->policy == GF_CACHE_LFU) {
+    GF_LAUNCH(k_score_hits, grid_for(n, 256, G), 256, 0, s, slots, n, c->scores, 1);
+  }
   GF_LAUNCH(k_count_misses, grid_for(n, 256, G), 256, 0, s, d_hit, (const int32_t*)nullptr, n, c->counters + 1);
+  int64_t nm = 0;
+  GF_TRY(dedupe_first(d_keys, n, slots, miss, msrc, nullptr, &nm, s));  // distinct misses, first-occurrence order
   *h_n_miss = nm;
   if (nm == 0) return GF_OK;
-  Scratch mb(s);
-  Arena M;
-  GF_TRY(mb.alloc((size_t)nm * (8 * 3 + 1) + (size_t)nm * dim * 4 * 2 + 8192));
-  M.base = mb.as<char>();
-  int64_t* flag = M.take<int64_t>(nm + 1);
-  int64_t* pos = M.take<int64_t>(nm + 1);
-  int64_t* okeys = M.take<int64_t>(nm);
-  uint8_t* found = M.take<uint8_t>(nm);
-  float* mrows = M.take<float>(nm * dim);
-  float* orows = M.take<float>(nm * dim);
-  // store.get(miss) (harness.py:440)
-  GF_TRY(gf_ftable_get(t, miss, nm, mrows, found, s));
-  // complete the returned rows with the fetched misses
-  if (d_values) GF_LAUNCH(k_fill_misses, grid_for(n * 32, 256, G), 256, 0, s, mrank, n, mrows, dim, d_values);
-  // insert_batch(miss[found], rows[found]) (harness.py:441)
-  GF_LAUNCH(k_found_flags, grid_for(nm, 256, G), 256, 0, s, found, nm, flag);
+  // insert_batch(miss[found], rows[found]) (harness.py:441): rows are read back from the output
+  GF_LAUNCH(k_unique_found, grid_for(nm, 256, G), 256, 0, s, msrc, found, nm, flag);
   GF_TRY(cub_call([&](void* tt, size_t& b) { return cub::DeviceScan::ExclusiveSum(tt, b, flag, pos, (int)(nm + 1), s); }, s));
-  GF_LAUNCH(k_found_scatter, grid_for(nm * 32, 256, G), 256, 0, s, flag, pos, nm, miss, mrows, dim, okeys, orows);
+  GF_LAUNCH(k_compact_found, grid_for(nm, 256, G), 256, 0, s, flag, pos, nm, miss, msrc, okeys, osrc);
   int64_t nf = 0;
   GF_CUDA(cudaMemcpyAsync(&nf, pos + nm, 8, cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
-  return insert_impl(c, okeys, nf, orows, h_admitted, s);
+  return place_impl(c, okeys, osrc, nf, values, h_admitted, s);
 }
 
 }  // extern "C"
