@@ -220,9 +220,51 @@ gf_status cub_call(F f, cudaStream_t s) {
   return GF_OK;
 }
 
+// K6 (fetch block): out[i] = cache row (slot >= 0), else table row (tidx >= 0), else zeros.  One warp
+// per row: every 128-bit load of the 16-byte-pitched source row is issued before any use, the row is
+// staged in shared memory, then written to the packed [n, dim] output with coalesced stores (any
+// dim alignment).
+constexpr int FG_V4 = 8;  // float4 per lane: rows up to 1024 floats
+__global__ void __launch_bounds__(256) k_fetch_gather(const float* __restrict__ cache, int64_t cpitch,
+                                                      const int32_t* __restrict__ slots, const float* __restrict__ table,
+                                                      int64_t tpitch, const int64_t* __restrict__ tidx, int64_t n,
+                                                      int64_t dim, float* __restrict__ out) {
+  __shared__ float4 sm[8][32 * FG_V4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int dim4 = (int)((dim + 3) >> 2);
+  const float* smf = reinterpret_cast<const float*>(sm[w]);
+  for (int64_t i = warp; i < n; i += nw) {
+    const int32_t sl = slots ? slots[i] : -1;
+    const float4* src = nullptr;
+    if (sl >= 0) src = reinterpret_cast<const float4*>(cache + (int64_t)sl * cpitch);
+    else if (tidx && tidx[i] >= 0) src = reinterpret_cast<const float4*>(table + tidx[i] * tpitch);
+    float4 v[FG_V4];
+#pragma unroll
+    for (int k = 0; k < FG_V4; k++) {
+      const int c4 = lane + 32 * k;
+      v[k] = (src && c4 < dim4) ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < FG_V4; k++)
+      if (lane + 32 * k < dim4) sm[w][lane + 32 * k] = v[k];
+    __syncwarp();
+    float* o = out + i * dim;
+    for (int64_t c = lane; c < dim; c += 32) __stcs(o + c, smf[c]);
+    __syncwarp();
+  }
+}
+
 gf_status gather(const float* table, int64_t ld, const int64_t* idx64, const int32_t* idx32, int64_t n, int64_t dim,
                  float* out, int64_t out_ld, cudaStream_t s) {
   if (n <= 0 || dim <= 0) return GF_OK;
+  if (out_ld == dim && (ld & 3) == 0 && (((uintptr_t)table) & 15) == 0 && dim <= 4 * 32 * FG_V4) {
+    // staged 128-bit path (rows of a 16-byte pitch, packed output of any alignment)
+    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * 16);
+    GF_LAUNCH(k_fetch_gather, blocks, 256, 0, s, table, ld, idx32, table, ld, idx64, n, dim, out);
+    return GF_OK;
+  }
   int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)num_sms() * 32);
   GF_LAUNCH(k_gather_rows, blocks, 256, 0, s, table, ld, idx64, idx32, n, dim, out, out_ld);
   return GF_OK;
@@ -540,41 +582,6 @@ gf_status grow(T*& p, int64_t keep, int64_t cap, cudaStream_t s, bool zero_tail 
   return GF_OK;
 }
 
-// K6 (fetch block): out[i] = cache row (slot >= 0), else table row (tidx >= 0), else zeros.  One warp
-// per row: every 128-bit load of the 16-byte-pitched source row is issued before any use, the row is
-// staged in shared memory, then written to the packed [n, dim] output with coalesced stores (any
-// dim alignment).
-constexpr int FG_V4 = 8;  // float4 per lane: rows up to 1024 floats
-__global__ void __launch_bounds__(256) k_fetch_gather(const float* __restrict__ cache, int64_t cpitch,
-                                                      const int32_t* __restrict__ slots, const float* __restrict__ table,
-                                                      int64_t tpitch, const int64_t* __restrict__ tidx, int64_t n,
-                                                      int64_t dim, float* __restrict__ out) {
-  __shared__ float4 sm[8][32 * FG_V4];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int dim4 = (int)((dim + 3) >> 2);
-  const float* smf = reinterpret_cast<const float*>(sm[w]);
-  for (int64_t i = warp; i < n; i += nw) {
-    const int32_t sl = slots[i];
-    const float4* src = nullptr;
-    if (sl >= 0) src = reinterpret_cast<const float4*>(cache + (int64_t)sl * cpitch);
-    else if (tidx[i] >= 0) src = reinterpret_cast<const float4*>(table + tidx[i] * tpitch);
-    float4 v[FG_V4];
-#pragma unroll
-    for (int k = 0; k < FG_V4; k++) {
-      const int c4 = lane + 32 * k;
-      v[k] = (src && c4 < dim4) ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int k = 0; k < FG_V4; k++)
-      if (lane + 32 * k < dim4) sm[w][lane + 32 * k] = v[k];
-    __syncwarp();
-    float* o = out + i * dim;
-    for (int64_t c = lane; c < dim; c += 32) __stcs(o + c, smf[c]);
-    __syncwarp();
-  }
-}
 
 __global__ void k_fill_from_table(const int32_t* __restrict__ slots, const float* __restrict__ table, int64_t tpitch,
                                   const int64_t* __restrict__ tidx, int64_t n, int64_t dim, float* out) {
