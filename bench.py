@@ -560,6 +560,7 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 20) -> dict:
     return {"value": round(rows / (ms / 1e3), 1), "unit": "fetched rows/s", "ms_per_minibatch": round(ms / batches, 4),
             "rows_per_minibatch": rows // batches, "achieved_gbs": round(gbs, 1), "frac": round(gbs / pk["hbm_gbs"], 4),
             "row_copy_share": round(gat / tot, 3) if tot else None,
+            "top_kernels": {k: round(v[1] / tot, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])[:8]},
             "node_hit_rate": round(ncache.stats()["hit_rate"], 4), "edge_hit_rate": round(ecache.stats()["hit_rate"], 4),
             "config": f"GDELT TGN minibatch {FETCH_MINIBATCH} edges -> {2 * FETCH_MINIBATCH} roots, 2-hop recent f10; "
                       f"node LRU cache 3% (d_v {FETCH_DV}), edge LRU cache 3 per mille (d_e {FETCH_DE}); "

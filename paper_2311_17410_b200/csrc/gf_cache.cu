@@ -347,10 +347,26 @@ __global__ void k_fifo_slots(int64_t head, int64_t cap, int64_t na, int64_t* asl
     aslot[j] = (head + j) % cap;
 }
 
-__global__ void k_free_flags(const int64_t* keys, int64_t cap, int64_t* flag, uint32_t* iota) {
+// free-slot flags, slot identities for the victim sort, and the score range of the occupied slots
+__global__ void k_free_flags(const int64_t* keys, const int64_t* scores, int64_t cap, int64_t* flag, uint32_t* iota,
+                             long long* mm) {
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x) {
-    flag[s] = keys[s] == GF_EMPTY_KEY;
+    const bool empty = keys[s] == GF_EMPTY_KEY;
+    flag[s] = empty;
     iota[s] = (uint32_t)s;
+    if (!empty) {
+      lo = min(lo, (long long)scores[s]);
+      hi = max(hi, (long long)scores[s]);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0 && lo <= hi) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) flag[cap] = 0;
 }
@@ -359,9 +375,10 @@ __global__ void k_free_scatter(const int64_t* flag, const int64_t* pos, int64_t 
     if (flag[s]) free_slots[pos[s]] = s;
 }
 // order-preserving int64 -> uint64 for the (score, slot) radix sort
-__global__ void k_score_keys(const int64_t* scores, int64_t cap, uint64_t* out) {
+// score - lo: order-preserving and narrow, so the victim sort runs over only the bits the range needs
+__global__ void k_score_keys(const int64_t* scores, int64_t cap, int64_t lo, uint64_t* out) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x)
-    out[s] = (uint64_t)scores[s] ^ 0x8000000000000000ull;
+    out[s] = (uint64_t)(scores[s] - lo);
 }
 __global__ void k_victims(const uint32_t* sorted_slots, int64_t r, int64_t* aslot) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < r; j += (int64_t)gridDim.x * blockDim.x)
@@ -419,7 +436,7 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
     const int64_t cap = c->capacity;
     Scratch fb(s);
     Arena F;
-    GF_TRY(fb.alloc((size_t)(cap + 1) * 8 * 3 + (size_t)cap * 4 * 2 + (size_t)cap * 8 * 2 + 4096));
+    GF_TRY(fb.alloc((size_t)(cap + 1) * 8 * 3 + (size_t)cap * 4 * 2 + (size_t)cap * 8 * 2 + 8192));
     F.base = fb.as<char>();
     int64_t* ff = F.take<int64_t>(cap + 1);
     int64_t* fpos = F.take<int64_t>(cap + 1);
@@ -428,11 +445,16 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
     uint32_t* sorted_slots = F.take<uint32_t>(cap);
     uint64_t* skeys = F.take<uint64_t>(cap);
     uint64_t* skeys_sorted = F.take<uint64_t>(cap);
-    GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, cap, ff, iota);
+    long long* mm = reinterpret_cast<long long*>(F.take<int64_t>(2));
+    const long long mm0[2] = {LLONG_MAX, LLONG_MIN};
+    GF_CUDA(cudaMemcpyAsync(mm, mm0, sizeof(mm0), cudaMemcpyHostToDevice, s));
+    GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, iota, mm);
     GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, ff, fpos, (int)(cap + 1), s); }, s));
     GF_LAUNCH(k_free_scatter, grid_for(cap, 256, G), 256, 0, s, ff, fpos, cap, free_slots);
     int64_t nfree = 0;
+    long long hmm[2];
     GF_CUDA(cudaMemcpyAsync(&nfree, fpos + cap, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GF_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
     GF_CUDA(cudaStreamSynchronize(s));
     int64_t nfill = std::min(nfree, na);
     if (nfill > 0) {
@@ -444,9 +466,13 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
     int64_t r = na - nfill;
     if (r > 0) {
       // victims: lowest (score, slot) over the post-fill occupied slots (cache.py:160-166)
-      GF_LAUNCH(k_score_keys, grid_for(cap, 256, G), 256, 0, s, c->scores, cap, skeys);
+      // post-fill scores: the occupied range plus the new slots' score
+      const long long lo = std::min<long long>(hmm[0], new_score), hi = std::max<long long>(hmm[1], new_score);
+      int bits = 1;
+      while (bits < 64 && ((unsigned long long)(hi - lo) >> bits) != 0) bits++;
+      GF_LAUNCH(k_score_keys, grid_for(cap, 256, G), 256, 0, s, c->scores, cap, (int64_t)lo, skeys);
       GF_TRY(cub_call([&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(t, b, skeys, skeys_sorted, iota, sorted_slots, (int)cap, 0, 64, s);
+        return cub::DeviceRadixSort::SortPairs(t, b, skeys, skeys_sorted, iota, sorted_slots, (int)cap, 0, bits, s);
       }, s));
       GF_LAUNCH(k_victims, grid_for(r, 256, G), 256, 0, s, sorted_slots, r, aslot);
       GF_LAUNCH(k_place, grid_for(r, 256, G), 256, 0, s, ukeys + nfill, usrc + nfill, aslot, r, c->keys, c->scores,

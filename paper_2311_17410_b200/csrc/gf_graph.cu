@@ -852,15 +852,18 @@ __device__ __forceinline__ void st_flag(int* p, int v) {
 
 template <int K>
 __global__ void __launch_bounds__(SCAN_T) k_scan_sum(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
-                                                      ScanState S, const IngestCounters* c) {
+                                                      ScanState S, const IngestCounters* c, bool per_segment) {
   __shared__ unsigned s_tile;
   __shared__ int64_t s_w[SCAN_T / 32][K];
   __shared__ int64_t s_base[K];
   if (c->abort) return;
+  // per-segment records: only num_segs + 1 of the E + 1 entries can be nonzero (the last is the total)
+  if (per_segment) n = min(n, (int64_t)c->num_segs + 1);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(S.ticket, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
+  if (tile * SCAN_TILE >= n) return;  // no later tile looks back at this one
   const int64_t i0 = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
   int64_t v[SCAN_ITEMS][K], run[K];
 #pragma unroll
@@ -1058,9 +1061,10 @@ __global__ void k_check_enumerate(const longlong4* __restrict__ off4, int64_t E,
                                   const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R, longlong2* trig) {
   if (c->abort) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c->new_blocks = off4[E].x;
-    c->new_slots = off4[E].y;
-    c->dir_need = off4[E].z;
+    const int64_t ns = c->num_segs;  // off4 holds the scan up to num_segs (the total)
+    c->new_blocks = off4[ns].x;
+    c->new_slots = off4[ns].y;
+    c->dir_need = off4[ns].z;
     if (c->new_slots > S->slots_free || c->dir_need > S->dir_free) c->abort |= ABORT_CAP;  // nothing written yet
   }
   const int64_t nseg = c->num_segs;
@@ -1412,10 +1416,10 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
       GF_LAUNCH(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize,
                 g->bcap, g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, old_tail);
-      GF_LAUNCH(k_scan_sum<4>, tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc);
+      GF_LAUNCH(k_scan_sum<4>, tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
       GF_LAUNCH(k_check_enumerate, grid_for(E, T, G), T, 0, s, off4, E, ds, dc, ce_pend, ce_ev, P, keys, seg_start,
                 g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
-      GF_LAUNCH(k_scan_sum<2>, tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc);
+      GF_LAUNCH(k_scan_sum<2>, tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
       NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
                    g->nflags, g->nrec};
       BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
