@@ -100,6 +100,22 @@ __device__ __forceinline__ Slot load_slot(const Slot* p) {
   return s;
 }
 
+// the three output fields only (ts, eid: one 128-bit load; nbr: one 32-bit load from the same sector)
+__device__ __forceinline__ Slot load_out3(const Slot* p) {
+  Slot s;
+  long long a, b;
+  int c;
+  asm("ld.global.nc.v2.b64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  asm("ld.global.nc.b32 %0, [%1];" : "=r"(c) : "l"(reinterpret_cast<const char*>(p) + 16));
+  s.ts = a;
+  s.eid = b;
+  s.nbr = c;
+  s.owner = 0;
+  s.valid = 1;
+  s.pad = 0;
+  return s;
+}
+
 __device__ __forceinline__ void store_out(const LayerOut& O, int64_t at, const Slot& s, uint64_t qkey, int64_t i) {
   if (at >= O.cap) {
     *O.overflow = 1;
@@ -714,7 +730,7 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
   bool irregular = false, live = false, known = true;
   uint64_t qkey = 0;
   LaneNode N;
-  LaneBlk hb;
+  LaneBlk hb{};
   // window search inside the boundary block
   auto finish = [&]() {
     hi = hb.cum + lane_block_lower_bound(GV, hb.base, hb.size, hb.t0, hb.t1, te);
@@ -853,6 +869,10 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
   }
 
   // ---- cooperative gather + CSR store of the warp's contiguous range ----
+  // recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
+  // (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
+  // choice is the faster one for its policy)
+#define GF_LOAD_OUT(ptr) (EARLY ? load_out3(ptr) : load_slot(ptr))
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   const int64_t out0 = base + wpre;
   __syncwarp();
@@ -863,7 +883,7 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
 #pragma unroll
     for (int u = 0; u < GF_GATHER_UNROLL; u++) {
       j[u] = s_owner[w][e + 32 * u];
-      s[u] = load_slot(GV.slots + s_sel[w][j[u]][e + 32 * u - s_pre[w][j[u]]]);
+      s[u] = GF_LOAD_OUT(GV.slots + s_sel[w][j[u]][e + 32 * u - s_pre[w][j[u]]]);
     }
 #pragma unroll
     for (int u = 0; u < GF_GATHER_UNROLL; u++)
@@ -872,8 +892,9 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
   for (; e < total; e += 32) {
     const int jj = s_owner[w][e];
     const int i = e - s_pre[w][jj];
-    store_out(O, out0 + e, load_slot(GV.slots + s_sel[w][jj][i]), s_key[w][jj], i);
+    store_out(O, out0 + e, GF_LOAD_OUT(GV.slots + s_sel[w][jj][i]), s_key[w][jj], i);
   }
+#undef GF_LOAD_OUT
 }
 
 // ========================== general path (deletions) =========================
