@@ -307,6 +307,11 @@ class TemporalSampler:
         self.policy = SamplingPolicy(strategy, delta)
         self.seed = seed
 
-    def sample(self, roots, ts, seed: int | None = None, root_key_base: int = 0, stream=None) -> LayeredSample:
-        req = SampleRequest(roots, ts, self.fanouts, self.policy, self.seed if seed is None else seed)
+    def sample(self, roots, ts, fanouts=None, strategy: str | None = None, seed: int | None = None,
+               root_key_base: int = 0, stream=None, delta: int | None = None) -> LayeredSample:
+        """``sample(roots, ts)`` with the constructor's settings, or the north-star form
+        ``sample(roots, ts, fanouts, strategy)`` overriding them for this call."""
+        fo = self.fanouts if fanouts is None else [int(f) for f in fanouts]
+        pol = self.policy if strategy is None else SamplingPolicy(strategy, self.policy.delta if delta is None else delta)
+        req = SampleRequest(roots, ts, fo, pol, self.seed if seed is None else seed)
         return sample_khop(self.graph, req, root_key_base=root_key_base, stream=stream)

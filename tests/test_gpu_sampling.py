@@ -217,3 +217,25 @@ def test_reference_semantics_goldens(cuda_device):
     g3.delete_node(1)
     assert gf.sample_layer(g3, [1], [0], [10], 10**9, gf.SamplingPolicy.recent(), 0).offsets.tolist() == [0, 0]
     assert gf.sample_layer(g3, [0], [0], [10], 10**9, gf.SamplingPolicy.recent(), 0).neighbors.tolist() == [2]
+
+
+def test_temporal_sampler_north_star_form(cuda_device):
+    """TemporalSampler.sample(roots, ts, fanouts, strategy) == the constructor-configured form."""
+    import torch
+
+    import paper_2311_17410_b200 as gf
+
+    src, dst, ts = gf.generate_synthetic_arrays(500, 30_000, 2.2, 50_000, seed=4, src_skew=2.2)
+    g = gf.DynamicGraph(directed=True, tau=64)
+    g.add_edges_arrays(src, dst, ts)
+    roots = torch.from_numpy(np.concatenate([src[-300:], dst[-300:]])).cuda()
+    rts = torch.from_numpy(np.concatenate([ts[-300:], ts[-300:]])).cuda()
+    base = gf.TemporalSampler(g, [5], "recent", seed=2)
+    for fo, strat in (([10, 10], "uniform"), ([3], "recent"), ([4, 2], "uniform")):
+        a = base.sample(roots, rts, fo, strat)
+        b = gf.TemporalSampler(g, fo, strat, seed=2).sample(roots, rts)
+        assert len(a.layers) == len(fo)
+        for la, lb in zip(a.layers, b.layers):
+            for x, y in zip((la.offsets, la.neighbors, la.edge_ids, la.timestamps),
+                            (lb.offsets, lb.neighbors, lb.edge_ids, lb.timestamps)):
+                assert torch.equal(x, y)
