@@ -63,6 +63,9 @@ def main() -> None:
             "regs": to_float(r["launch__registers_per_thread"]),
             "issue_per_sched": round(to_float(r["smsp__issue_active.avg.per_cycle_active"]), 3),
         }
+        te = r.get("smsp__thread_inst_executed_per_inst_executed.ratio")
+        if te:
+            e["warp_exec_efficiency_pct"] = round(100 * to_float(te) / 32, 1)
         req = r.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum")
         sec = r.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")
         if req and sec:
