@@ -1546,6 +1546,8 @@ void free_graph(gf_graph* g) {
   if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);
   if (g->ing_host) cudaFreeHost(g->ing_host);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+  if (g->smp_buf) cudaFree(g->smp_buf);
+  if (g->smp_host) cudaFreeHost(g->smp_host);
 
 }
 

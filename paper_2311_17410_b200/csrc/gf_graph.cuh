@@ -16,6 +16,7 @@
 //   nflags     (u8 per node)                   bit 0: block list not on the sizing law's closed form
 #pragma once
 
+#include <atomic>
 #include <vector>
 
 #include "gf_common.cuh"
@@ -62,6 +63,12 @@ struct gf_graph {
   cudaStream_t cap_stream = nullptr;
   int64_t ing_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   int64_t ing_nodes = 0;      // kernel launches per replay
+  // persistent sampling scratch (totals, per-hop tile state, child keys) + pinned totals; a call
+  // that finds it busy (another stream) allocates its own
+  void* smp_buf = nullptr;
+  size_t smp_bytes = 0;
+  int64_t* smp_host = nullptr;
+  std::atomic<int> smp_busy{0};
 };
 
 namespace gf {

@@ -1109,18 +1109,27 @@ bool fused_enabled() {
 
 // total must already be zero (callers clear their totals once per call): a layer with no
 // queries launches nothing that would write it.
+bool uses_fused(const gf_graph* g, int64_t fanout) {
+  return !g->any_deleted && fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled();
+}
+
+int64_t tile_words(int64_t cap_q) { return (cap_q + FT - 1) / FT + 1; }  // status words + ticket
+
+// tile_state: (tiles + 1) zeroed words for the fused kernel, or NULL to allocate them here
 gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_offsets, const LayerOut& O, int64_t* total,
-                       cudaStream_t s) {
+                       cudaStream_t s, uint64_t* tile_state = nullptr) {
   GraphView GV = view_of(g);
   const bool fast = !g->any_deleted;
-  if (fast && Q.fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled() && cap_q > 0) {
-    // per-call tile state (concurrent sampling of one graph on several streams stays safe);
+  if (uses_fused(g, Q.fanout) && cap_q > 0) {
     // offsets[0] is written by tile 0, which always runs
     const int64_t tiles = (cap_q + FT - 1) / FT;
     Scratch sb(s);
-    GF_TRY(sb.alloc(sizeof(uint64_t) * (tiles + 1)));
-    TileCtl C{sb.as<uint64_t>(), reinterpret_cast<unsigned long long*>(sb.as<uint64_t>() + tiles), total};
-    GF_CUDA(cudaMemsetAsync(C.status, 0, sizeof(uint64_t) * (tiles + 1), s));
+    if (!tile_state) {
+      GF_TRY(sb.alloc(sizeof(uint64_t) * (tiles + 1)));
+      tile_state = sb.as<uint64_t>();
+      GF_CUDA(cudaMemsetAsync(tile_state, 0, sizeof(uint64_t) * (tiles + 1), s));
+    }
+    TileCtl C{tile_state, reinterpret_cast<unsigned long long*>(tile_state + tiles), total};
     if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, FT, 0, s, GV, Q, O, C);
     else GF_LAUNCH(k_sample_fused<false>, tiles, FT, 0, s, GV, Q, O, C);
     return GF_OK;
@@ -1199,20 +1208,53 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
   int64_t key_cap = 0;
   if (need_keys)
     for (int h = 0; h + 1 < n_hops; h++) key_cap = std::max(key_cap, h_caps[h]);
-  Scratch sb(s);
-  Arena Ar;
-  {
-    Arena probe;
-    probe.take<int64_t>(n_hops + 2);
-    probe.take<uint64_t>(key_cap);
-    probe.take<uint64_t>(key_cap);
-    GF_TRY(sb.alloc(probe.off + 1024));
+  // one region: totals, then every hop's tile state (zeroed by one memset), then the child keys
+  int64_t zero_words = n_hops + 2;
+  std::vector<int64_t> tile_off(n_hops, -1);
+  for (int h = 0; h < n_hops; h++) {
+    const int64_t cq = (h == 0) ? n_roots : h_caps[h - 1];
+    if (uses_fused(g, h_fanouts[h]) && cq > 0) {
+      tile_off[h] = zero_words;
+      zero_words += tile_words(cq);
+    }
   }
-  Ar.base = sb.as<char>();
-  int64_t* totals = Ar.take<int64_t>(n_hops + 2);
-  uint64_t* keybuf[2] = {Ar.take<uint64_t>(key_cap), Ar.take<uint64_t>(key_cap)};
+  const size_t bytes = sizeof(int64_t) * (size_t)zero_words + 256 + 2 * sizeof(uint64_t) * (size_t)key_cap + 512;
+  Scratch sb(s);
+  char* base = nullptr;
+  int64_t* hbuf = nullptr;
+  std::vector<int64_t> hvec;
+  const bool own = g->smp_busy.exchange(1) == 0;  // the persistent buffer, unless another call holds it
+  struct Release {
+    gf_graph* g;
+    bool own;
+    ~Release() {
+      if (own) g->smp_busy.store(0);
+    }
+  } rel{g, own};
+  if (own) {
+    if (bytes > g->smp_bytes) {
+      if (g->smp_buf) GF_CUDA(cudaFreeAsync(g->smp_buf, s));
+      g->smp_buf = nullptr;
+      g->smp_bytes = 0;
+      GF_CUDA(cudaMallocAsync(&g->smp_buf, bytes + bytes / 4, s));
+      g->smp_bytes = bytes + bytes / 4;
+    }
+    if (!g->smp_host) GF_CUDA(cudaMallocHost(&g->smp_host, 4096));
+    base = (char*)g->smp_buf;
+    if (n_hops + 1 <= 512) hbuf = g->smp_host;
+  } else {
+    GF_TRY(sb.alloc(bytes));
+    base = sb.as<char>();
+  }
+  if (!hbuf) {
+    hvec.resize(n_hops + 1);
+    hbuf = hvec.data();
+  }
+  int64_t* totals = reinterpret_cast<int64_t*>(base);
+  uint64_t* keys0 = reinterpret_cast<uint64_t*>(base + ((sizeof(int64_t) * zero_words + 255) & ~size_t(255)));
+  uint64_t* keybuf[2] = {keys0, keys0 + key_cap};
   int* overflow = reinterpret_cast<int*>(totals + n_hops);
-  GF_CUDA(cudaMemsetAsync(totals, 0, sizeof(int64_t) * (n_hops + 2), s));
+  GF_CUDA(cudaMemsetAsync(totals, 0, sizeof(int64_t) * zero_words, s));
   const int64_t* src = d_roots;
   const int64_t* tend = d_ts;
   const int64_t* n_dev = nullptr;
@@ -1226,7 +1268,8 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
     if (g_profile.load(std::memory_order_relaxed))
       g_prof_tag = std::string(policy == GF_POLICY_RECENT ? "recent" : policy == GF_POLICY_UNIFORM ? "uniform" : "tw") +
                    "/hop" + std::to_string(h);
-    gf_status st = layer_launch(g, Q, cap_q, d_offsets[h], O, totals + h, s);
+    gf_status st = layer_launch(g, Q, cap_q, d_offsets[h], O, totals + h, s,
+                                tile_off[h] >= 0 ? reinterpret_cast<uint64_t*>(totals + tile_off[h]) : nullptr);
     g_prof_tag.clear();
     GF_TRY(st);
     src = d_nbr[h];
@@ -1234,8 +1277,8 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
     n_dev = totals + h;
     in_keys = out_keys;
   }
-  std::vector<int64_t> h(n_hops + 1);
-  GF_CUDA(cudaMemcpyAsync(h.data(), totals, sizeof(int64_t) * (n_hops + 1), cudaMemcpyDeviceToHost, s));
+  int64_t* h = hbuf;
+  GF_CUDA(cudaMemcpyAsync(h, totals, sizeof(int64_t) * (n_hops + 1), cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < n_hops; i++) h_totals[i] = h[i];
   if ((int)h[n_hops]) return fail(GF_ERANGE, "output buffer too small");
