@@ -33,6 +33,7 @@ struct gf_cache {
   int64_t* hkeys = nullptr;
   int32_t* hslots = nullptr;
   long long* counters = nullptr;  // hits, misses, evictions
+  long long* hsmall = nullptr;    // pinned: the fetch block's counts read back
 };
 
 struct gf_cache_snap {
@@ -375,6 +376,11 @@ __global__ void k_free_scatter(const int64_t* flag, const int64_t* pos, int64_t 
     if (flag[s]) free_slots[pos[s]] = s;
 }
 // order-preserving int64 -> uint64 for the (score, slot) radix sort
+__global__ void k_iota(uint32_t* iota, int64_t cap) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x)
+    iota[s] = (uint32_t)s;
+}
+
 // score - lo: order-preserving and narrow, so the victim sort runs over only the bits the range needs
 __global__ void k_score_keys(const int64_t* scores, int64_t cap, int64_t lo, uint64_t* out) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x)
@@ -385,8 +391,15 @@ __global__ void k_victims(const uint32_t* sorted_slots, int64_t r, int64_t* aslo
     aslot[j] = sorted_slots[j];
 }
 
+// free-slot state computed ahead of the placement (fetch block: read back with its other counts)
+struct FreeState {
+  const int64_t* free_slots;  // ascending free slots
+  int64_t nfree;
+  long long lo, hi;           // score range of the occupied slots (LLONG_MAX/MIN when none)
+};
+
 gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int64_t u, const float* values,
-                     int64_t* h_admitted, cudaStream_t s);
+                     int64_t* h_admitted, cudaStream_t s, const FreeState* pre = nullptr);
 
 gf_status insert_impl(gf_cache* c, const int64_t* keys, int64_t n, const float* values, int64_t* h_admitted, cudaStream_t s) {
   *h_admitted = 0;
@@ -417,7 +430,7 @@ gf_status insert_impl(gf_cache* c, const int64_t* keys, int64_t n, const float* 
 // Admit the first min(u, max_update) of u distinct, uncached keys (cache.py:144-177); the row of
 // ukeys[j] is values[usrc[j]].
 gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int64_t u, const float* values,
-                     int64_t* h_admitted, cudaStream_t s) {
+                     int64_t* h_admitted, cudaStream_t s, const FreeState* pre) {
   *h_admitted = 0;
   const int64_t G = 8 * num_sms();
   int64_t na = std::min<int64_t>(u, c->max_update);  // cache.py:144
@@ -445,17 +458,25 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
     uint32_t* sorted_slots = F.take<uint32_t>(cap);
     uint64_t* skeys = F.take<uint64_t>(cap);
     uint64_t* skeys_sorted = F.take<uint64_t>(cap);
-    long long* mm = reinterpret_cast<long long*>(F.take<int64_t>(2));
-    const long long mm0[2] = {LLONG_MAX, LLONG_MIN};
-    GF_CUDA(cudaMemcpyAsync(mm, mm0, sizeof(mm0), cudaMemcpyHostToDevice, s));
-    GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, iota, mm);
-    GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, ff, fpos, (int)(cap + 1), s); }, s));
-    GF_LAUNCH(k_free_scatter, grid_for(cap, 256, G), 256, 0, s, ff, fpos, cap, free_slots);
     int64_t nfree = 0;
     long long hmm[2];
-    GF_CUDA(cudaMemcpyAsync(&nfree, fpos + cap, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    GF_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
-    GF_CUDA(cudaStreamSynchronize(s));
+    if (pre) {
+      free_slots = const_cast<int64_t*>(pre->free_slots);
+      nfree = pre->nfree;
+      hmm[0] = pre->lo;
+      hmm[1] = pre->hi;
+      GF_LAUNCH(k_iota, grid_for(cap, 256, G), 256, 0, s, iota, cap);
+    } else {
+      long long* mm = reinterpret_cast<long long*>(F.take<int64_t>(2));
+      const long long mm0[2] = {LLONG_MAX, LLONG_MIN};
+      GF_CUDA(cudaMemcpyAsync(mm, mm0, sizeof(mm0), cudaMemcpyHostToDevice, s));
+      GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, iota, mm);
+      GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, ff, fpos, (int)(cap + 1), s); }, s));
+      GF_LAUNCH(k_free_scatter, grid_for(cap, 256, G), 256, 0, s, ff, fpos, cap, free_slots);
+      GF_CUDA(cudaMemcpyAsync(&nfree, fpos + cap, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      GF_CUDA(cudaMemcpyAsync(hmm, mm, sizeof(hmm), cudaMemcpyDeviceToHost, s));
+      GF_CUDA(cudaStreamSynchronize(s));
+    }
     int64_t nfill = std::min(nfree, na);
     if (nfill > 0) {
       GF_LAUNCH(k_place, grid_for(nfill, 256, G), 256, 0, s, ukeys, usrc, free_slots, nfill, c->keys, c->scores, new_score,
@@ -482,13 +503,13 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
     }
     GF_TRY(rebuild_map(c, s));
     *h_admitted = na;
-    GF_CUDA(cudaStreamSynchronize(s));
+    if (!pre) GF_CUDA(cudaStreamSynchronize(s));  // the fetch block stays stream-ordered
     return GF_OK;
   }
   GF_LAUNCH(k_copy_rows_to_slots, grid_for(na * 32, 256, G), 256, 0, s, values, c->dim, usrc, aslot, na, c->storage, c->pitch);
   GF_TRY(rebuild_map(c, s));
   *h_admitted = na;
-  GF_CUDA(cudaStreamSynchronize(s));
+  if (!pre) GF_CUDA(cudaStreamSynchronize(s));
   return GF_OK;
 }
 
@@ -621,21 +642,51 @@ __global__ void k_fill_from_table(const int32_t* __restrict__ slots, const float
   }
 }
 
-__global__ void k_unique_found(const int64_t* __restrict__ msrc, const uint8_t* __restrict__ found, int64_t m,
-                               int64_t* flag) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
-    flag[j] = found[msrc[j]];
-  if (blockIdx.x == 0 && threadIdx.x == 0) flag[m] = 0;
+
+
+struct AddLL2 {
+  __device__ __forceinline__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
+    return make_longlong2(a.x + b.x, a.y + b.y);
+  }
+};
+
+// fetch block: per occurrence, {first occurrence of a missing key, ... and found in the table}
+__global__ void k_ff_flags(const int64_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ slots,
+                           const int64_t* __restrict__ sk, const long long* __restrict__ smin, int64_t smask,
+                           const uint8_t* __restrict__ found, longlong2* flag2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    long long f = 0;
+    if (slots[i] < 0) f = (smin[set_find(sk, smask, keys[i])] == i);
+    flag2[i] = make_longlong2(f, f && found[i]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) flag2[n] = make_longlong2(0, 0);
 }
 
-__global__ void k_compact_found(const int64_t* __restrict__ flag, const int64_t* __restrict__ pos, int64_t m,
-                                const int64_t* __restrict__ miss, const int64_t* __restrict__ msrc, int64_t* okeys,
-                                int64_t* osrc) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
-    if (flag[j]) {
-      okeys[pos[j]] = miss[j];
-      osrc[pos[j]] = msrc[j];
+// the found distinct misses in first-occurrence order, with the position of their first occurrence
+__global__ void k_ff_scatter(const int64_t* __restrict__ keys, int64_t n, const longlong2* __restrict__ flag2,
+                             const longlong2* __restrict__ pos2, int64_t* okeys, int64_t* osrc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag2[i].y) {
+      okeys[pos2[i].y] = keys[i];
+      osrc[pos2[i].y] = i;
     }
+}
+
+// {distinct misses, found distinct misses, free slots, occupied score min, max} for one readback
+__global__ void k_ff_counts(const longlong2* pos2, int64_t n, const int64_t* fpos, int64_t cap, const long long* mm,
+                            long long* out) {
+  if (threadIdx.x || blockIdx.x) return;
+  out[0] = pos2[n].x;
+  out[1] = pos2[n].y;
+  out[2] = fpos ? fpos[cap] : 0;
+  out[3] = mm ? mm[0] : LLONG_MAX;
+  out[4] = mm ? mm[1] : LLONG_MIN;
+}
+
+__global__ void k_mm_init(long long* mm) {
+  if (threadIdx.x || blockIdx.x) return;
+  mm[0] = LLONG_MAX;
+  mm[1] = LLONG_MIN;
 }
 
 gf_status ftable_get_idx(gf_ftable* t, const int64_t* ids, int64_t n, int64_t* idx, uint8_t* found, cudaStream_t s) {
@@ -722,6 +773,7 @@ gf_status gf_cache_destroy(gf_cache* c) {
   cudaFree(c->hkeys);
   cudaFree(c->hslots);
   cudaFree(c->counters);
+  if (c->hsmall) cudaFreeHost(c->hsmall);
   delete c;
   return GF_OK;
 }
@@ -982,32 +1034,54 @@ gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, in
   DeviceGuard dg(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t G = 8 * num_sms();
-  const int64_t dim = c->dim;
+  const int64_t dim = c->dim, cap = c->capacity;
+  const bool lru_lfu = c->policy != GF_CACHE_FIFO && c->max_update > 0;
+  const int64_t ssize = pow2_at_least(2 * n);
+  size_t scan_bytes = 0, free_bytes = 0;
+  GF_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, scan_bytes, (longlong2*)nullptr, (longlong2*)nullptr, AddLL2(),
+                                         make_longlong2(0, 0), (int)(n + 1), s));
+  if (lru_lfu)
+    GF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, free_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)(cap + 1), s));
   Scratch sb(s);
-  Arena A;
   int32_t* slots;
-  int64_t *tidx, *miss, *msrc, *flag, *pos, *okeys, *osrc;
+  int64_t *tidx, *okeys, *osrc, *sk, *ff = nullptr, *fpos = nullptr, *free_slots = nullptr;
+  long long *smin, *mm = nullptr, *counts;
   uint8_t* found;
+  longlong2 *flag2, *pos2;
+  uint32_t* iota_unused = nullptr;
+  void *scan_tmp, *free_tmp = nullptr;
   float* values = d_values;
   auto carve = [&](Arena& a) {
     slots = a.take<int32_t>(n);
     tidx = a.take<int64_t>(n);
     found = a.take<uint8_t>(n);
-    miss = a.take<int64_t>(n);
-    msrc = a.take<int64_t>(n);
-    flag = a.take<int64_t>(n + 1);
-    pos = a.take<int64_t>(n + 1);
+    flag2 = a.take<longlong2>(n + 1);
+    pos2 = a.take<longlong2>(n + 1);
     okeys = a.take<int64_t>(n);
     osrc = a.take<int64_t>(n);
+    sk = a.take<int64_t>(ssize);
+    smin = a.take<long long>(ssize);
+    counts = a.take<long long>(8);
+    scan_tmp = a.take<char>((int64_t)scan_bytes);
+    if (lru_lfu) {
+      ff = a.take<int64_t>(cap + 1);
+      fpos = a.take<int64_t>(cap + 1);
+      free_slots = a.take<int64_t>(cap + 1);
+      iota_unused = a.take<uint32_t>(cap);
+      mm = a.take<long long>(2);
+      free_tmp = a.take<char>((int64_t)free_bytes);
+    }
     if (!d_values) values = a.take<float>(n * dim);  // rows are still needed for the insert
   };
   {
     Arena probe;
     carve(probe);
     GF_TRY(sb.alloc(probe.off + 4096));
+    Arena A;
     A.base = sb.as<char>();
     carve(A);
   }
+  if (!c->hsmall) GF_CUDA(cudaMallocHost(&c->hsmall, 64));
   // cache.fetch(keys) (harness.py:438, cache.py:85-121): probe, score event, miss counting
   GF_LAUNCH(k_lookup, grid_for(n, 256, G), 256, 0, s, d_keys, n, c->hkeys, c->hslots, c->tsize - 1, slots, d_hit,
             c->counters);
@@ -1016,24 +1090,38 @@ gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, in
   GF_TRY(ftable_get_idx(t, d_keys, n, tidx, found, s));
   GF_TRY(fetch_gather(c, slots, t, tidx, n, values, s));
   if (c->policy == GF_CACHE_LRU) {
-    GF_LAUNCH(k_lru_decay, grid_for(c->capacity, 256, G), 256, 0, s, c->keys, c->scores, c->capacity);
+    GF_LAUNCH(k_lru_decay, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap);
     GF_LAUNCH(k_score_hits, grid_for(n, 256, G), 256, 0, s, slots, n, c->scores, 0);
   } else if (c->policy == GF_CACHE_LFU) {
     GF_LAUNCH(k_score_hits, grid_for(n, 256, G), 256, 0, s, slots, n, c->scores, 1);
   }
   GF_LAUNCH(k_count_misses, grid_for(n, 256, G), 256, 0, s, d_hit, (const int32_t*)nullptr, n, c->counters + 1);
-  int64_t nm = 0;
-  GF_TRY(dedupe_first(d_keys, n, slots, miss, msrc, nullptr, &nm, s));  // distinct misses, first-occurrence order
-  *h_n_miss = nm;
-  if (nm == 0) return GF_OK;
+  // free slots and the occupied score range, ahead of the placement (the fetch changes no key)
+  if (lru_lfu) {
+    GF_LAUNCH(k_mm_init, 1, 1, 0, s, mm);
+    GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, iota_unused, mm);
+    size_t fb = free_bytes;
+    GF_CUDA(cub::DeviceScan::ExclusiveSum(free_tmp, fb, ff, fpos, (int)(cap + 1), s));
+    GF_LAUNCH(k_free_scatter, grid_for(cap, 256, G), 256, 0, s, ff, fpos, cap, free_slots);
+  }
+  // distinct misses (first-occurrence order) and the found ones among them, in one scan
+  GF_CUDA(cudaMemsetAsync(sk, 0xff, (size_t)ssize * 8, s));    // EMPTY_KEY = -1
+  GF_CUDA(cudaMemsetAsync(smin, 0x7f, (size_t)ssize * 8, s));  // large
+  GF_LAUNCH(k_first_insert, grid_for(n, 256, G), 256, 0, s, d_keys, n, slots, sk, smin, ssize - 1);
+  GF_LAUNCH(k_ff_flags, grid_for(n, 256, G), 256, 0, s, d_keys, n, slots, sk, smin, ssize - 1, found, flag2);
+  size_t sbt = scan_bytes;
+  GF_CUDA(cub::DeviceScan::ExclusiveScan(scan_tmp, sbt, flag2, pos2, AddLL2(), make_longlong2(0, 0), (int)(n + 1), s));
+  GF_LAUNCH(k_ff_scatter, grid_for(n, 256, G), 256, 0, s, d_keys, n, flag2, pos2, okeys, osrc);
+  GF_LAUNCH(k_ff_counts, 1, 1, 0, s, pos2, n, fpos, cap, mm, counts);
+  GF_CUDA(cudaMemcpyAsync(c->hsmall, counts, 5 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  GF_CUDA(cudaStreamSynchronize(s));  // the block's one synchronisation
+  const long long* hc = c->hsmall;
+  *h_n_miss = hc[0];
+  const int64_t nf = hc[1];
+  if (nf == 0) return GF_OK;
   // insert_batch(miss[found], rows[found]) (harness.py:441): rows are read back from the output
-  GF_LAUNCH(k_unique_found, grid_for(nm, 256, G), 256, 0, s, msrc, found, nm, flag);
-  GF_TRY(cub_call([&](void* tt, size_t& b) { return cub::DeviceScan::ExclusiveSum(tt, b, flag, pos, (int)(nm + 1), s); }, s));
-  GF_LAUNCH(k_compact_found, grid_for(nm, 256, G), 256, 0, s, flag, pos, nm, miss, msrc, okeys, osrc);
-  int64_t nf = 0;
-  GF_CUDA(cudaMemcpyAsync(&nf, pos + nm, 8, cudaMemcpyDeviceToHost, s));
-  GF_CUDA(cudaStreamSynchronize(s));
-  return place_impl(c, okeys, osrc, nf, values, h_admitted, s);
+  FreeState pre{free_slots, hc[2], hc[3], hc[4]};
+  return place_impl(c, okeys, osrc, nf, values, h_admitted, s, &pre);
 }
 
 }  // extern "C"
