@@ -324,6 +324,8 @@ def bench_ours(args, cfg, world, rank, local):
 
     device = torch.device("cuda", local)
     R = cfg["roots"] if args.roots is None else args.roots
+    if args.strong:  # fixed total root count (R = 2^23 split over the ranks)
+        R = max(2, (args.strong // world) // 2 * 2)
     src, dst, ts = make_stream(cfg, device)
     torch.cuda.synchronize()
     g, ingest_ms = build_graph(cfg, src, dst, ts, world, rank, device)
@@ -459,7 +461,7 @@ def bench_ours(args, cfg, world, rank, local):
             "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None,
             "dtype": "int64",
             "data": "synthetic (reference generator law, drawn on device; seed 0)",
@@ -636,6 +638,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fetch", action="store_true")
+    ap.add_argument("--strong", type=int, default=0, metavar="TOTAL_ROOTS",
+                    help="strong scaling: TOTAL_ROOTS split over the ranks (default: 2^20 roots per rank, weak)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-chunk", type=int, default=16)
     args = ap.parse_args()
