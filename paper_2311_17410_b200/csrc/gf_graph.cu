@@ -7,9 +7,11 @@
 //   events (edge j, endpoint side) -> stable radix sort by node -> per-node
 //   segments -> chronology check (serial resolve only if a batch could reject)
 //   -> ids by scan -> per-segment block plan (capacity law with the live
-//   degree at allocation) -> new blocks sorted by the event that triggers them
-//   (= the reference's allocation order, so handles match) -> slot bases by
-//   scan in handle order -> metadata/directory/slot writes.
+//   degree at allocation) -> handles and slot bases by one scan over the events
+//   that trigger an allocation (= the reference's allocation order; handles
+//   freed by offload are reused LIFO first) -> metadata/directory/slot writes.
+// Nothing is read back mid-call (see add_edges_fast), and the launch sequence
+// is replayed as a CUDA graph.
 #include <cub/cub.cuh>
 
 #include <string.h>
@@ -44,6 +46,8 @@ struct IngestScalars {
   const int64_t *src, *dst, *ts, *eids_in;
   int64_t* out_eids;
   int64_t num_nodes, blk_used, slots_used, dir_used, next_edge_id, slots_free, dir_free;
+  const int64_t* free_list;  // handles freed by offload, reused LIFO (storage.py:171-181)
+  int64_t nfree;
 };
 
 template <class T>
@@ -57,65 +61,7 @@ gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
   return GF_OK;
 }
 
-__global__ void k_init_nodes(int64_t lo, int64_t hi, int64_t* head, int64_t* tail, int64_t* nb, int64_t* deg,
-                             uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap, uint8_t* nflags,
-                             int64_t* nrec) {
-  for (int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < hi; v += (int64_t)gridDim.x * blockDim.x) {
-    head[v] = GF_NO_BLOCK;
-    tail[v] = GF_NO_BLOCK;
-    nb[v] = 0;
-    deg[v] = 0;
-    valid[v] = 1;
-    nslots[v] = 0;
-    doff[v] = -1;
-    dcap[v] = 0;
-    nflags[v] = 0;
-    int64_t* r = nrec + v * NREC;
-    r[0] = -1;
-    r[1] = 0;
-    r[2] = NREC_VALID;
-    for (int w = 3; w < NREC; w++) r[w] = 0;
-  }
-}
 
-__global__ void k_minmax(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, const int64_t* __restrict__ ts,
-                         int64_t n, IngestCounters* c) {
-  long long mn = LLONG_MAX, mx = LLONG_MIN, tn = LLONG_MAX, tx = LLONG_MIN;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    long long a = src[i], b = dst[i], t = ts[i];
-    mn = min(mn, min(a, b));
-    mx = max(mx, max(a, b));
-    tn = min(tn, t);
-    tx = max(tx, t);
-  }
-  for (int o = 16; o; o >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    tn = min(tn, __shfl_xor_sync(0xffffffffu, tn, o));
-    tx = max(tx, __shfl_xor_sync(0xffffffffu, tx, o));
-  }
-  __shared__ long long sm[4][32];
-  const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sm[0][w] = mn;
-    sm[1][w] = mx;
-    sm[2][w] = tn;
-    sm[3][w] = tx;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // one set of atomics per block
-    for (int i = 1; i < nw; i++) {
-      mn = min(mn, sm[0][i]);
-      mx = max(mx, sm[1][i]);
-      tn = min(tn, sm[2][i]);
-      tx = max(tx, sm[3][i]);
-    }
-    atomicMin(&c->minv, mn);
-    atomicMax(&c->maxv, mx);
-    atomicMin(&c->tsmin, tn);
-    atomicMax(&c->tsmax, tx);
-  }
-}
 
 // one event per (edge, stored endpoint), in the reference's append order
 __global__ void k_make_events(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n, int directed,
@@ -166,62 +112,9 @@ __global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __
 }
 
 
-// chronology: accept everything, unless some stored endpoint may see a decreasing timestamp,
-// in which case per-node latest timestamps are prepared for the serial resolve
-__global__ void k_accept_prep(uint8_t* acc, int64_t n, int64_t* tm, int64_t num_nodes, const int64_t* tail,
-                              const int64_t* bsize, const int64_t* btmax, const IngestCounters* c, const IngestScalars* S) {
-  if (c->abort) return;
-  if (!c->viol) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
-    return;
-  }
-  if (S) num_nodes = S->num_nodes;
-  if (c->maxv + 1 > num_nodes) num_nodes = c->maxv + 1;  // nodes this batch creates have no tail
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < num_nodes; v += (int64_t)gridDim.x * blockDim.x)
-    tm[v] = node_tmax(tail, bsize, btmax, v);
-}
 
-// Sequential chronology resolve (storage.py:426-437): only when a batch may reject.
-__global__ void k_accept_serial(const int64_t* src, const int64_t* dst, const int64_t* ts, int64_t n, int directed,
-                                int64_t* tm, uint8_t* acc, const IngestCounters* c) {
-  if (!c->viol || c->abort || threadIdx.x || blockIdx.x) return;
-  for (int64_t j = 0; j < n; j++) {
-    int64_t s = src[j], d = dst[j], t = ts[j];
-    bool ok = t >= tm[s] && (directed || t >= tm[d]);
-    acc[j] = ok;
-    if (ok) {
-      tm[s] = t;
-      if (!directed) tm[d] = t;
-    }
-  }
-}
 
-__global__ void k_keep(const uint32_t* __restrict__ vals, int64_t E, int directed, const uint8_t* __restrict__ acc,
-                       int64_t* keep, const IngestCounters* c) {
-  if (c->abort) return;  // vals may be uninitialised (no events were made)
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x)
-    keep[i] = acc[ev_edge(vals[i], directed)];
-  if (blockIdx.x == 0 && threadIdx.x == 0) keep[E] = 0;
-}
 
-__global__ void k_eids(const uint8_t* __restrict__ acc, const int64_t* __restrict__ rank, int64_t n, int64_t next_id,
-                       const int64_t* __restrict__ eids_in, int64_t* out_eids, IngestCounters* c,
-                       const IngestScalars* S) {
-  if (S) next_id = S->next_edge_id;
-  long long mx = LLONG_MIN;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    int64_t e = -1;
-    if (acc[j]) {
-      e = eids_in ? eids_in[j] : next_id + rank[j];
-      mx = max(mx, (long long)e);
-    }
-    out_eids[j] = e;
-    if (S) S->out_eids[j] = e;
-    if (j == n - 1) c->n_acc = rank[j] + acc[j];
-  }
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0 && mx != LLONG_MIN) atomicMax(&c->max_eid, mx);
-}
 
 // compacted accepted events (segment-major, arrival order inside a segment)
 __global__ void k_compact(const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl, const int64_t* __restrict__ cpos,
@@ -256,11 +149,6 @@ struct SegPlan {
   longlong4* plan4;   // {new blocks, new slots, new directory capacity, 0} per segment, zero to E (scan input)
 };
 
-struct AddLL4 {
-  __device__ __forceinline__ longlong4 operator()(const longlong4& a, const longlong4& b) const {
-    return make_longlong4(a.x + b.x, a.y + b.y, a.z + b.z, 0);
-  }
-};
 
 __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                        const int64_t* __restrict__ cpos, const int64_t* __restrict__ ce_pend, int64_t E,
@@ -307,12 +195,6 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
   }
 }
 
-__global__ void k_totals(const longlong4* off4, int64_t E, IngestCounters* c) {
-  if (threadIdx.x || blockIdx.x || c->abort) return;
-  c->new_blocks = off4[E].x;
-  c->new_slots = off4[E].y;
-  c->dir_need = off4[E].z;
-}
 
 
 struct Recs {
@@ -321,78 +203,14 @@ struct Recs {
   int64_t* cap;     // capacity
   int32_t* seg;     // owning segment
   uint32_t* key;    // original event index of the first event = allocation order
-  uint32_t* idx;    // identity values for the sort
-  int64_t* handle;  // assigned handle
 };
 
-__global__ void k_enumerate(const int64_t* __restrict__ ce_pend, const uint32_t* __restrict__ ce_ev, const IngestCounters* c,
-                            const longlong4* __restrict__ off4, const int64_t* __restrict__ keys_node_of_seg_unused,
-                            SegPlan P, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
-                            const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R, longlong2* trig) {
-  if (c->abort) return;
-  int64_t nseg = c->num_segs;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
-    int64_t nb = P.nb_new[s];
-    if (!nb) continue;
-    int64_t v = keys[seg_start[s]];
-    int64_t cs = P.cstart[s], cnt = P.acc_cnt[s], fill = P.fill[s];
-    int64_t deg = degree[v] + fill, used = fill, rem = cnt - fill;
-    int64_t r = off4[s].x;
-    while (rem > 0) {
-      int64_t cap = sizing_cap(kind, tau, param, deg, ce_pend[cs + used]);
-      int64_t take = min(cap, rem);
-      R.first[r] = used;
-      R.count[r] = take;
-      R.cap[r] = cap;
-      R.seg[r] = (int32_t)s;
-      R.key[r] = ce_ev[cs + used];
-      R.idx[r] = (uint32_t)r;
-      if (trig) trig[ce_ev[cs + used]] = make_longlong2(1, cap);  // allocation order = triggering event order
-      r++;
-      deg += take;
-      used += take;
-      rem -= take;
-    }
-  }
-}
 
-// r-th allocation takes free_handles.pop() (LIFO, storage.py:172-173) while any are left, then fresh handles
-__global__ void k_assign_handles(const uint32_t* __restrict__ perm, int64_t nrec, int64_t blk_used, const int64_t* rcap,
-                                 const int64_t* __restrict__ freel, int64_t nfree, int64_t* handle, int64_t* cap_sorted) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t rec = perm[r];
-    handle[rec] = r < nfree ? freel[nfree - 1 - r] : blk_used + (r - nfree);
-    cap_sorted[r] = rcap[rec];
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) cap_sorted[nrec] = 0;
-}
 
 struct BlockArrays {
   int64_t *cap, *size, *tmin, *tmax, *prev, *next, *base;
 };
 
-__global__ void k_write_blocks(const uint32_t* __restrict__ perm, int64_t nrec, int64_t blk_used, int64_t slots_used,
-                               const int64_t* __restrict__ base_scan, Recs R, const longlong4* __restrict__ off4, SegPlan P,
-                               const uint32_t* __restrict__ ce_ev, const uint32_t* __restrict__ keys,
-                               const int64_t* __restrict__ seg_start, const int64_t* tail, const int64_t* __restrict__ ts,
-                               int directed, BlockArrays B) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrec; r += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t rec = perm[r];
-    int64_t h = R.handle[rec];
-    int32_t s = R.seg[rec];
-    int64_t k = rec - off4[s].x, nb = P.nb_new[s];
-    int64_t cs = P.cstart[s];
-    int64_t f = R.first[rec], cnt = R.count[rec];
-    B.cap[h] = R.cap[rec];
-    B.size[h] = cnt;
-    B.tmin[h] = ts[ev_edge(ce_ev[cs + f], directed)];
-    B.tmax[h] = ts[ev_edge(ce_ev[cs + f + cnt - 1], directed)];
-    B.base[h] = slots_used + base_scan[r];
-    int64_t v = keys[seg_start[s]];
-    B.prev[h] = (k == 0) ? tail[v] : R.handle[rec - 1];
-    B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : R.handle[rec + 1];
-  }
-}
 
 struct NodeArrays {
   int64_t *head, *tail, *num_blocks, *degree, *nslots, *dir_off, *dir_cap;
@@ -404,130 +222,9 @@ struct DirArrays {
   int64_t* e;  // DIRW words per entry
 };
 
-// one warp per segment: lane 0 updates the node and its tail block; the lanes copy a regrown
-// directory and append the new blocks' entries together (hub directories can be thousands long)
-__global__ void k_finalize(const IngestCounters* c, const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
-                           SegPlan P, const longlong4* __restrict__ off4, int64_t dir_used,
-                           Recs R, const uint32_t* __restrict__ ce_ev, const int64_t* __restrict__ ts, int directed,
-                           NodeArrays N, BlockArrays B, DirArrays D, int kind, const IngestScalars* S) {
-  if (c->abort) return;
-  if (S) dir_used = S->dir_used;
-  const int lane = threadIdx.x & 31;
-  const int64_t nseg = c->num_segs;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = warp; s < nseg; s += nwarps) {
-    const int64_t cnt = P.acc_cnt[s];
-    if (!cnt) continue;
-    const int64_t v = keys[seg_start[s]];
-    const int64_t t = N.tail[v], fill = P.fill[s], nb = P.nb_new[s], cs = P.cstart[s];
-    const int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v], deg_old = N.degree[v], oo = N.dir_off[v];
-    const int64_t dnew = P.plan4[s].z, r0 = off4[s].x;
-    const int64_t doff = dnew > 0 ? dir_used + off4[s].z : oo;
-    const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? ts[ev_edge(ce_ev[cs + fill - 1], directed)] : 0;
-    __syncwarp();
-    // block directory: grow (copy) if needed, then append the new blocks
-    if (nb > 0 && dnew > 0)
-      for (int64_t w = lane; w < nb_old * DIRW; w += 32) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
-    __syncwarp();
-    for (int64_t k = lane; k < nb; k += 32) {
-      const int64_t rec = r0 + k, h = R.handle[rec];
-      int64_t* e = D.e + (doff + nb_old + k) * DIRW;
-      e[0] = B.tmin[h];
-      e[1] = ns_old + R.first[rec];
-      e[2] = B.base[h];
-      e[3] = B.tmax[h];
-    }
-    if (lane == 0) {
-      // a block allocated while live degree != slots written (a deletion happened) or by
-      // batch sizing leaves the closed-form position -> block law (SizingLaw)
-      if (nb > 0 && (kind == GF_SIZING_BATCH || deg_old != ns_old)) N.nflags[v] |= 1;
-      if (t != GF_NO_BLOCK && fill > 0) {
-        B.size[t] = P.tail_size[s] + fill;
-        B.tmax[t] = t_tmax;
-        D.e[(doff + nb_old - 1) * DIRW + 3] = t_tmax;  // old tail grew
-      }
-      int64_t tl = t;
-      if (nb > 0) {
-        if (t == GF_NO_BLOCK) N.head[v] = R.handle[r0];
-        else B.next[t] = R.handle[r0];
-        tl = R.handle[r0 + nb - 1];
-        N.tail[v] = tl;
-        if (dnew > 0) {
-          N.dir_off[v] = doff;
-          N.dir_cap[v] = dnew;
-        }
-      }
-      const int64_t nbt = nb_old + nb;
-      N.num_blocks[v] = nbt;
-      N.degree[v] = deg_old + cnt;
-      N.nslots[v] = ns_old + cnt;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const int64_t nbt = nb_old + nb, tl = N.tail[v];
-      int64_t* r = N.nrec + v * NREC;
-      r[0] = doff;
-      r[1] = ns_old + cnt;
-      r[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
-      r[3] = D.e[doff * DIRW + 1];
-      r[4] = D.e[(doff + nbt - 1) * DIRW + 1];
-      r[5] = B.base[tl];
-      r[6] = B.tmin[tl];
-      r[7] = B.tmax[tl];
-      r[8] = D.e[doff * DIRW];
-    }
-  }
-}
 
 __global__ void k_noderec_invalidate(int64_t* nrec, int64_t v) { nrec[v * NREC + 2] &= ~NREC_VALID; }
 
-__global__ void k_scatter_slots(const IngestCounters* c, const int32_t* __restrict__ ce_seg, const uint32_t* __restrict__ ce_ev,
-                                const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start, SegPlan P,
-                                const longlong4* __restrict__ off4, Recs R, const int64_t* tail_before_unused,
-                                const int64_t* __restrict__ bbase, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
-                                const int64_t* __restrict__ ts, const int64_t* __restrict__ eids, int directed,
-                                const int64_t* __restrict__ old_tail, Slot* slots, int64_t* sts, int64_t* fts,
-                                int32_t* fts16) {
-  if (c->abort) return;
-  int64_t nacc_ev = 0;
-  {
-    int64_t nseg = c->num_segs;
-    nacc_ev = P.cstart[nseg - 1] + P.acc_cnt[nseg - 1];
-  }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nacc_ev; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t s = ce_seg[i];
-    int64_t r = i - P.cstart[s];
-    uint32_t ev = ce_ev[i];
-    int64_t j = ev_edge(ev, directed);
-    int side = directed ? 0 : (int)(ev & 1);
-    int64_t v = keys[seg_start[s]];
-    int64_t pos;
-    int64_t fill = P.fill[s];
-    if (r < fill) {
-      pos = bbase[old_tail[s]] + P.tail_size[s] + r;
-    } else {
-      int64_t lo = off4[s].x, hi = lo + P.nb_new[s];  // last rec with first <= r
-      while (hi - lo > 1) {
-        int64_t m = (lo + hi) >> 1;
-        if (R.first[m] <= r) lo = m;
-        else hi = m;
-      }
-      pos = bbase[R.handle[lo]] + (r - R.first[lo]);
-    }
-    Slot sl;
-    sl.ts = ts[j];
-    sl.eid = eids[j];
-    sl.nbr = (int32_t)(side ? src[j] : dst[j]);
-    sl.owner = (int32_t)v;
-    sl.valid = 1;
-    sl.pad = 0;
-    slots[pos] = sl;
-    sts[pos] = sl.ts;
-    if ((pos & (FENCE - 1)) == 0) fts[pos / FENCE] = sl.ts;
-    if ((pos & (FENCE16 - 1)) == 0) fts16[pos / FENCE16] = (int32_t)max(min(sl.ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);
-  }
-}
 
 
 template <class F>
@@ -546,31 +243,6 @@ int bits_for(int64_t n) {
   return b;
 }
 
-gf_status ensure_nodes(gf_graph* g, int64_t need, cudaStream_t s) {
-  if (need <= g->num_nodes) return GF_OK;
-  if (need > ((int64_t)1 << 31)) return fail(GF_EINVAL, "node ids must be < 2^31");
-  if (need > g->node_cap) {
-    g->gen++;
-    int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, g->node_cap * 2));
-    int64_t k = g->num_nodes;
-    GF_TRY(grow_array(g->head, k, nc, s));
-    GF_TRY(grow_array(g->tail, k, nc, s));
-    GF_TRY(grow_array(g->num_blocks, k, nc, s));
-    GF_TRY(grow_array(g->degree, k, nc, s));
-    GF_TRY(grow_array(g->node_valid, k, nc, s));
-    GF_TRY(grow_array(g->nslots, k, nc, s));
-    GF_TRY(grow_array(g->dir_off, k, nc, s));
-    GF_TRY(grow_array(g->dir_cap, k, nc, s));
-    GF_TRY(grow_array(g->nflags, k, nc, s));
-    GF_TRY(grow_array(g->nrec, k * NREC, nc * NREC, s));
-    g->node_cap = nc;
-  }
-  int64_t cnt = need - g->num_nodes;
-  GF_LAUNCH(k_init_nodes, grid_for(cnt, 256, 4096), 256, 0, s, g->num_nodes, need, g->head, g->tail, g->num_blocks,
-            g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
-  g->num_nodes = need;
-  return GF_OK;
-}
 
 gf_status ensure_blocks(gf_graph* g, int64_t need, cudaStream_t s) {
   if (need <= g->blk_cap) return GF_OK;
@@ -612,180 +284,6 @@ gf_status ensure_dir(gf_graph* g, int64_t need, cudaStream_t s) {
   return GF_OK;
 }
 
-gf_status add_edges_impl(gf_graph* g, const int64_t* src, const int64_t* dst, const int64_t* ts, int64_t n,
-                         const int64_t* eids_in, int64_t* out_eids, int64_t* h_rej, cudaStream_t s) {
-  if (h_rej) *h_rej = 0;
-  if (n == 0) return GF_OK;
-  if (n < 0 || n >= ((int64_t)1 << 30)) return fail(GF_EINVAL, "batch size must be in [0, 2^30)");
-  const int dir = g->directed;
-  const int64_t E = dir ? n : 2 * n;
-
-  Scratch cbuf(s);
-  GF_TRY(cbuf.alloc(sizeof(IngestCounters)));
-  IngestCounters* dc = cbuf.as<IngestCounters>();
-  IngestCounters hc;
-  memset(&hc, 0, sizeof(hc));
-  hc.minv = LLONG_MAX;
-  hc.maxv = LLONG_MIN;
-  hc.max_eid = LLONG_MIN;
-  hc.tsmin = LLONG_MAX;
-  hc.tsmax = LLONG_MIN;
-  GF_CUDA(cudaMemcpyAsync(dc, &hc, sizeof(hc), cudaMemcpyHostToDevice, s));
-  GF_LAUNCH(k_minmax, grid_for(n, 256, 2 * num_sms()), 256, 0, s, src, dst, ts, n, dc);
-  GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
-  GF_CUDA(cudaStreamSynchronize(s));
-  if (hc.minv < 0) return fail(GF_EINVAL, "node ids must be non-negative");  // storage.py:408-409
-  GF_TRY(ensure_nodes(g, hc.maxv + 1, s));                                  // storage.py:410-412
-
-  // ---- scratch: one carve sequence, run once to size the buffer and once to place it ----
-  uint32_t *keys_in, *keys, *vals_in, *vals, *ce_ev;
-  int32_t *heads, *incl, *ce_seg;
-  int64_t *seg_start, *rank, *tm, *keep, *cpos, *ce_pend, *old_tail;
-  uint8_t* acc;
-  longlong4* off4;
-  SegPlan P;
-  auto carve = [&](Arena& A) {
-    keys_in = A.take<uint32_t>(E);
-    keys = A.take<uint32_t>(E);
-    vals_in = A.take<uint32_t>(E);
-    vals = A.take<uint32_t>(E);
-    heads = A.take<int32_t>(E);
-    incl = A.take<int32_t>(E);
-    seg_start = A.take<int64_t>(E + 1);
-    acc = A.take<uint8_t>(n);
-    rank = A.take<int64_t>(n + 1);
-    tm = A.take<int64_t>(g->num_nodes);
-    keep = A.take<int64_t>(E + 1);
-    cpos = A.take<int64_t>(E + 1);
-    ce_ev = A.take<uint32_t>(E);
-    ce_pend = A.take<int64_t>(E);
-    ce_seg = A.take<int32_t>(E);
-    P.acc_cnt = A.take<int64_t>(E + 1);
-    P.cstart = A.take<int64_t>(E + 1);
-    P.fill = A.take<int64_t>(E + 1);
-    P.tail_size = A.take<int64_t>(E + 1);
-    P.nb_new = A.take<int64_t>(E + 1);
-    P.plan4 = A.take<longlong4>(E + 1);
-    off4 = A.take<longlong4>(E + 1);
-    old_tail = A.take<int64_t>(E + 1);
-  };
-  Scratch sb(s);
-  {
-    Arena probe;
-    carve(probe);
-    GF_TRY(sb.alloc(probe.off + 4096));
-    Arena A;
-    A.base = sb.as<char>();
-    carve(A);
-  }
-
-  const int T = 256;
-  const int64_t G = 8 * num_sms();
-  GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc, nullptr);
-  int endbit = bits_for(g->num_nodes);
-  GF_TRY(cub_call([&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s);
-  }, s));
-  GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
-  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, heads, incl, (int)E, s); }, s));
-  GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
-            seg_start, dc);
-  // chronology: accept all unless some stored endpoint sees a decreasing timestamp
-  GF_LAUNCH(k_accept_prep, grid_for(std::max(n, g->num_nodes), T, G), T, 0, s, acc, n, tm, g->num_nodes, g->tail,
-            g->bsize, g->btmax, dc, nullptr);
-  GF_LAUNCH(k_accept_serial, 1, 1, 0, s, src, dst, ts, n, dir, tm, acc, dc);
-  // edge ids by scan (storage.py:438-442)
-  GF_TRY(cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveSum(t, b, acc, rank, (int)n, s);
-  }, s));
-  GF_LAUNCH(k_eids, grid_for(n, T, G), T, 0, s, acc, rank, n, g->next_edge_id, eids_in, out_eids, dc, nullptr);
-  GF_LAUNCH(k_keep, grid_for(E, T, G), T, 0, s, vals, E, dir, acc, keep, dc);
-  GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, keep, cpos, (int)(E + 1), s); }, s));
-  GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
-  GF_LAUNCH(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize, g->bcap,
-            g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, old_tail);
-  GF_TRY(cub_call([&](void* t, size_t& b) {
-    return cub::DeviceScan::ExclusiveScan(t, b, P.plan4, off4, AddLL4(), make_longlong4(0, 0, 0, 0), (int)(E + 1), s);
-  }, s));
-  GF_LAUNCH(k_totals, 1, 1, 0, s, off4, E, dc);
-  GF_CUDA(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
-  GF_CUDA(cudaStreamSynchronize(s));
-
-  const int64_t nrec = hc.new_blocks;
-  // freed handles (offload) are reused first, LIFO (storage.py:171-181)
-  const int64_t nfree = (int64_t)g->free_handles.size();
-  const int64_t nfresh = std::max<int64_t>(0, nrec - nfree);
-  GF_TRY(ensure_blocks(g, g->blk_used + nfresh, s));
-  GF_TRY(ensure_slots(g, g->slots_used + hc.new_slots, s));
-  GF_TRY(ensure_dir(g, g->dir_used + hc.dir_need, s));
-
-  Scratch rb(s);
-  Arena RA;
-  {
-    Arena probe;
-    for (int q = 0; q < 3; q++) probe.take<int64_t>(nrec + 1);
-    probe.take<int32_t>(nrec); probe.take<uint32_t>(nrec); probe.take<uint32_t>(nrec); probe.take<uint32_t>(nrec);
-    probe.take<uint32_t>(nrec); probe.take<int64_t>(nrec + 1); probe.take<int64_t>(nrec + 1); probe.take<int64_t>(nrec + 1);
-    probe.take<int64_t>(nfree);
-    GF_TRY(rb.alloc(probe.off + 4096));
-  }
-  RA.base = rb.as<char>();
-  Recs R;
-  R.first = RA.take<int64_t>(nrec + 1);
-  R.count = RA.take<int64_t>(nrec + 1);
-  R.cap = RA.take<int64_t>(nrec + 1);
-  R.seg = RA.take<int32_t>(nrec);
-  R.key = RA.take<uint32_t>(nrec);
-  R.idx = RA.take<uint32_t>(nrec);
-  uint32_t* key_sorted = RA.take<uint32_t>(nrec);
-  uint32_t* perm = RA.take<uint32_t>(nrec);
-  R.handle = RA.take<int64_t>(nrec + 1);
-  int64_t* cap_sorted = RA.take<int64_t>(nrec + 1);
-  int64_t* base_scan = RA.take<int64_t>(nrec + 1);
-  int64_t* d_free = RA.take<int64_t>(nfree);
-  if (nfree && nrec) GF_CUDA(cudaMemcpyAsync(d_free, g->free_handles.data(), 8 * nfree, cudaMemcpyHostToDevice, s));
-
-  if (nrec > 0) {
-    GF_LAUNCH(k_enumerate, grid_for(E, T, G), T, 0, s, ce_pend, ce_ev, dc, off4, nullptr, P, keys, seg_start,
-              g->degree, g->sizing_kind, g->tau, g->sizing_param, R, nullptr);
-    int kb = bits_for(E + 1);
-    GF_TRY(cub_call([&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, R.key, key_sorted, R.idx, perm, (int)nrec, 0, kb, s);
-    }, s));
-    GF_LAUNCH(k_assign_handles, grid_for(nrec, T, G), T, 0, s, perm, nrec, g->blk_used, R.cap, d_free, nfree, R.handle,
-              cap_sorted);
-    GF_TRY(cub_call([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, cap_sorted, base_scan, (int)(nrec + 1), s);
-    }, s));
-    BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
-    GF_LAUNCH(k_write_blocks, grid_for(nrec, T, G), T, 0, s, perm, nrec, g->blk_used, g->slots_used, base_scan, R,
-              off4, P, ce_ev, keys, seg_start, g->tail, ts, dir, B);
-  }
-  if (hc.n_acc > 0) {
-    BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
-    NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid, g->nflags,
-                 g->nrec};
-    DirArrays D{g->dir};
-    GF_LAUNCH(k_finalize, grid_for(32 * E, T, G), T, 0, s, dc, keys, seg_start, P, off4, g->dir_used, R, ce_ev, ts,
-              dir, N, B, D, g->sizing_kind, nullptr);
-    GF_LAUNCH(k_scatter_slots, grid_for(E, T, G), T, 0, s, dc, ce_seg, ce_ev, keys, seg_start, P, off4, R, nullptr,
-              g->bbase, src, dst, ts, out_eids, dir, old_tail, g->slots, g->sts, g->fts, g->fts16);
-  }
-  g->blk_used += nfresh;
-  g->free_handles.resize(nfree - std::min(nfree, nrec));
-  g->slots_used += hc.new_slots;
-  g->dir_used += hc.dir_need;
-  if (eids_in) {
-    if (hc.n_acc > 0 && hc.max_eid + 1 > g->next_edge_id) g->next_edge_id = hc.max_eid + 1;
-  } else {
-    g->next_edge_id += hc.n_acc;
-  }
-  g->total_edges_inserted += hc.n_acc;
-  if (hc.tsmin < INT32_MIN || hc.tsmax > INT32_MAX) g->ts32 = 0;  // the 32-bit fence is no longer exact
-  if (h_rej) *h_rej = n - hc.n_acc;
-  GF_CUDA(cudaGetLastError());
-  return GF_OK;
-}
 
 // ---- sync-free ingest --------------------------------------------------------
 // The same plan as add_edges_impl, but every size the host needs is either bounded by the
@@ -1103,7 +601,10 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
                          int directed, const int64_t* __restrict__ old_tail, NodeArrays N, BlockArrays B, DirArrays D,
                          int kind, Slot* slots, int64_t* sts, int64_t* fts, int32_t* fts16) {
   if (c->abort) return;
-  const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used;
+  const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used, nfree = S->nfree;
+  const int64_t* __restrict__ freel = S->free_list;
+  // the r-th allocation of the batch takes free_handles.pop() while any are left, then a fresh handle
+  auto handle_of = [&](int64_t r) { return r < nfree ? freel[nfree - 1 - r] : blk_used + (r - nfree); };
   const int lane = threadIdx.x & 31;
   const int64_t nseg = c->num_segs;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1125,7 +626,7 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
     for (int64_t k = lane; k < nb; k += 32) {
       const int64_t r = r0 + k;
       const longlong2 tr = tscan[R.key[r]];
-      const int64_t h = blk_used + tr.x, base = slots_used + tr.y;
+      const int64_t h = handle_of(tr.x), base = slots_used + tr.y;
       const int64_t f = R.first[r], n_in = R.count[r];
       const int64_t tmin = ts[ev_edge(ce_ev[cs + f], directed)];
       const int64_t tmax = ts[ev_edge(ce_ev[cs + f + n_in - 1], directed)];
@@ -1134,8 +635,8 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
       B.tmin[h] = tmin;
       B.tmax[h] = tmax;
       B.base[h] = base;
-      B.prev[h] = (k == 0) ? t : blk_used + tscan[R.key[r - 1]].x;
-      B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : blk_used + tscan[R.key[r + 1]].x;
+      B.prev[h] = (k == 0) ? t : handle_of(tscan[R.key[r - 1]].x);
+      B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : handle_of(tscan[R.key[r + 1]].x);
       int64_t* e = D.e + (doff + nb_old + k) * DIRW;
       e[0] = tmin;
       e[1] = ns_old + f;
@@ -1155,7 +656,7 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
     tmin_last = __shfl_sync(0xffffffffu, tmin_last, src_lane);
     tmax_last = __shfl_sync(0xffffffffu, tmax_last, src_lane);
     base_last = __shfl_sync(0xffffffffu, base_last, src_lane);
-    const int64_t h_first = nb > 0 ? blk_used + tscan[R.key[r0]].x : GF_NO_BLOCK;
+    const int64_t h_first = nb > 0 ? handle_of(tscan[R.key[r0]].x) : GF_NO_BLOCK;
     __syncwarp();
     if (lane == 0) {
       // a block allocated while live degree != slots written (a deletion happened) or by
@@ -1275,6 +776,16 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
   static const bool no_graph = getenv("GF_INGEST_NO_GRAPH") != nullptr;
   const int T = 256;
   const int64_t G = 8 * num_sms();
+  // handles freed by offload: their device copy is read by the commit (outside the captured graph)
+  const int64_t nfree = (int64_t)g->free_handles.size();
+  if (nfree > g->free_dev_cap) {
+    if (g->free_dev) GF_CUDA(cudaFreeAsync(g->free_dev, s));
+    g->free_dev = nullptr;
+    g->free_dev_cap = 0;
+    GF_CUDA(cudaMallocAsync(&g->free_dev, sizeof(int64_t) * (size_t)(2 * nfree), s));
+    g->free_dev_cap = 2 * nfree;
+  }
+  if (nfree) GF_CUDA(cudaMemcpyAsync(g->free_dev, g->free_handles.data(), sizeof(int64_t) * nfree, cudaMemcpyHostToDevice, s));
   IngestCounters hc;
   const auto t_start = std::chrono::steady_clock::now();
   for (int attempt = 0;; attempt++) {
@@ -1310,8 +821,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       p[i++] = a.take<longlong4>(E + 1); p[i++] = a.take<longlong4>(E + 1);  // plan4, off4
       p[i++] = a.take<int64_t>(E + 1);  // old_tail
       for (int q = 0; q < 3; q++) p[i++] = a.take<int64_t>(E + 1);  // R.first/count/cap
-      p[i++] = a.take<int32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);  // R.seg/key/idx
-      p[i++] = a.take<int64_t>(E + 1);  // R.handle
+      p[i++] = a.take<int32_t>(E); p[i++] = a.take<uint32_t>(E);  // R.seg/key
       p[i++] = a.take<longlong2>(E); p[i++] = a.take<longlong2>(E);      // trig, tscan
       p[i++] = a.take<char>((int64_t)cub_bytes);
       p[i++] = a.take<int64_t>(tiles4 * 4); p[i++] = a.take<int64_t>(tiles4 * 4);  // plan scan agg/inc
@@ -1372,8 +882,6 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     R.cap = (int64_t*)P_[i++];
     R.seg = (int32_t*)P_[i++];
     R.key = (uint32_t*)P_[i++];
-    R.idx = (uint32_t*)P_[i++];
-    R.handle = (int64_t*)P_[i++];
     longlong2* trig = (longlong2*)P_[i++];
     longlong2* tscan = (longlong2*)P_[i++];
     void* cubtmp = P_[i++];
@@ -1389,7 +897,8 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
 
     // per-call values: read on the device through ds
     *hs = IngestScalars{src_in, dst_in, ts_in, eids_user, out_user, g->num_nodes, g->blk_used, g->slots_used,
-                        g->dir_used, g->next_edge_id, g->slot_cap - g->slots_used, g->dir_cap_total - g->dir_used};
+                        g->dir_used, g->next_edge_id, g->slot_cap - g->slots_used, g->dir_cap_total - g->dir_used,
+                        g->free_dev, nfree};
 
     // the launch sequence: identical for every call with the same key
     auto enqueue = [&](cudaStream_t s) -> gf_status {
@@ -1482,7 +991,9 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     }
   }
   if (hc.maxv + 1 > g->num_nodes) g->num_nodes = hc.maxv + 1;  // storage.py:410-412
-  g->blk_used += hc.new_blocks;
+  const int64_t nrec = hc.new_blocks;
+  g->blk_used += std::max<int64_t>(0, nrec - nfree);  // fresh handles only
+  g->free_handles.resize(nfree - std::min(nfree, nrec));
   g->slots_used += hc.new_slots;
   g->dir_used += hc.dir_need;
   if (eids_user) {
@@ -1547,6 +1058,7 @@ void free_graph(gf_graph* g) {
   if (g->ing_host) cudaFreeHost(g->ing_host);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   if (g->smp_buf) cudaFree(g->smp_buf);
+  if (g->free_dev) cudaFree(g->free_dev);
   if (g->smp_host) cudaFreeHost(g->smp_host);
 
 }
@@ -1614,11 +1126,7 @@ gf_status gf_graph_add_edges(gf_graph* g, const int64_t* d_src, const int64_t* d
   if (!g) return fail(GF_EINVAL, "graph is NULL");
   if (n > 0 && (!d_src || !d_dst || !d_ts || !d_out_eids)) return fail(GF_EINVAL, "NULL input array");
   DeviceGuard dg(g->device);
-  static const bool slow = getenv("GF_SLOW_INGEST") != nullptr;
-  // freed handles (offload) are reused LIFO by the sorted-allocation path
-  if (g->free_handles.empty() && !slow)
-    return add_edges_fast(g, d_src, d_dst, d_ts, n, d_eids_in, d_out_eids, h_out_rejected, (cudaStream_t)stream);
-  return add_edges_impl(g, d_src, d_dst, d_ts, n, d_eids_in, d_out_eids, h_out_rejected, (cudaStream_t)stream);
+  return add_edges_fast(g, d_src, d_dst, d_ts, n, d_eids_in, d_out_eids, h_out_rejected, (cudaStream_t)stream);
 }
 
 gf_status gf_graph_delete_edges(gf_graph* g, const int64_t* d_eids, int64_t n, int64_t* h_out_deleted, void* stream) {

@@ -61,6 +61,8 @@ struct gf_graph {
   void* ing_host = nullptr;   // pinned: per-call scalars (H2D) + counters (D2H)
   cudaGraphExec_t ing_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
+  int64_t* free_dev = nullptr;  // device copy of free_handles for the commit kernel
+  int64_t free_dev_cap = 0;
   int64_t ing_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   int64_t ing_nodes = 0;      // kernel launches per replay
   // persistent sampling scratch (totals, per-hop tile state, child keys) + pinned totals; a call
