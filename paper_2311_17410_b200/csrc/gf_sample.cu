@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
   for (int i = 0; i < k; i++) s_owner[w][pre + i] = (uint8_t)lane;
   if (k > 0) {
     const int64_t nv = hi - lo;
-    if (Q.policy == GF_POLICY_RECENT || k == nv) {
+    if (EARLY || Q.policy == GF_POLICY_RECENT || k == nv) {  // EARLY: launched for recent only
       // newest first: output r is list position hi-1-r (sampling.py:188-190)
       const int64_t inblk = hi - cum;
 #pragma unroll
