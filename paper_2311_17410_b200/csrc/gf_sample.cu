@@ -749,7 +749,6 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
   if (q < n) {
     const int64_t v = Q.src[q];
     te = Q.t_end[q];
-    qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
     if (v >= 0 && v < GV.num_nodes) {
       const int64_t* r = GV.nrec + v * NREC;
       int64_t w2, w3;
@@ -796,6 +795,9 @@ __global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_M
   // ---- selection into shared memory (independent of the output base) ----
   const int pre = incl - k;
   s_pre[w][lane] = pre;
+  // the query key feeds only the uniform draws and the child keys, so it is loaded here rather than
+  // held in a register through the search
+  if ((!EARLY || O.keys) && q < n) qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
   s_key[w][lane] = qkey;
   for (int i = 0; i < k; i++) s_owner[w][pre + i] = (uint8_t)lane;
   if (k > 0) {
