@@ -697,7 +697,13 @@ __device__ __forceinline__ void tile_publish(int k, int lane, int w, int32_t* s_
 #ifndef GF_FUSED_THREADS
 #define GF_FUSED_THREADS 256
 #endif
-constexpr int FT = GF_FUSED_THREADS;  // queries per tile = threads per CTA
+#ifndef GF_FUSED_THREADS_RECENT
+#define GF_FUSED_THREADS_RECENT 128
+#endif
+// queries per tile = threads per CTA, per policy (A/B: 128 is faster for the latency-bound recent
+// hops, 256 for the bandwidth-bound uniform hops)
+template <bool EARLY>
+constexpr int fused_threads() { return EARLY ? GF_FUSED_THREADS_RECENT : GF_FUSED_THREADS; }
 
 // EARLY: publish the tile aggregate before the in-block window search when every count is
 // already known (recent policy: long lists give k = fanout once the boundary block is found)
@@ -705,8 +711,10 @@ template <bool EARLY>
 #ifndef GF_FUSED_MINB_RECENT
 #define GF_FUSED_MINB_RECENT GF_FUSED_MINB
 #endif
-__global__ void __launch_bounds__(FT, (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_MINB) * 256 / FT)
+__global__ void __launch_bounds__(fused_threads<EARLY>(),
+                                  (EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_MINB) * 256 / fused_threads<EARLY>())
     k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
+  constexpr int FT = fused_threads<EARLY>();
   constexpr int NW = FT / 32;
   __shared__ uint32_t s_sel[NW][32][KMAX];
   __shared__ uint8_t s_owner[NW][32 * KMAX];
@@ -1115,7 +1123,10 @@ bool uses_fused(const gf_graph* g, int64_t fanout) {
   return !g->any_deleted && fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled();
 }
 
-int64_t tile_words(int64_t cap_q) { return (cap_q + FT - 1) / FT + 1; }  // status words + ticket
+int tile_threads(int policy) { return policy == GF_POLICY_RECENT ? fused_threads<true>() : fused_threads<false>(); }
+int64_t tile_words(int64_t cap_q, int policy) {  // status words + ticket
+  return (cap_q + tile_threads(policy) - 1) / tile_threads(policy) + 1;
+}
 
 // tile_state: (tiles + 1) zeroed words for the fused kernel, or NULL to allocate them here
 gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_offsets, const LayerOut& O, int64_t* total,
@@ -1124,7 +1135,8 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   const bool fast = !g->any_deleted;
   if (uses_fused(g, Q.fanout) && cap_q > 0) {
     // offsets[0] is written by tile 0, which always runs
-    const int64_t tiles = (cap_q + FT - 1) / FT;
+    const int ft = tile_threads(Q.policy);
+    const int64_t tiles = (cap_q + ft - 1) / ft;
     Scratch sb(s);
     if (!tile_state) {
       GF_TRY(sb.alloc(sizeof(uint64_t) * (tiles + 1)));
@@ -1132,8 +1144,8 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
       GF_CUDA(cudaMemsetAsync(tile_state, 0, sizeof(uint64_t) * (tiles + 1), s));
     }
     TileCtl C{tile_state, reinterpret_cast<unsigned long long*>(tile_state + tiles), total};
-    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, FT, 0, s, GV, Q, O, C);
-    else GF_LAUNCH(k_sample_fused<false>, tiles, FT, 0, s, GV, Q, O, C);
+    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, ft, 0, s, GV, Q, O, C);
+    else GF_LAUNCH(k_sample_fused<false>, tiles, ft, 0, s, GV, Q, O, C);
     return GF_OK;
   }
   GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
@@ -1217,7 +1229,7 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
     const int64_t cq = (h == 0) ? n_roots : h_caps[h - 1];
     if (uses_fused(g, h_fanouts[h]) && cq > 0) {
       tile_off[h] = zero_words;
-      zero_words += tile_words(cq);
+      zero_words += tile_words(cq, policy);
     }
   }
   const size_t bytes = sizeof(int64_t) * (size_t)zero_words + 256 + 2 * sizeof(uint64_t) * (size_t)key_cap + 512;
