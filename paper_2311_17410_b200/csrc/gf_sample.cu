@@ -670,6 +670,9 @@ __device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irreg
 #ifndef GF_GATHER_UNROLL
 #define GF_GATHER_UNROLL 2
 #endif
+#ifndef GF_GATHER_UNROLL_RECENT
+#define GF_GATHER_UNROLL_RECENT 2
+#endif
 
 // tile scan of the counts; thread 0 publishes the tile aggregate (tile 0: inclusive prefix)
 template <int NW>
@@ -716,6 +719,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
     k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
   constexpr int FT = fused_threads<EARLY>();
   constexpr int NW = FT / 32;
+  constexpr int GU = EARLY ? GF_GATHER_UNROLL_RECENT : GF_GATHER_UNROLL;  // record loads in flight per lane
   __shared__ uint32_t s_sel[NW][32][KMAX];
   __shared__ uint8_t s_owner[NW][32 * KMAX];
   __shared__ uint64_t s_key[NW][32];
@@ -887,16 +891,16 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   const int64_t out0 = base + wpre;
   __syncwarp();
   int e = lane;
-  for (; e + 32 * (GF_GATHER_UNROLL - 1) < total; e += 32 * GF_GATHER_UNROLL) {
-    Slot s[GF_GATHER_UNROLL];
-    int j[GF_GATHER_UNROLL];
+  for (; e + 32 * (GU - 1) < total; e += 32 * GU) {
+    Slot s[GU];
+    int j[GU];
 #pragma unroll
-    for (int u = 0; u < GF_GATHER_UNROLL; u++) {
+    for (int u = 0; u < GU; u++) {
       j[u] = s_owner[w][e + 32 * u];
       s[u] = GF_LOAD_OUT(GV.slots + s_sel[w][j[u]][e + 32 * u - s_pre[w][j[u]]]);
     }
 #pragma unroll
-    for (int u = 0; u < GF_GATHER_UNROLL; u++)
+    for (int u = 0; u < GU; u++)
       store_out(O, out0 + e + 32 * u, s[u], s_key[w][j[u]], e + 32 * u - s_pre[w][j[u]]);
   }
   for (; e < total; e += 32) {
