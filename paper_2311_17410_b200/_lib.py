@@ -132,11 +132,18 @@ def np_ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(ctypes.POINTER(ctype))
 
 
-def stream_ptr(stream=None) -> int:
+def stream_ptr(stream=None, device=None) -> int:
+    """Raw cudaStream_t of ``stream`` or of the current stream (of ``device``, default: current)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:  # fast path: no Stream object construction
+        idx = torch.cuda.current_device() if device is None else (device.index if device.index is not None
+                                                                   else torch.cuda.current_device())
+        return raw(idx)
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def launch_count() -> int:

@@ -215,6 +215,17 @@ def sample_khop(graph: DynamicGraph, request: SampleRequest, workers: int = 1, r
     return out if on_dev else out.to_host()
 
 
+_ARR_TYPES: dict[int, tuple] = {}
+
+
+def _arr_types(n: int):
+    """ctypes array types for n hops (cached: building them costs more than the C call's setup)."""
+    t = _ARR_TYPES.get(n)
+    if t is None:
+        t = _ARR_TYPES[n] = (ctypes.c_void_p * n, ctypes.c_int64 * n)
+    return t
+
+
 def sample_khop_device(graph: DynamicGraph, roots, tends, fanouts, policy: SamplingPolicy, seed: int = 0,
                        root_key_base: int = 0, stream=None) -> LayeredSample:
     """Fused multi-hop driver (gf_sample_khop) on CUDA tensors; one host sync per hop."""
@@ -241,8 +252,7 @@ def sample_khop_device(graph: DynamicGraph, roots, tends, fanouts, policy: Sampl
     flat = torch.empty(sum(sizes), dtype=torch.int64, device=dev)
     parts = list(torch.split(flat, sizes))
     nbr, eid, tss, offs = (parts[i * n_hops:(i + 1) * n_hops] for i in range(4))
-    VP = ctypes.c_void_p * n_hops
-    I64 = ctypes.c_int64 * n_hops
+    VP, I64 = _arr_types(n_hops)
     totals = I64()
     code, delta = _policy_args(policy)
     st = load().gf_sample_khop(graph.handle, ptr(roots), ptr(tends), int(roots.numel()), I64(*fanouts), n_hops, code,
