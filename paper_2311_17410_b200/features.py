@@ -180,6 +180,9 @@ def fetch_features(cache, table, keys, stream=None):
     n = int(k.numel())
     values = torch.empty((n, cache.dim), dtype=torch.float32, device=cache.device)
     hit = torch.empty(max(n, 1), dtype=torch.uint8, device=cache.device)
+    if stream is not None:  # the block's last kernels (the insert) still read values on that stream
+        for t in (k, values, hit):
+            t.record_stream(stream)
     nm, adm = ctypes.c_int64(), ctypes.c_int64()
     check(load().gf_fetch_features(cache.handle, table.handle, ptr(k), n, ptr(values), ptr(hit), ctypes.byref(nm),
                                    ctypes.byref(adm), stream_ptr(stream)))
