@@ -798,6 +798,9 @@ gf_status gf_cache_insert(gf_cache* c, const int64_t* d_keys, int64_t n, const f
 
 gf_status gf_cache_stats(gf_cache* c, int64_t* h_hits, int64_t* h_misses, int64_t* h_evictions) {
   if (!c) return fail(GF_EINVAL, "NULL argument");
+  DeviceGuard dg(c->device);
+  // the fetch block's insert is stream-ordered and may still be counting evictions on any stream
+  GF_CUDA(cudaDeviceSynchronize());
   long long v[4];
   GF_CUDA(cudaMemcpy(v, c->counters, sizeof(v), cudaMemcpyDeviceToHost));
   if (h_hits) *h_hits = v[0];
@@ -808,7 +811,10 @@ gf_status gf_cache_stats(gf_cache* c, int64_t* h_hits, int64_t* h_misses, int64_
 
 gf_status gf_cache_reset_stats(gf_cache* c) {
   if (!c) return fail(GF_EINVAL, "NULL argument");
+  DeviceGuard dg(c->device);
+  GF_CUDA(cudaDeviceSynchronize());
   GF_CUDA(cudaMemset(c->counters, 0, 8 * 4));
+  GF_CUDA(cudaDeviceSynchronize());
   return GF_OK;
 }
 
