@@ -239,3 +239,32 @@ def test_temporal_sampler_north_star_form(cuda_device):
             for x, y in zip((la.offsets, la.neighbors, la.edge_ids, la.timestamps),
                             (lb.offsets, lb.neighbors, lb.edge_ids, lb.timestamps)):
                 assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("fanouts", [[15, 10], [3, 5, 2]])
+def test_khop_time_window_and_wide_fanouts_vs_oracle(cuda_device, fanouts):
+    """Multi-hop time-window and uniform sampling (MAG-style [15, 10], three hops) bit-exact vs the oracle."""
+    import torch
+
+    import paper_2311_17410_b200 as gf
+    from oracle import OracleGraph
+
+    src, dst, ts = gf.generate_synthetic_arrays(3000, 120_000, 2.2, 120, seed=9, src_skew=2.2)  # MAG-like ties
+    g = gf.DynamicGraph(directed=True, tau=8192)
+    o = OracleGraph(True, 8192)
+    for lo in range(0, len(src), 40_000):
+        g.add_edges_arrays(src[lo:lo + 40_000], dst[lo:lo + 40_000], ts[lo:lo + 40_000])
+        o.add_edges(src[lo:lo + 40_000], dst[lo:lo + 40_000], ts[lo:lo + 40_000])
+    rng = np.random.default_rng(3)
+    pick = rng.integers(0, len(src), 2000)
+    roots = np.concatenate([src[pick], dst[pick]])
+    rts = np.concatenate([ts[pick], ts[pick] + 1])
+    for policy, delta in (("uniform", 0), ("time_window", 30)):
+        req = gf.SampleRequest(torch.from_numpy(roots).cuda(), torch.from_numpy(rts).cuda(), fanouts,
+                               gf.SamplingPolicy(policy, delta), seed=11)
+        got = gf.sample_khop(g, req)
+        ref = o.sample_khop(roots, rts, fanouts, policy, delta=delta, seed=11)
+        assert len(got.layers) == len(ref)
+        for lay, r in zip(got.layers, ref):
+            for a, w in zip((lay.offsets, lay.neighbors, lay.edge_ids, lay.timestamps), (r[2], r[3], r[4], r[5])):
+                np.testing.assert_array_equal(a.cpu().numpy(), w)
