@@ -41,10 +41,14 @@ CONFIGS = {
     # name: nodes, edges, directed, tau, skew, src_skew, span, roots per GPU
     "gdelt": dict(nodes=17_000, edges=191_000_000, directed=True, tau=8192, skew=2.2, src_skew=2.2, span=175_200,
                   roots=1 << 20, label="GDELT-shaped TGN 2-hop f10 (17K nodes, 191M edges, directed, tau 8192)"),
+    # configs[1]: TGAT uniform [10, 10]; roots = 2 x 600 per minibatch in the paper, 2^16 here to fill the GPU
     "reddit": dict(nodes=11_000, edges=672_000, directed=False, tau=48, skew=2.2, src_skew=None, span=2_592_000,
-                   roots=1 << 16, label="REDDIT-shaped TGAT 2-hop f10 (11K nodes, 672K edges, undirected, tau 48)"),
+                   roots=1 << 16, policies=("uniform",),
+                   label="REDDIT-shaped TGAT 2-hop f10 uniform (11K nodes, 672K edges, undirected, tau 48)"),
+    # configs[0]: TGN recent [10] (the reference's CPU case); 8,000 roots = one 4,000-edge minibatch
     "wiki": dict(nodes=9_000, edges=157_000, directed=False, tau=48, skew=2.2, src_skew=None, span=2_592_000,
-                 roots=8_000, label="WIKI-shaped (9K nodes, 157K edges, undirected, tau 48)"),
+                 roots=8_000, fanouts=[10], policies=("recent",),
+                 label="WIKI-shaped TGN 1-hop f10 recent (9K nodes, 157K edges, undirected, tau 48)"),
     # configs[4] at one GPU's share of the 8-way partition (owner = v % 8): 1/8 of the nodes and
     # edges of the MAG shape, GraphSAGE-temporal uniform [15, 10], 10M-edge ingest batches
     "mag8": dict(nodes=15_250_000, edges=162_500_000, directed=True, tau=8192, skew=2.2, src_skew=2.2, span=120,
