@@ -11,24 +11,22 @@
 //      t_end the boundary is in the tail block (the common case for recent
 //      roots), else an interpolation/bisection search over the node's block
 //      directory (32-byte entries, one 256-bit load per probe);
-//   2. the same search over the block's fence index (every 32nd timestamp,
-//      L2-sized);
-//   3. one 32-timestamp window of the dense ts array (eight 256-bit loads).
+//   2. the same search over the block's fence index (32-bit fences every 16
+//      slots while every timestamp fits int32, else int64 fences every 32);
+//   3. one 16- (or 32-) timestamp window of the dense ts array.
 // Selection:
 //   recent:     the k newest valid candidates, newest first (sampling.py:188-190) -- bit-exact.
 //   uniform/tw: k distinct candidates by Floyd's algorithm on a Philox4x32-10 stream
 //               keyed by (hop seed, query key); positions map to slots by the
 //               sizing law's closed form (or the directory for irregular lists).
-// Output (K3): a count pass, a device scan, and a write pass; hop totals stay
-// on the device so a k-hop call is a fixed launch sequence with one host
-// synchronisation at the end.
+// Output (K3): fast path -- one fused kernel per hop (k_sample_fused: search,
+// tile scan with decoupled look-back, selection, cooperative gather/store);
+// hop totals stay on the device, so a k-hop call is k launches and one host
+// synchronisation.  The unfused count -> scan -> write kernels remain for
+// fanout > 16 and for A/B (GF_NO_FUSED).
 //
-// Fast path (no deletions ever applied): the window search runs one query per
-// lane (32 in flight per warp; interpolation on timestamps keeps the chain of
-// dependent loads short); the write pass selects per lane and moves the
-// selected slots warp-cooperatively (coalesced stores).  General path (after
-// deletions): one warp per query, scanning candidate validity (valid edge and
-// valid neighbour, sampling.py:178).
+// General path (after deletions): one warp per query, scanning candidate
+// validity (valid edge and valid neighbour, sampling.py:178).
 #include <cub/cub.cuh>
 
 #include <string.h>
