@@ -9,7 +9,9 @@
 //
 // key -> slot map: open addressing (linear probing, splitmix64 hash) over a
 // power-of-two table >= 2x capacity, rebuilt from keys[] after every insert.
-// Rows are stored with a 16-byte aligned pitch so K6 moves them as int4.
+// Rows are stored with a 16-byte aligned pitch so K6 moves them with 128-bit loads, staged in
+// shared memory for packed outputs of any width.  The fetch block copies each output row once
+// (hits from the cache, misses from the table) and synchronises with the host once.
 #include <cub/cub.cuh>
 
 #include <algorithm>

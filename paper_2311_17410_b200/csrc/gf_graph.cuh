@@ -13,6 +13,8 @@
 //   sts        (int64 per slot)                dense copy of the slot timestamps (window reads)
 //   fts        (int64 per 32 slots)            fence index: fts[i] = ts of pool slot 32*i, a sorted
 //                                              subsequence of every block's timestamps (L2-sized)
+//   fts16      (int32 per 16 slots)            32-bit fence, exact while every timestamp fits int32
+//                                              (ts32); leaves one-line (128 B) windows
 //   nflags     (u8 per node)                   bit 0: block list not on the sizing law's closed form
 #pragma once
 
