@@ -504,7 +504,7 @@ FETCH_MINIBATCH = 4000      # TGN minibatch edges -> 8,000 roots (harness.py:424
 FETCH_EDGE_TABLE = 5_000_000  # edge features held for the latest 5M edges (142 GB for all 191M)
 
 
-def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 20) -> dict:
+def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50) -> dict:
     """Feature-cache fetch block (harness.py:432-446) on GPU: per minibatch of the latest edges,
     2-hop recent f10 sample, then node keys = roots + last-layer neighbours through an LRU node cache
     (d_v 413) and edge keys = every layer's edge ids through an LRU edge cache (d_e 186); misses

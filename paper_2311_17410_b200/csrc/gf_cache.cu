@@ -494,9 +494,11 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
       int bits = 1;
       while (bits < 64 && ((unsigned long long)(hi - lo) >> bits) != 0) bits++;
       GF_LAUNCH(k_score_keys, grid_for(cap, 256, G), 256, 0, s, c->scores, cap, (int64_t)lo, skeys);
+      cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
       GF_TRY(cub_call([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, skeys, skeys_sorted, iota, sorted_slots, (int)cap, 0, bits, s);
       }, s));
+      if (e0) prof_stop("cub_victim_sort", s, e0);
       GF_LAUNCH(k_victims, grid_for(r, 256, G), 256, 0, s, sorted_slots, r, aslot);
       GF_LAUNCH(k_place, grid_for(r, 256, G), 256, 0, s, ukeys + nfill, usrc + nfill, aslot, r, c->keys, c->scores,
                 new_score, c->counters + 2, 1);
