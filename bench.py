@@ -537,6 +537,11 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50) -> dict:
         nkeys = torch.cat([roots, smp.layers[-1].neighbors]).contiguous()
         ekeys = torch.cat([lay.edge_ids for lay in smp.layers]).contiguous()
         mb.append((nkeys, ekeys))
+    # reserve the largest output blocks once, so the caching allocator never grows inside the timed loop
+    mx_n, mx_e = max(int(nk.numel()) for nk, _ in mb), max(int(ek.numel()) for _, ek in mb)
+    held = [torch.empty((mx_n, FETCH_DV), dtype=torch.float32, device=device),
+            torch.empty((mx_e, FETCH_DE), dtype=torch.float32, device=device)]
+    del held
     for nk, ek in mb[:2]:  # warm-up
         gf.fetch_features(ncache, ntab, nk)
         gf.fetch_features(ecache, etab, ek)
