@@ -970,7 +970,8 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     const auto t_enq = std::chrono::steady_clock::now();
     GF_CUDA(cudaStreamSynchronize(s));
     hc = *hcp;
-    if (getenv("GF_INGEST_TIMING")) {
+    static const bool timing = getenv("GF_INGEST_TIMING") != nullptr;
+    if (timing) {
       static double enq = 0, tot = 0;
       static int calls = 0;
       const auto t_end = std::chrono::steady_clock::now();
