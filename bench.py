@@ -149,6 +149,21 @@ class ClockSampler:
                 "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
+def self_launch(args) -> int | None:
+    """--gpus N > 1 without a torchrun environment: re-run this command under torch.distributed.run
+    with N ranks on 127.0.0.1 (one process per GPU) and return its exit code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=dict(os.environ)).returncode
+
+
 def dist_setup(args):
     import torch
 
@@ -158,8 +173,18 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
 
+        if args.gpus not in (1, world) and rank == 0:
+            print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} ranks", file=sys.stderr)
+        # the NCCL communicator-init lines (rank count, NVLink/NVLS transport) go to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one tiny collective so the communicator (and its INIT log) exists before any timing
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)
+        if rank == 0:
+            print(f"bench: NCCL communicator up, {int(t.item())} ranks", file=sys.stderr, flush=True)
     else:
         if torch.cuda.is_available():
             torch.cuda.set_device(0)
@@ -655,6 +680,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-chunk", type=int, default=16)
     args = ap.parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
     cfg = CONFIGS[args.config]
     global FANOUTS, POLICIES, INGEST_BATCH
     FANOUTS = list(cfg.get("fanouts", FANOUTS))

@@ -171,7 +171,7 @@ gf_status gf_cache_destroy(gf_cache* c);
 /* VectorCache.fetch (cache.py:85-121).  d_values [n x dim] fp32 row-major
  * (zeros for misses), d_hit[n] (0/1), d_miss_keys (capacity n) receives the
  * missed keys deduplicated in first-occurrence order; *h_n_miss their count
- * (synchronous).  d_hit_slots (optional, n entries): cache slot per key or -1. */
+ * (synchronous). */
 gf_status gf_cache_fetch(gf_cache* c, const int64_t* d_keys, int64_t n, float* d_values, uint8_t* d_hit,
                          int64_t* d_miss_keys, int64_t* h_n_miss, void* stream);
 /* VectorCache.insert_batch (cache.py:123-177).  d_values [n x dim].
@@ -213,8 +213,14 @@ gf_status gf_ftable_size(gf_ftable* t, int64_t* h_n);
 gf_status gf_ftable_ids(gf_ftable* t, int64_t* d_ids, int64_t cap, int64_t* h_n, void* stream);
 
 /* Harness fetch block (harness.py:438-446): cache.fetch(keys) -> table.get(miss)
- * -> cache.insert_batch(found rows).  d_values [n x dim] receives cached rows
- * (zeros on miss, as VectorCache.fetch returns).  Counts are host outputs. */
+ * -> cache.insert_batch(found rows), one call.  d_values [n x dim] receives the
+ * COMPLETE row of every key: the cached row for a hit, the table row for a miss
+ * whose id the table holds, zeros for an id the table does not hold (the
+ * reference harness discards fetch's values, harness.py:438,443, so the block
+ * returns the rows a trainer would consume).  d_hit[n] is the cache hit mask.
+ * *h_n_miss = distinct missed keys, *h_admitted = rows the insert admitted.
+ * Returns with the insert still queued on `stream`: readers of the cache state
+ * on other streams synchronise (gf_cache_stats / get_state / snapshot do). */
 gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, int64_t n, float* d_values,
                             uint8_t* d_hit, int64_t* h_n_miss, int64_t* h_admitted, void* stream);
 

@@ -101,7 +101,7 @@ class VectorCache:
         storage = np.zeros((self.capacity, self.dim), np.float32)
         head = ctypes.c_int64(0)
         check(load().gf_cache_get_state(self._h, _lib.np_ptr(keys, ctypes.c_int64), _lib.np_ptr(scores, ctypes.c_int64),
-                                        _lib.np_ptr(storage, ctypes.c_float), ctypes.byref(head), stream_ptr()))
+                                        _lib.np_ptr(storage, ctypes.c_float), ctypes.byref(head), stream_ptr(device=self.device)))
         return keys, scores, storage, int(head.value)
 
     def _set_state(self, keys=None, scores=None, storage=None, fifo_head=None):
@@ -111,7 +111,7 @@ class VectorCache:
         head = self.fifo_head if fifo_head is None else int(fifo_head)
         check(load().gf_cache_set_state(self._h, None if k is None else _lib.np_ptr(k, ctypes.c_int64),
                                         None if s is None else _lib.np_ptr(s, ctypes.c_int64),
-                                        None if r is None else _lib.np_ptr(r, ctypes.c_float), head, stream_ptr()))
+                                        None if r is None else _lib.np_ptr(r, ctypes.c_float), head, stream_ptr(device=self.device)))
 
     @property
     def keys(self) -> np.ndarray:
@@ -134,7 +134,7 @@ class VectorCache:
     @property
     def fifo_head(self) -> int:
         head = ctypes.c_int64(0)
-        check(load().gf_cache_get_state(self._h, None, None, None, ctypes.byref(head), stream_ptr()))
+        check(load().gf_cache_get_state(self._h, None, None, None, ctypes.byref(head), stream_ptr(device=self.device)))
         return int(head.value)
 
     @property
@@ -155,7 +155,7 @@ class VectorCache:
         miss = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
         nm = ctypes.c_int64(0)
         check(load().gf_cache_fetch(self._h, ptr(keys), n, ptr(values), ptr(hit), ptr(miss), ctypes.byref(nm),
-                                    stream_ptr(stream)))
+                                    stream_ptr(stream, self.device)))
         return values, hit.bool(), miss[: int(nm.value)]
 
     def fetch(self, keys):
@@ -190,7 +190,7 @@ class VectorCache:
             k = torch.from_numpy(kn).to(self.device)
             v = torch.from_numpy(vn.reshape(len(kn), self.dim)).to(self.device)
         adm = ctypes.c_int64(0)
-        check(load().gf_cache_insert(self._h, ptr(k), int(k.numel()), ptr(v), ctypes.byref(adm), stream_ptr()))
+        check(load().gf_cache_insert(self._h, ptr(k), int(k.numel()), ptr(v), ctypes.byref(adm), stream_ptr(device=self.device)))
         return int(adm.value)
 
     # -- snapshot / persistence (cache.py:181-233) --------------------------------------
@@ -232,14 +232,14 @@ class VectorCache:
 class DeviceCacheSnapshot:
     def __init__(self, cache: VectorCache):
         h = ctypes.c_void_p()
-        check(load().gf_cache_snapshot(cache.handle, ctypes.byref(h), stream_ptr()))
+        check(load().gf_cache_snapshot(cache.handle, ctypes.byref(h), stream_ptr(device=cache.device)))
         self._h = h
         self.shape = (cache.policy, cache.capacity, cache.dim)
 
     def restore_into(self, cache: VectorCache) -> None:
         if self.shape != (cache.policy, cache.capacity, cache.dim):
             raise SnapshotMismatchError("snapshot shape does not match the cache")
-        check(load().gf_cache_restore(cache.handle, self._h, stream_ptr()))
+        check(load().gf_cache_restore(cache.handle, self._h, stream_ptr(device=cache.device)))
 
     def __del__(self):
         h = getattr(self, "_h", None)

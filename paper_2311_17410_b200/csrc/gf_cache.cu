@@ -771,6 +771,7 @@ gf_status gf_cache_create(int policy, int64_t capacity, int64_t dim, double lam,
 
 gf_status gf_cache_destroy(gf_cache* c) {
   if (!c) return GF_OK;
+  DeviceGuard dg(c->device);
   cudaFree(c->keys);
   cudaFree(c->scores);
   cudaFree(c->storage);
@@ -786,6 +787,7 @@ gf_status gf_cache_fetch(gf_cache* c, const int64_t* d_keys, int64_t n, float* d
                          int64_t* h_n_miss, void* stream) {
   if (!c || !h_n_miss) return fail(GF_EINVAL, "NULL argument");
   if (n > 0 && (!d_keys || !d_hit || !d_miss_keys)) return fail(GF_EINVAL, "NULL array");
+  DeviceGuard dg(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   GF_TRY(fetch_impl(c, d_keys, n, d_values, d_hit, d_miss_keys, h_n_miss, nullptr, s));
   if (n > 0)
@@ -797,6 +799,7 @@ gf_status gf_cache_insert(gf_cache* c, const int64_t* d_keys, int64_t n, const f
                           void* stream) {
   if (!c || !h_admitted) return fail(GF_EINVAL, "NULL argument");
   if (n > 0 && (!d_keys || !d_values)) return fail(GF_EINVAL, "NULL array");
+  DeviceGuard dg(c->device);
   return insert_impl(c, d_keys, n, d_values, h_admitted, (cudaStream_t)stream);
 }
 
@@ -825,6 +828,10 @@ gf_status gf_cache_reset_stats(gf_cache* c) {
 gf_status gf_cache_get_state(gf_cache* c, int64_t* h_keys, int64_t* h_scores, float* h_storage, int64_t* h_fifo_head,
                              void* stream) {
   if (!c) return fail(GF_EINVAL, "NULL argument");
+  DeviceGuard dg(c->device);
+  // gf_fetch_features returns with its insert still queued on the caller's stream: order
+  // against every stream, as gf_cache_stats does
+  GF_CUDA(cudaDeviceSynchronize());
   cudaStream_t s = (cudaStream_t)stream;
   if (h_keys) GF_CUDA(cudaMemcpyAsync(h_keys, c->keys, 8 * c->capacity, cudaMemcpyDeviceToHost, s));
   if (h_scores) GF_CUDA(cudaMemcpyAsync(h_scores, c->scores, 8 * c->capacity, cudaMemcpyDeviceToHost, s));
@@ -839,13 +846,15 @@ gf_status gf_cache_get_state(gf_cache* c, int64_t* h_keys, int64_t* h_scores, fl
 gf_status gf_cache_set_state(gf_cache* c, const int64_t* h_keys, const int64_t* h_scores, const float* h_storage,
                              int64_t fifo_head, void* stream) {
   if (!c) return fail(GF_EINVAL, "NULL argument");
+  if (fifo_head < 0 || fifo_head >= c->capacity) return fail(GF_EINVAL, "bad fifo head");  // before any copy
+  DeviceGuard dg(c->device);
+  GF_CUDA(cudaDeviceSynchronize());
   cudaStream_t s = (cudaStream_t)stream;
   if (h_keys) GF_CUDA(cudaMemcpyAsync(c->keys, h_keys, 8 * c->capacity, cudaMemcpyHostToDevice, s));
   if (h_scores) GF_CUDA(cudaMemcpyAsync(c->scores, h_scores, 8 * c->capacity, cudaMemcpyHostToDevice, s));
   if (h_storage && c->dim > 0)
     GF_CUDA(cudaMemcpy2DAsync(c->storage, 4 * c->pitch, h_storage, 4 * c->dim, 4 * c->dim, c->capacity,
                               cudaMemcpyHostToDevice, s));
-  if (fifo_head < 0) return fail(GF_EINVAL, "bad fifo head");
   c->fifo_head = fifo_head;
   GF_TRY(rebuild_map(c, s));
   GF_CUDA(cudaStreamSynchronize(s));
@@ -854,6 +863,8 @@ gf_status gf_cache_set_state(gf_cache* c, const int64_t* h_keys, const int64_t* 
 
 gf_status gf_cache_snapshot(gf_cache* c, gf_cache_snap** out, void* stream) {
   if (!c || !out) return fail(GF_EINVAL, "NULL argument");
+  DeviceGuard dg(c->device);
+  GF_CUDA(cudaDeviceSynchronize());
   cudaStream_t s = (cudaStream_t)stream;
   gf_cache_snap* p = new gf_cache_snap();
   p->policy = c->policy;
@@ -879,6 +890,8 @@ gf_status gf_cache_restore(gf_cache* c, const gf_cache_snap* p, void* stream) {
   if (!c || !p) return fail(GF_EINVAL, "NULL argument");
   if (p->policy != c->policy || p->capacity != c->capacity || p->dim != c->dim)  // cache.py:194-198
     return fail(GF_EINVAL, "snapshot shape does not match the cache");
+  DeviceGuard dg(c->device);
+  GF_CUDA(cudaDeviceSynchronize());
   cudaStream_t s = (cudaStream_t)stream;
   size_t rows = 4 * (size_t)std::max<int64_t>(1, c->capacity * c->pitch);
   GF_CUDA(cudaMemcpyAsync(c->keys, p->keys, 8 * c->capacity, cudaMemcpyDeviceToDevice, s));
@@ -914,6 +927,7 @@ gf_status gf_ftable_create(int kind, int64_t dim, int device, gf_ftable** out) {
 
 gf_status gf_ftable_destroy(gf_ftable* t) {
   if (!t) return GF_OK;
+  DeviceGuard dg(t->device);
   cudaFree(t->rows);
   cudaFree(t->present);
   cudaFree(t->ids);
@@ -956,6 +970,7 @@ gf_status gf_ftable_ids(gf_ftable* t, int64_t* d_ids, int64_t cap, int64_t* h_n,
 gf_status gf_ftable_put(gf_ftable* t, const int64_t* d_ids, int64_t n, const float* d_rows, void* stream) {
   if (!t) return fail(GF_EINVAL, "NULL argument");
   if (n == 0) return GF_OK;
+  DeviceGuard dg(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t G = 8 * num_sms();
   Scratch sb(s);
@@ -1017,6 +1032,7 @@ gf_status gf_ftable_put(gf_ftable* t, const int64_t* d_ids, int64_t n, const flo
 gf_status gf_ftable_get(gf_ftable* t, const int64_t* d_ids, int64_t n, float* d_rows, uint8_t* d_found, void* stream) {
   if (!t) return fail(GF_EINVAL, "NULL argument");
   if (n == 0) return GF_OK;
+  DeviceGuard dg(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   Scratch sb(s);
   GF_TRY(sb.alloc((size_t)n * 8));

@@ -31,6 +31,14 @@ def world() -> tuple[int, int]:
     return dist.get_world_size(), dist.get_rank()
 
 
+def _coll_device(dev):
+    """Device for collective buffers: the data's device under NCCL, the host under gloo (whose
+    collectives run on CPU tensors; the CPU tests and 2-ranks-on-one-GPU tests use it)."""
+    import torch
+
+    return dev if _dist().get_backend() == "nccl" else torch.device("cpu")
+
+
 def exclusive_prefix(count: int, device=None) -> tuple[int, int]:
     """(sum of counts on lower ranks, global total) for this rank's count."""
     import torch
@@ -39,7 +47,7 @@ def exclusive_prefix(count: int, device=None) -> tuple[int, int]:
     if n == 1:
         return 0, int(count)
     dist = _dist()
-    t = torch.tensor([int(count)], dtype=torch.int64, device=device)
+    t = torch.tensor([int(count)], dtype=torch.int64, device=_coll_device(device or torch.device("cpu")))
     allc = [torch.zeros_like(t) for _ in range(n)]
     dist.all_gather(allc, t)
     vals = [int(x.item()) for x in allc]
@@ -58,8 +66,9 @@ def gather_edge_batch(src, dst, ts):
     if n == 1:
         return src, dst, ts
     dist = _dist()
-    dev = src.device
-    local = torch.stack([src.to(torch.int64), dst.to(torch.int64), ts.to(torch.int64)])  # [3, m]
+    out_dev = src.device
+    dev = _coll_device(out_dev)
+    local = torch.stack([src.to(dev, torch.int64), dst.to(dev, torch.int64), ts.to(dev, torch.int64)])  # [3, m]
     m = torch.tensor([local.shape[1]], dtype=torch.int64, device=dev)
     lens = [torch.zeros_like(m) for _ in range(n)]
     dist.all_gather(lens, m)
@@ -75,7 +84,7 @@ def gather_edge_batch(src, dst, ts):
         dist.all_gather(parts, pad)
         full = torch.stack(parts)
     cols = [full[i, :, : lens[i]] for i in range(n)]
-    batch = torch.cat(cols, dim=1)
+    batch = torch.cat(cols, dim=1).to(out_dev)
     return batch[0].contiguous(), batch[1].contiguous(), batch[2].contiguous()
 
 

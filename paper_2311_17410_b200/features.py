@@ -69,34 +69,34 @@ class _DeviceTable:
         n = len(self)
         out = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
         got = ctypes.c_int64()
-        check(load().gf_ftable_ids(self._h, ptr(out), n, ctypes.byref(got), stream_ptr()))
+        check(load().gf_ftable_ids(self._h, ptr(out), n, ctypes.byref(got), stream_ptr(device=self.device)))
         return out[: got.value]
 
     def _put(self, ids, rows):
         import torch
 
         if isinstance(ids, torch.Tensor) and ids.is_cuda:
-            i = ids.to(torch.int64).contiguous()
+            i = ids.to(device=self.device, dtype=torch.int64).contiguous()
             r = rows.to(device=self.device, dtype=torch.float32).contiguous()
         else:
             i = torch.from_numpy(np.ascontiguousarray(np.asarray(ids, dtype=np.int64))).to(self.device)
             r = torch.from_numpy(np.ascontiguousarray(np.asarray(rows, dtype=np.float32))).to(self.device)
         if tuple(r.shape) != (i.numel(), self.dim):
             raise ValueError(f"rows must be ({i.numel()}, {self.dim}), got {tuple(r.shape)}")
-        check(load().gf_ftable_put(self._h, ptr(i), int(i.numel()), ptr(r), stream_ptr()))
+        check(load().gf_ftable_put(self._h, ptr(i), int(i.numel()), ptr(r), stream_ptr(device=self.device)))
 
     def get(self, ids):
         """Rows for ids (zeros where unknown) and the found mask."""
         import torch
 
         on_dev = isinstance(ids, torch.Tensor) and ids.is_cuda
-        i = ids.to(torch.int64).contiguous() if on_dev else \
+        i = ids.to(device=self.device, dtype=torch.int64).contiguous() if on_dev else \
             torch.from_numpy(np.ascontiguousarray(np.asarray(ids, dtype=np.int64))).to(self.device)
         n = int(i.numel())
         out = torch.zeros((n, self.dim), dtype=torch.float32, device=self.device)
         found = torch.zeros(n, dtype=torch.uint8, device=self.device)
         if n:
-            check(load().gf_ftable_get(self._h, ptr(i), n, ptr(out), ptr(found), stream_ptr()))
+            check(load().gf_ftable_get(self._h, ptr(i), n, ptr(out), ptr(found), stream_ptr(device=self.device)))
         if on_dev:
             return out, found.bool()
         return out.cpu().numpy(), found.cpu().numpy().astype(bool)
@@ -175,7 +175,9 @@ def fetch_features(cache, table, keys, stream=None):
     """
     import torch
 
-    k = keys.to(torch.int64).contiguous() if isinstance(keys, torch.Tensor) else \
+    # host tensors and tensors on another device are moved to the cache's device first: the kernels
+    # dereference the key pointer on that device
+    k = keys.to(device=cache.device, dtype=torch.int64).contiguous() if isinstance(keys, torch.Tensor) else \
         torch.from_numpy(np.ascontiguousarray(np.asarray(keys, dtype=np.int64))).to(cache.device)
     n = int(k.numel())
     values = torch.empty((n, cache.dim), dtype=torch.float32, device=cache.device)
@@ -185,7 +187,7 @@ def fetch_features(cache, table, keys, stream=None):
             t.record_stream(stream)
     nm, adm = ctypes.c_int64(), ctypes.c_int64()
     check(load().gf_fetch_features(cache.handle, table.handle, ptr(k), n, ptr(values), ptr(hit), ctypes.byref(nm),
-                                   ctypes.byref(adm), stream_ptr(stream)))
+                                   ctypes.byref(adm), stream_ptr(stream, cache.device)))
     return values, hit[:n].bool(), int(nm.value), int(adm.value)
 
 

@@ -44,11 +44,16 @@ class DistTransport:
         self.dist = dist
         self.P = dist.get_world_size()
         self.rank = dist.get_rank()
+        # gloo's all_to_all runs on host tensors (CPU tests, several ranks sharing one GPU)
+        self.host = dist.get_backend() != "nccl"
 
     def exchange(self, chunks):
         """chunks[d]: int64 tensor [k, n_d] for rank d -> list of tensors received from each rank."""
         import torch
 
+        if self.host and chunks and chunks[0].is_cuda:
+            dev0 = chunks[0].device
+            return [c.to(dev0) for c in self.exchange([c.cpu() for c in chunks])]
         k = chunks[0].shape[0]
         dev = chunks[0].device
         send_n = torch.tensor([c.shape[1] for c in chunks], dtype=torch.int64, device=dev)
@@ -182,8 +187,9 @@ class GpuEngine:
         self.graph = DynamicGraph(directed=True, tau=tau, sizing=sizing, device=device)
         self.device = self.graph.device
 
-    def add(self, src, dst, ts, eids):
-        self.graph.add_edges_arrays(src, dst, ts, eids)
+    def add(self, src, dst, ts, eids) -> int:
+        """Append owner entries with their global ids; returns the number rejected as out of order."""
+        return self.graph.add_edges_arrays(src, dst, ts, eids)[1]
 
     def delete_node(self, v: int) -> bool:
         return self.graph.delete_node(v)
@@ -232,8 +238,14 @@ class PartitionedGraph:
         owner = es % self.P
         chunks = [torch.stack([es[owner == d], ed[owner == d], et[owner == d], ei[owner == d]]) for d in range(self.P)]
         got = torch.cat(self.t.exchange(chunks), dim=1)  # source-rank order = stream order
+        rejected = 0
         if got.shape[1]:
-            self.e.add(got[0].contiguous(), got[1].contiguous(), got[2].contiguous(), got[3].contiguous())
+            rejected = int(self.e.add(got[0].contiguous(), got[1].contiguous(), got[2].contiguous(),
+                                      got[3].contiguous()))
+        # cluster.py:199-200 asserts a time-sorted stream; a rejection at one owner would leave the
+        # partitions disagreeing about an edge, so every rank learns of it and fails loudly
+        if any(self.t.allgather_int(rejected)):
+            raise ValueError("partitioned ingestion requires a time-sorted stream (an owner rejected an edge)")
         return ids
 
     def delete_node(self, v: int) -> bool:

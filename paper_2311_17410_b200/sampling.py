@@ -176,7 +176,7 @@ def _layer_device(graph: DynamicGraph, src, t_start, t_end, fanout: int, policy:
         total = ctypes.c_int64(0)
         st = lib.gf_sample_layer(graph.handle, ptr(src), ptr(t_start), ptr(t_end), n, int(fanout), code, delta,
                                  seed & _U64, ptr(keys), key_base & _U64, ptr(offsets), ptr(nbr), ptr(eid), ptr(ts),
-                                 ptr(okeys), cap, ctypes.byref(total), stream_ptr(stream))
+                                 ptr(okeys), cap, ctypes.byref(total), stream_ptr(stream, graph.device))
         if st == _lib.GF_ERANGE:
             cap = int(total.value)
             continue
@@ -258,7 +258,7 @@ def sample_khop_device(graph: DynamicGraph, roots, tends, fanouts, policy: Sampl
     st = load().gf_sample_khop(graph.handle, ptr(roots), ptr(tends), int(roots.numel()), I64(*fanouts), n_hops, code,
                                delta, seed & _U64, root_key_base & _U64, VP(*[ptr(o) for o in offs]),
                                VP(*[ptr(x) for x in nbr]), VP(*[ptr(x) for x in eid]), VP(*[ptr(x) for x in tss]),
-                               I64(*caps), totals, stream_ptr(stream))
+                               I64(*caps), totals, stream_ptr(stream, graph.device))
     check(st)
     layers = []
     src, te = roots, tends

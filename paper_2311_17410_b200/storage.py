@@ -269,7 +269,7 @@ class DynamicGraph:
             valid = np.zeros(n, np.uint8)
             check(load().gf_graph_export_nodes(
                 self._h, *[_lib.np_ptr(cols[k], ctypes.c_int64) for k in ("head", "tail", "num_blocks", "degree")],
-                _lib.np_ptr(valid, ctypes.c_uint8), stream_ptr()))
+                _lib.np_ptr(valid, ctypes.c_uint8), stream_ptr(device=self.device)))
             cols["node_valid"] = valid.astype(bool)
             return cols
         return self._exported("nodes", run)
@@ -280,7 +280,7 @@ class DynamicGraph:
             names = ("capacity", "size", "tmin", "tmax", "prev", "next")
             cols = {k: np.zeros(n, np.int64) for k in names}
             check(load().gf_graph_export_blocks(self._h, *[_lib.np_ptr(cols[k], ctypes.c_int64) for k in names],
-                                                stream_ptr()))
+                                                stream_ptr(device=self.device)))
             return cols
         return self._exported("blocks", run)
 
@@ -295,7 +295,7 @@ class DynamicGraph:
             check(load().gf_graph_export_slots(self._h, 0, nb, _lib.np_ptr(offs, ctypes.c_int64),
                                                _lib.np_ptr(nbr, ctypes.c_int64), _lib.np_ptr(eid, ctypes.c_int64),
                                                _lib.np_ptr(ts, ctypes.c_int64), _lib.np_ptr(valid, ctypes.c_uint8),
-                                               stream_ptr()))
+                                               stream_ptr(device=self.device)))
             out = []
             for h in range(nb):
                 cap = int(b["capacity"][h])
@@ -366,7 +366,7 @@ class DynamicGraph:
     # -- mutation -----------------------------------------------------------------
     def reserve(self, nodes: int, blocks: int, slots: int) -> None:
         """Pre-size the device node table, block arena and slot pool (they also grow on demand)."""
-        check(load().gf_graph_reserve(self._h, int(nodes), int(blocks), int(slots), stream_ptr()))
+        check(load().gf_graph_reserve(self._h, int(nodes), int(blocks), int(slots), stream_ptr(device=self.device)))
 
     def add_edges_arrays(self, src, dst, ts, edge_ids=None, stream=None):
         """Batch append from arrays or CUDA tensors; returns (eids tensor, n_rejected).
@@ -390,7 +390,7 @@ class DynamicGraph:
         rej = ctypes.c_int64(0)
         self._version += 1
         check(load().gf_graph_add_edges(self._h, ptr(s), ptr(d), ptr(t), s.numel(), ptr(e), ptr(out),
-                                        ctypes.byref(rej), stream_ptr(stream)))
+                                        ctypes.byref(rej), stream_ptr(stream, self.device)))
         return out, int(rej.value)
 
     def add_edges(self, batch, *, edge_ids: list[int] | None = None) -> InsertionResult:
@@ -414,7 +414,7 @@ class DynamicGraph:
             return 0
         out = ctypes.c_int64(0)
         self._version += 1
-        check(load().gf_graph_delete_edges(self._h, ptr(ids), ids.numel(), ctypes.byref(out), stream_ptr()))
+        check(load().gf_graph_delete_edges(self._h, ptr(ids), ids.numel(), ctypes.byref(out), stream_ptr(device=self.device)))
         return int(out.value)
 
     def delete_edges_set(self, edge_ids) -> set[int]:
@@ -431,7 +431,7 @@ class DynamicGraph:
         """storage.py:507-512."""
         out = ctypes.c_int(0)
         self._version += 1
-        check(load().gf_graph_delete_node(self._h, int(node), ctypes.byref(out), stream_ptr()))
+        check(load().gf_graph_delete_node(self._h, int(node), ctypes.byref(out), stream_ptr(device=self.device)))
         return bool(out.value)
 
     def offload_before(self, cutoff: int, sink) -> int:
@@ -444,14 +444,14 @@ class DynamicGraph:
         lib = load()
         blen, edges = ctypes.c_int64(0), ctypes.c_int64(0)
         check(lib.gf_graph_offload_before(self._h, int(cutoff), None, 0, ctypes.byref(blen), ctypes.byref(edges), 0,
-                                          stream_ptr()))
+                                          stream_ptr(device=self.device)))
         blob = np.zeros(int(blen.value), dtype=np.uint8)
         check(lib.gf_graph_offload_before(self._h, int(cutoff), _lib.np_ptr(blob, ctypes.c_uint8), len(blob),
-                                          ctypes.byref(blen), ctypes.byref(edges), 0, stream_ptr()))
+                                          ctypes.byref(blen), ctypes.byref(edges), 0, stream_ptr(device=self.device)))
         sink.write(blob.tobytes())
         self._version += 1
         check(lib.gf_graph_offload_before(self._h, int(cutoff), None, 0, ctypes.byref(blen), ctypes.byref(edges), 1,
-                                          stream_ptr()))
+                                          stream_ptr(device=self.device)))
         return int(edges.value)
 
     def _live_handles(self) -> list[int]:

@@ -3,9 +3,9 @@
 A frame is a 20-byte little-endian header -- magic ``TGRP``, version (u16),
 message type (u16), request id (u64), payload length (u32) -- and a payload
 of typed fields; every array is a u32 element count followed by the packed
-elements.  The byte layout is the reference's (tests/test_wire.py pins
+elements.  The byte layout is the reference's (tests/test_formats.py pins
 round trips and byte equality against frames the unmodified reference
-encoded, tests/golden/wire.npz).
+encoded, stored as the wire_* entries of tests/golden/formats.npz).
 
 The codec here is table driven: each message type lists its fields as
 (name, kind, numpy dtype) and one packer / one reader walk the table.

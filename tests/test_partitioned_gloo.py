@@ -25,7 +25,7 @@ class OracleEngine:
 
     def add(self, src, dst, ts, eids):
         out = self.g.add_edges(src.numpy(), dst.numpy(), ts.numpy(), eids.numpy())
-        assert (out >= 0).all()
+        return int((out < 0).sum())
 
     def delete_node(self, v):
         return self.g.delete_node(v)
