@@ -337,12 +337,35 @@ def cpu_sample_rate(o, roots, rts, faithful: bool, budget_s: float, chunk: int, 
     return edges / t_total if t_total else 0.0, used, edges, t_total
 
 
+TRAFFIC_SOURCES = ("bench.py", "paper_2311_17410_b200/csrc/gf_sample.cu", "paper_2311_17410_b200/csrc/gf_graph.cuh")
+# profiles/r01_randread.md: one random 32 B record costs a 128 B line; ~37.5 G lines/s on a B200
+RANDOM_LINE_CAP = {"lines_per_s": 37.5e9, "bytes_per_line": 128, "source": "profiles/r01_randread.md"}
+
+
+def source_sha16() -> str:
+    """Hash of the files whose change invalidates an ncu traffic capture (scripts/ncu_summarize.py)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in TRAFFIC_SOURCES:
+        with open(os.path.join(ROOT, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def load_traffic() -> dict:
+    """profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per sampler launch
+    from one ncu capture of this workload (scripts/ncu_sampler.sh + scripts/ncu_summarize.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         with open(p) as fh:
             return json.load(fh)
     return {}
+
+
+def launch_key(name: str) -> str:
+    """'k_sample_fused<false>[uniform/hop1]' -> 'k_sample_fused[uniform/hop1]'."""
+    return re.sub(r"<.*?>|\(\)", "", name)
 
 
 def bench_ours(args, cfg, world, rank, local):
@@ -414,9 +437,25 @@ def bench_ours(args, cfg, world, rank, local):
             base_bytes[base] = base_bytes.get(base, 0) + b
         base_ms[base] = base_ms.get(base, 0.0) + kms
         kernels[name] = ent
+    for ent in kernels.values():
+        if ent.get("achieved_gbs"):
+            ent["frac"] = round(ent["achieved_gbs"] / pk["hbm_gbs"], 4)
     dom_name = max(base_bytes, key=lambda k: base_ms[k])
     achieved = base_bytes[dom_name] / (base_ms[dom_name] / 1e3) / 1e9
-    traffic = load_traffic().get(dom_name) if args.config == "gdelt" else None  # ncu capture is of the gdelt step
+    # the dominant single launch and its measured DRAM traffic (ncu capture of this config, keyed by
+    # the hash of the sources it depends on)
+    dom_launch = max((k for k in kernels if "alg_bytes" in kernels[k]), key=lambda k: kernels[k]["ms"])
+    tr = load_traffic()
+    sha = source_sha16()
+    tr_launch = (tr.get("launches") or {}).get(launch_key(dom_launch)) if tr.get("config") == args.config else None
+    traffic = tr_launch["dram_bytes"] if tr_launch else None
+    dom = {"launch": dom_launch, "ms": kernels[dom_launch]["ms"], "alg_bytes": kernels[dom_launch]["alg_bytes"],
+           "achieved_gbs": kernels[dom_launch]["achieved_gbs"], "frac": kernels[dom_launch]["frac"],
+           "traffic": traffic, "traffic_ratio": round(traffic / kernels[dom_launch]["alg_bytes"], 3) if traffic else None,
+           "traffic_source": "profiles/ncu_traffic.json" if traffic else None,
+           "traffic_sha_match": (tr.get("source_sha16") == sha) if traffic else None}
+    if traffic:
+        dom["ncu_ms"] = tr_launch.get("ms")
     pipe_ms = sum(v for k, v in base_ms.items() if k.startswith(("k_count", "k_write", "k_total", "cub_scan", "k_sample_fused")))
     pipe_gbs = (BYTES_PER_QUERY * q_p + BYTES_PER_EDGE * e_p) / (pipe_ms / 1e3) / 1e9 if pipe_ms else None
 
@@ -465,7 +504,19 @@ def bench_ours(args, cfg, world, rank, local):
     per_policy = {}
     for pol in POLICIES:
         pms, pe = timed_steps(g, roots, rts, key_base, 3, (pol,))
-        per_policy[pol] = {"value": round(pe / (pms / 1e3), 1), "ms_per_step": round(pms / 3, 4)}
+        qs = [v for k_, v in layer_qs.items() if k_.startswith(pol + "/")]
+        pb = sum(BYTES_PER_QUERY * q_ + BYTES_PER_EDGE * s_ for q_, s_ in qs)
+        per_policy[pol] = {"value": round(pe / (pms / 1e3), 1), "ms_per_step": round(pms / 3, 4),
+                           "alg_bytes_per_step": pb,
+                           "frac": round(pb / (pms / 3 / 1e3) / 1e9 / pk["hbm_gbs"], 4)}
+        if pol == "uniform":
+            # every uniform pick is one random record: at most RANDOM_LINE_CAP lines/s, so the policy's
+            # algorithmic fraction cannot exceed (picks/s at the cap) * alg bytes per pick / peak
+            s_tot = sum(s_ for _, s_ in qs)
+            cap_ms = s_tot / RANDOM_LINE_CAP["lines_per_s"] * 1e3
+            per_policy[pol]["random_line_cap"] = {**RANDOM_LINE_CAP, "picks_per_step": s_tot,
+                                                  "floor_ms_per_step": round(cap_ms, 4),
+                                                  "frac_cap": round(pb / (cap_ms / 1e3) / 1e9 / pk["hbm_gbs"], 4)}
     rroots, rrts = replay_roots_for_rank(src, dst, ts, R, rank)
     rms, re_ = timed_steps(g, rroots, rrts, key_base, 3)
     replay = {"value": round(re_ / (rms / 1e3), 1), "unit": "sampled edges/s", "ms_per_step": round(rms / 3, 4),
@@ -510,7 +561,9 @@ def bench_ours(args, cfg, world, rank, local):
                          "peak_source": pk["source"],
                          "alg_bytes": f"{BYTES_PER_QUERY} B/query + {BYTES_PER_EDGE} B/sampled edge (SURVEY.md 8(d)); fused kernel = both",
                          "pipeline_gbs": round(pipe_gbs, 1) if pipe_gbs else None,
-                         "pipeline_frac": round(pipe_gbs / pk["hbm_gbs"], 4) if pipe_gbs else None},
+                         "pipeline_frac": round(pipe_gbs / pk["hbm_gbs"], 4) if pipe_gbs else None,
+                         "dominant_launch": dom, "source_sha16": sha,
+                         **(l2_fraction(cfg, info, base_bytes[dom_name], base_ms[dom_name]) or {})},
             "kernels": kernels,
             "per_policy": per_policy,
             "fetch": fetch,
@@ -521,6 +574,23 @@ def bench_ours(args, cfg, world, rank, local):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+
+
+def l2_fraction(cfg, info, alg_bytes, ms) -> dict | None:
+    """Stores that fit the 126 MB L2 (WIKI/REDDIT shapes) are bound by L2, not HBM, bandwidth: report
+    the kernel's algorithmic bytes against the measured L2 read bandwidth (profiles/l2_bandwidth.json,
+    scripts/l2bw.cu) next to the HBM fraction."""
+    store_bytes = info.device_bytes
+    if store_bytes > 100e6:
+        return None
+    p = os.path.join(ROOT, "profiles", "l2_bandwidth.json")
+    if not os.path.exists(p):
+        return {"l2_resident_store_bytes": store_bytes, "l2_peak_gbs": None}
+    with open(p) as fh:
+        l2 = json.load(fh)
+    gbs = alg_bytes / (ms / 1e3) / 1e9
+    return {"l2_resident_store_bytes": store_bytes, "l2_peak_gbs": l2["l2_read_gbs"],
+            "l2_frac": round(gbs / l2["l2_read_gbs"], 4), "l2_source": "profiles/l2_bandwidth.json"}
 
 
 # GDELT feature dims (PAPER.md:555) and cache sizes (3% of nodes / 3 per mille of edges, PAPER.md:583)

@@ -229,6 +229,25 @@ gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, in
 gf_status gf_gather_rows(const float* d_table, int64_t ld, const int64_t* d_idx, int64_t n, int64_t dim,
                          float* d_out, void* stream);
 
+/* ---- multi-GPU exchange helpers (gf_part.cu) ---------- */
+/* Stable bucketing by owner = key mod nparts (floor modulo, partition.py:38-39; cluster.py:244
+ * routes queries by src % machines, cluster.py:296-325 feature ids by owner).  d_perm[j] = index
+ * of the j-th key in send order (owner-major, original order inside an owner); d_keys_out (may be
+ * NULL) = keys in that order; h_counts[p] = keys owned by p (host, synchronous).  1 <= nparts <= 64. */
+gf_status gf_bucket_by_owner(const int64_t* d_keys, int64_t n, int nparts, int64_t* d_perm, int64_t* d_keys_out,
+                             int64_t* h_counts, void* stream);
+/* Merge owner answers back into request order (cluster.py:268-292): query j of the send order
+ * (d_perm[j] = its original index) returned d_cnt_sorted[j] edges, stored consecutively in each
+ * of the narr (<= 8) arrays d_in[a] (send order).  Writes d_offsets[n+1] (original order, CSR)
+ * and d_out[a] (original order); *h_total = edges (synchronous). */
+gf_status gf_csr_merge(const int64_t* d_perm, const int64_t* d_cnt_sorted, int64_t n, int narr,
+                       const int64_t* const* d_in, int64_t* d_offsets, int64_t* const* d_out, int64_t* h_total,
+                       void* stream);
+/* Row scatter: out[dest[i], :] = in[i, :] (row pitches ld_in / ld_out in floats) -- feature rows
+ * answered by their owners back into request order. */
+gf_status gf_scatter_rows(const float* d_in, int64_t ld_in, const int64_t* d_dest, int64_t n, int64_t dim, float* d_out,
+                          int64_t ld_out, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

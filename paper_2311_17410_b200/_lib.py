@@ -79,6 +79,9 @@ _SIGS = {
     "gf_ftable_ids": (c_int, [c_vp, c_vp, c_i64, P_i64, c_vp]),
     "gf_fetch_features": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, P_i64, P_i64, c_vp]),
     "gf_gather_rows": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp]),
+    "gf_bucket_by_owner": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, P_i64, c_vp]),
+    "gf_csr_merge": (c_int, [c_vp, c_vp, c_i64, c_int, ctypes.POINTER(c_vp), c_vp, ctypes.POINTER(c_vp), P_i64, c_vp]),
+    "gf_scatter_rows": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp]),
 }
 
 EXPORTED = tuple(_SIGS)

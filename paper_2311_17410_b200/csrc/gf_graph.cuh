@@ -13,8 +13,11 @@
 //   sts        (int64 per slot)                dense copy of the slot timestamps (window reads)
 //   fts        (int64 per 32 slots)            fence index: fts[i] = ts of pool slot 32*i, a sorted
 //                                              subsequence of every block's timestamps (L2-sized)
-//   fts16      (int32 per 16 slots)            32-bit fence, exact while every timestamp fits int32
-//                                              (ts32); leaves one-line (128 B) windows
+//   sts32      (int32 per slot)                32-bit copy of the slot timestamps, exact while every
+//                                              timestamp fits int32 (ts32): 32 per 128 B line
+//   fts32      (int32 per 32 slots)            32-bit fence, fts32[i] = ts of pool slot 32*i (ts32):
+//                                              29 MB at GDELT scale, and the 32-slot window it leaves
+//                                              is ONE aligned line of sts32
 //   nflags     (u8 per node)                   bit 0: block list not on the sizing law's closed form
 #pragma once
 
@@ -53,7 +56,8 @@ struct gf_graph {
   gf::Slot* slots = nullptr;
   int64_t* sts = nullptr;
   int64_t* fts = nullptr;
-  int32_t* fts16 = nullptr;  // 32-bit fence every 16 slots (valid while ts32)
+  int32_t* sts32 = nullptr;  // 32-bit slot timestamps (valid while ts32)
+  int32_t* fts32 = nullptr;  // 32-bit fence every 32 slots (valid while ts32)
   int ts32 = 1;              // every timestamp ingested so far fits in int32
   // persistent ingest scratch (sync-free path), sized for the largest batch seen
   void* ing_buf = nullptr;
@@ -78,7 +82,7 @@ struct gf_graph {
 namespace gf {
 
 constexpr int FENCE = 32;    // pool slots per fence entry (int64 fence, general path)
-constexpr int FENCE16 = 16;  // pool slots per 32-bit fence entry: a 16-timestamp window is one 128 B line
+constexpr int FENCE32 = 32;  // pool slots per 32-bit fence entry: a 32-slot window of sts32 is one 128 B line
 
 // NodeRec: one 128-byte line per node, everything a sampler query needs first
 // (one coalesced load): word 0 dir_off, 1 nslots (list end), 2 num_blocks |
@@ -129,7 +133,8 @@ struct GraphView {
   const Slot* slots;
   const int64_t* sts;
   const int64_t* fts;
-  const int32_t* fts16;
+  const int32_t* sts32;
+  const int32_t* fts32;
   const uint8_t* nflags;
   const int64_t* nrec;
   int64_t num_nodes;
@@ -140,7 +145,7 @@ struct GraphView {
 
 inline GraphView view_of(const gf_graph* g) {
   return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off,   g->dir,
-                   g->slots,      g->sts,        g->fts,    g->fts16,     g->nflags,
+                   g->slots,      g->sts,        g->fts,    g->sts32,     g->fts32,     g->nflags,
                    g->nrec,       g->num_nodes,  g->any_deleted, g->ts32,
                    sizing_law(g->sizing_kind, g->tau, g->sizing_param)};
 }

@@ -20,6 +20,11 @@ not by where the query runs, the result equals a single-GPU sample of the
 unpartitioned graph bit for bit (tests/test_partitioned*.py), the property
 the reference checks for its cluster (tests/test_cluster.py:62-84).
 
+Data movement around the all-to-alls runs on the GPU (exchange.py -> gf_part.cu): owner
+bucketing is a stable counting sort, the answers are merged into request order by one CSR-merge
+kernel and feature rows by a row scatter.  The host sees only the per-owner counts the
+all-to-all needs for its split sizes (one small copy per exchange, not one per source rank).
+
 Transports: ``DistTransport`` (torch.distributed all_to_all_single: NCCL over
 NVLink between GPUs, gloo on CPU) and ``ThreadTransport`` (P ranks as
 threads of one process on one GPU, the counterpart of the reference's
@@ -32,6 +37,7 @@ import threading
 
 import numpy as np
 
+from . import exchange as X
 from .sampling import LayeredSample, SampleLayer, SamplingPolicy, hop_seed
 
 
@@ -142,26 +148,30 @@ class PartitionedFeatures:
 
         dev = ids.device
         n = int(ids.numel())
-        owner = ids % self.P
-        order = torch.argsort(owner, stable=True)
-        owner_sorted = owner[order]
-        chunks = [ids[order[owner_sorted == d]].reshape(1, -1) for d in range(self.P)]
+        perm, ids_sorted, counts = X.bucket_by_owner(ids, self.P)
+        chunks, pos = [], 0
+        for c in counts:
+            chunks.append(ids_sorted[pos:pos + c].reshape(1, -1))
+            pos += c
         asked = self.t.exchange(chunks)
-        replies_rows, replies_found = [], []
-        for q in asked:
-            if q.shape[1]:
-                rows, found = self.table.get(q.reshape(-1))
-            else:
-                rows = torch.zeros((0, self.dim), dtype=torch.float32, device=dev)
-                found = torch.zeros(0, dtype=torch.bool, device=dev)
-            replies_rows.append(rows.to(torch.float32))
-            replies_found.append(found.to(torch.int64).reshape(1, -1))
+        sizes = [int(q.shape[1]) for q in asked]
+        qall = torch.cat([q.reshape(-1) for q in asked]) if asked else torch.zeros(0, dtype=torch.int64, device=dev)
+        if qall.numel():
+            rows, found = self.table.get(qall)  # one lookup for every requester
+        else:
+            rows = torch.zeros((0, self.dim), dtype=torch.float32, device=dev)
+            found = torch.zeros(0, dtype=torch.bool, device=dev)
+        rows, found = rows.to(torch.float32), found.to(torch.int64)
+        replies_rows, replies_found, pos = [], [], 0
+        for c in sizes:
+            replies_rows.append(rows[pos:pos + c])
+            replies_found.append(found[pos:pos + c].reshape(1, -1))
+            pos += c
         rows_back = torch.cat(_exchange_rows(self.t, replies_rows)) if n else torch.zeros((0, self.dim), device=dev)
         found_back = torch.cat([f.reshape(-1) for f in self.t.exchange(replies_found)])
-        out = torch.zeros((n, self.dim), dtype=torch.float32, device=dev)
+        out = X.scatter_rows(rows_back, perm, n) if n else torch.zeros((0, self.dim), dtype=torch.float32, device=dev)
         found = torch.zeros(n, dtype=torch.bool, device=dev)
-        out[order] = rows_back
-        found[order] = found_back.bool()
+        found[perm] = found_back.bool()
         return out, found
 
 
@@ -235,8 +245,12 @@ class PartitionedGraph:
             ed = torch.stack([dst, src], 1).reshape(-1)
             et = torch.stack([ts, ts], 1).reshape(-1)
             ei = torch.stack([ids, ids], 1).reshape(-1)
-        owner = es % self.P
-        chunks = [torch.stack([es[owner == d], ed[owner == d], et[owner == d], ei[owner == d]]) for d in range(self.P)]
+        perm, es_s, owner_counts = self._bucket(es)
+        ent = torch.stack([es_s, ed[perm], et[perm], ei[perm]])
+        chunks, pos = [], 0
+        for c in owner_counts:
+            chunks.append(ent[:, pos:pos + c])
+            pos += c
         got = torch.cat(self.t.exchange(chunks), dim=1)  # source-rank order = stream order
         rejected = 0
         if got.shape[1]:
@@ -253,18 +267,24 @@ class PartitionedGraph:
         return bool(self.e.delete_node(v))
 
     # -- sampling -------------------------------------------------------------------
+    # owner bucketing and the request-order merge run on the GPU (gf_part.cu)
+    def _bucket(self, keys):
+        return X.bucket_by_owner(keys, self.P)
+
+    def _merge(self, perm, cnt_sorted, arrays):
+        return X.csr_merge(perm, cnt_sorted, arrays)
+
     def sample_layer(self, src, tend, keys, fanout: int, policy: SamplingPolicy, seed_h: int):
         import torch
 
         dev = self.device
         n = int(src.numel())
-        owner = src % self.P
-        order = torch.argsort(owner, stable=True)
-        owner_sorted = owner[order]
-        chunks = []
-        for d in range(self.P):
-            sel = order[owner_sorted == d]
-            chunks.append(torch.stack([src[sel], tend[sel], keys[sel]]))  # keys: uint64 bit patterns in int64
+        perm, src_s, owner_counts = self._bucket(src)
+        qs = torch.stack([src_s, tend[perm], keys[perm]])  # keys: uint64 bit patterns in int64
+        chunks, pos = [], 0
+        for c in owner_counts:
+            chunks.append(qs[:, pos:pos + c])
+            pos += c
         recv = self.t.exchange(chunks)
         q = torch.cat(recv, dim=1)
         per_src = [int(c.shape[1]) for c in recv]
@@ -276,35 +296,22 @@ class PartitionedGraph:
             counts = torch.zeros(0, dtype=torch.int64, device=dev)
             nbr = eid = ts = okeys = torch.zeros(0, dtype=torch.int64, device=dev)
             offs = torch.zeros(1, dtype=torch.int64, device=dev)
-        # answers back to each origin: per query counts, then the flat edges
-        back_counts, back_edges, qpos, epos = [], [], 0, 0
-        for s, nq in enumerate(per_src):
-            c = counts[qpos:qpos + nq]
-            ne = int(c.sum().item()) if nq else 0
-            back_counts.append(c.reshape(1, -1))
-            back_edges.append(torch.stack([nbr[epos:epos + ne], eid[epos:epos + ne], ts[epos:epos + ne],
-                                           okeys[epos:epos + ne]]))
-            qpos += nq
-            epos += ne
+        # answers back to each origin: per query counts, then the flat edges (the owner's offsets at
+        # the source-rank boundaries: one small host copy)
+        bounds = [0]
+        for nq in per_src:
+            bounds.append(bounds[-1] + nq)
+        eb = offs[torch.tensor(bounds, device=offs.device)].tolist()
+        edges = torch.stack([nbr, eid, ts, okeys])
+        back_counts = [counts[bounds[i]:bounds[i + 1]].reshape(1, -1) for i in range(len(per_src))]
+        back_edges = [edges[:, eb[i]:eb[i + 1]] for i in range(len(per_src))]
         cnt_recv = self.t.exchange(back_counts)
         edge_recv = self.t.exchange(back_edges)
-        # merge into the original query order
-        cnt_sorted = torch.cat([c.reshape(-1) for c in cnt_recv])  # in `order`
+        # merge into the original query order (send order -> request order, one kernel)
+        cnt_sorted = torch.cat([c.reshape(-1) for c in cnt_recv])
         edges_sorted = torch.cat(edge_recv, dim=1)
-        counts_orig = torch.empty(n, dtype=torch.int64, device=dev)
-        counts_orig[order] = cnt_sorted
-        offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(counts_orig, 0, out=offsets[1:])
-        # sorted query i's edges go to offsets[order[i]] .. + cnt_sorted[i]
-        start_sorted = torch.zeros_like(cnt_sorted)
-        if n:
-            start_sorted[1:] = torch.cumsum(cnt_sorted, 0)[:-1]
-        total = int(offsets[-1].item())
-        qid = torch.repeat_interleave(torch.arange(n, device=dev), cnt_sorted)
-        within = torch.arange(total, device=dev) - start_sorted[qid]
-        dest = offsets[order[qid]] + within
-        out = torch.empty((4, total), dtype=torch.int64, device=dev)
-        out[:, dest] = edges_sorted
+        offsets, out, _ = self._merge(perm, cnt_sorted, [edges_sorted[0], edges_sorted[1], edges_sorted[2],
+                                                         edges_sorted[3]])
         return SampleLayer(src, tend, offsets, out[0], out[1], out[2]), out[3]
 
     def sample_khop(self, roots, ts, fanouts, policy: SamplingPolicy, seed: int = 0, root_key_base: int = 0):

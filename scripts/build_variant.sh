@@ -4,7 +4,7 @@ set -e
 name=$1; shift
 cd "$(dirname "$0")/../paper_2311_17410_b200/csrc"
 out=/tmp/variant_$name; mkdir -p $out
-for f in gf_util gf_graph gf_sample gf_cache gf_offload; do
+for f in gf_util gf_graph gf_sample gf_cache gf_offload gf_part; do
   nvcc -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -gencode arch=compute_100a,code=sm_100a \
        --expt-relaxed-constexpr "$@" -c $f.cu -o $out/$f.o &
 done

@@ -1,7 +1,9 @@
 """Where ingest time goes: GDELT-law stream, 100K-edge batches through gf_graph_add_edges.
 
 Prints edges/s (device events around the loop), the per-kernel device time from the library's
-launch profiler, and host wall time per batch.  Usage: python scripts/ingest_profile.py [edges] [batch]
+launch profiler, and host wall time per batch.
+Usage: python scripts/ingest_profile.py [edges] [batch] [nodes] [span]
+(GDELT: 17000 nodes, span 175200 -- the defaults; mag8: 15250000 nodes, span 120, 10M batches)
 """
 
 import os
@@ -16,10 +18,12 @@ from paper_2311_17410_b200 import _lib  # noqa: E402
 
 E = int(sys.argv[1]) if len(sys.argv) > 1 else 20_000_000
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
+NODES = int(sys.argv[3]) if len(sys.argv) > 3 else 17_000
+SPAN = int(sys.argv[4]) if len(sys.argv) > 4 else 175_200
 dev = torch.device("cuda", 0)
-src, dst, ts = gf.generate_synthetic_device(17_000, E, 2.2, 175_200, seed=0, src_skew=2.2, device=dev)
+src, dst, ts = gf.generate_synthetic_device(NODES, E, 2.2, SPAN, seed=0, src_skew=2.2, device=dev)
 g = gf.DynamicGraph(directed=True, tau=8192, device=dev)
-g.reserve(17_000, 17_000 * 16 + E // 8192 + 1024, E + min(17_000 * 8192, E // 2))
+g.reserve(NODES, NODES * 16 + E // 8192 + 1024, E + min(NODES * 8192, E // 2))
 half = E // 2
 for lo in range(0, half, B):  # warm half
     g.add_edges_arrays(src[lo:lo + B], dst[lo:lo + B], ts[lo:lo + B])
@@ -47,7 +51,7 @@ print(f"  kernel sum {tot:.1f} ms = {tot / nb * 1e3:.0f} us/batch")
 # unprofiled rate
 torch.cuda.synchronize()
 g2 = gf.DynamicGraph(directed=True, tau=8192, device=dev)
-g2.reserve(17_000, 17_000 * 16 + E // 8192 + 1024, E + min(17_000 * 8192, E // 2))
+g2.reserve(NODES, NODES * 16 + E // 8192 + 1024, E + min(NODES * 8192, E // 2))
 a.record()
 for lo in range(0, E, B):
     g2.add_edges_arrays(src[lo:lo + B], dst[lo:lo + B], ts[lo:lo + B])

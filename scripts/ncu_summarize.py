@@ -6,7 +6,11 @@ gpurun_out/launches.csv (the launch list), writes
   profiles/<round>_ncu_sampler_launches.json  per-launch metrics
   profiles/ncu_traffic.json                   dram read+write bytes per launch, averaged per kernel
   profiles/<round>_launches.csv               copy of the launch list
-Usage: python scripts/ncu_summarize.py r01
+Usage: python scripts/ncu_summarize.py r02 [report] [config]
+
+profiles/ncu_traffic.json records, per launch (k_sample_fused[<policy>/hop<h>]), the DRAM bytes
+and ncu duration, the config the capture ran (bench.py --config), and the hash of the sources
+(bench.TRAFFIC_SOURCES) at summary time, so bench.py can tell a stale capture from a current one.
 """
 
 from __future__ import annotations
@@ -47,8 +51,10 @@ def raw_rows(rep: str) -> list[dict]:
 
 
 def main() -> None:
-    rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    rows = raw_rows(os.path.join(ROOT, "gpurun_out", "prof.ncu-rep"))
+    rnd = sys.argv[1] if len(sys.argv) > 1 else "r02"
+    rep = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "prof.ncu-rep")
+    config = sys.argv[3] if len(sys.argv) > 3 else "gdelt"
+    rows = raw_rows(rep)
     summ, traffic = {}, {}
     for i, r in enumerate(rows):
         # launches come in step order; the tag follows the launch index (template args stripped)
@@ -71,11 +77,17 @@ def main() -> None:
         if req and sec:
             e["ld_sectors_per_request"] = round(to_float(sec) / max(1.0, to_float(req)), 2)
         summ[f"{name}[{tag}]"] = e
-        traffic.setdefault(name, []).append(to_float(r["dram__bytes_read.sum"]) + to_float(r["dram__bytes_write.sum"]))
+        traffic[f"{name}[{tag}]"] = {"dram_bytes": int(to_float(r["dram__bytes_read.sum"]) + to_float(r["dram__bytes_write.sum"])),
+                                     "ms": e["ms"]}
     with open(os.path.join(ROOT, "profiles", f"{rnd}_ncu_sampler_launches.json"), "w") as f:
         json.dump(summ, f, indent=1)
+    sys.path.insert(0, ROOT)
+    import bench
+
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
-        json.dump({k: int(sum(v) / len(v)) for k, v in traffic.items()}, f, indent=1)
+        json.dump({"config": config, "source_sha16": bench.source_sha16(), "sources": list(bench.TRAFFIC_SOURCES),
+                   "report": os.path.basename(rep), "metric": "dram__bytes_read.sum + dram__bytes_write.sum per launch",
+                   "launches": traffic}, f, indent=1)
     launches = os.path.join(ROOT, "gpurun_out", "launches.csv")
     if os.path.exists(launches):
         shutil.copy(launches, os.path.join(ROOT, "profiles", f"{rnd}_launches.csv"))

@@ -268,3 +268,40 @@ def test_khop_time_window_and_wide_fanouts_vs_oracle(cuda_device, fanouts):
         for lay, r in zip(got.layers, ref):
             for a, w in zip((lay.offsets, lay.neighbors, lay.edge_ids, lay.timestamps), (r[2], r[3], r[4], r[5])):
                 np.testing.assert_array_equal(a.cpu().numpy(), w)
+
+
+@pytest.mark.parametrize("tau", [1, 2, 4, 48, 8192])
+def test_recent_khop_duplicate_heavy_roots_bitwise(cuda_device, tau):
+    """The recent policy's per-call boundary memo (gf_sample.cu RecentMemo): roots repeat the same
+    (node, t_end) pairs many times, block sizes range from 1 slot (tau 1: every hop-2+ selection
+    crosses blocks) to 8192, and the fanout changes per hop ([3, 16, 7]) so memo entries written
+    under one fanout are reused under another -- bitwise vs the oracle, hop by hop."""
+    import torch
+
+    import paper_2311_17410_b200 as gf
+    from oracle import OracleGraph
+
+    src, dst, ts = gf.generate_synthetic_arrays(300, 40_000, 2.2, 2_000, seed=8, src_skew=2.2)
+    g = gf.DynamicGraph(directed=True, tau=tau)
+    o = OracleGraph(True, tau)
+    for lo in range(0, len(src), 10_000):
+        g.add_edges_arrays(src[lo:lo + 10_000], dst[lo:lo + 10_000], ts[lo:lo + 10_000])
+        o.add_edges(src[lo:lo + 10_000], dst[lo:lo + 10_000], ts[lo:lo + 10_000])
+    rng = np.random.default_rng(tau)
+    base = np.concatenate([src[-300:], dst[-300:], np.arange(-2, 302)])
+    bts = np.concatenate([ts[-300:], ts[-300:], rng.integers(-5, 2_010, 304)])
+    pick = rng.integers(0, len(base), 6_000)
+    roots, rts = base[pick], bts[pick]
+    dev = torch.device("cuda:0")
+    got = gf.TemporalSampler(g, [3, 16, 7], "recent").sample(torch.from_numpy(roots).to(dev),
+                                                           torch.from_numpy(rts).to(dev))
+    want = o.sample_khop(roots, rts, [3, 16, 7], "recent", threads=8)
+    for h, (lay, ref) in enumerate(zip(got.layers, want)):
+        for nm, w in zip(("source_nodes", "source_times", "offsets", "neighbors", "edge_ids", "timestamps"), ref):
+            np.testing.assert_array_equal(_host(getattr(lay, nm)), w, err_msg=f"hop{h} {nm}")
+    # sample_layer without t_starts (all TS_MIN) also takes the memo path
+    lay = gf.sample_layer(g, torch.from_numpy(roots).to(dev), torch.full((len(roots),), TS_MIN, device=dev),
+                          torch.from_numpy(rts).to(dev), 10, gf.SamplingPolicy.recent(), 0)
+    w = o.sample_layer(roots, np.full(len(roots), TS_MIN), rts, 10, "recent")
+    for nm, ww in zip(("offsets", "neighbors", "edge_ids", "timestamps"), w):
+        np.testing.assert_array_equal(_host(getattr(lay, nm)), ww)

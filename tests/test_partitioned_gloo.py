@@ -41,6 +41,40 @@ class OracleEngine:
         return tuple(torch.from_numpy(np.ascontiguousarray(a)) for a in (offs, nb, eid, ts, ok))
 
 
+def _host_partitioned_graph():
+    """PartitionedGraph whose bucketing / merge run on host tensors: the CPU engine here is the
+    oracle, so the device kernels (gf_part.cu) are replaced by their numpy statement; the GPU
+    tests (tests/test_gpu_multiproc.py) cover the kernels themselves."""
+    from paper_2311_17410_b200.partitioned import PartitionedGraph
+
+    class HostPartitionedGraph(PartitionedGraph):
+        def _bucket(self, keys):
+            k = keys.numpy()
+            owner = np.mod(k, self.P)
+            perm = np.argsort(owner, kind="stable")
+            counts = np.bincount(owner, minlength=self.P).tolist()
+            return torch.from_numpy(perm), torch.from_numpy(k[perm]), counts
+
+        def _merge(self, perm, cnt_sorted, arrays):
+            perm_np, cnt = perm.numpy(), cnt_sorted.numpy()
+            n = len(perm_np)
+            cnt_orig = np.zeros(n, np.int64)
+            cnt_orig[perm_np] = cnt
+            offsets = np.concatenate([[0], np.cumsum(cnt_orig)]).astype(np.int64)
+            start = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+            outs = []
+            for a in arrays:
+                a = a.numpy()
+                o = np.empty_like(a)
+                for i in range(n):
+                    d = offsets[perm_np[i]]
+                    o[d:d + cnt[i]] = a[start[i]:start[i] + cnt[i]]
+                outs.append(torch.from_numpy(o))
+            return torch.from_numpy(offsets), outs, int(offsets[-1])
+
+    return HostPartitionedGraph
+
+
 def _port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -64,7 +98,7 @@ def _worker(rank, world, port, out_dir, directed):
         from paper_2311_17410_b200.distributed import shard_range
         from paper_2311_17410_b200.partitioned import DistTransport, PartitionedGraph
 
-        pg = PartitionedGraph(DistTransport(), OracleEngine(32), directed=directed)
+        pg = _host_partitioned_graph()(DistTransport(), OracleEngine(32), directed=directed)
         src, dst, ts = _stream()
         for lo in range(0, len(src), 5_000):
             hi = min(len(src), lo + 5_000)
