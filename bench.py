@@ -523,7 +523,8 @@ def bench_ours(args, cfg, world, rank, local):
               "roots": "R/2 uniformly drawn edges (seed 1+rank), src+dst at own ts (SURVEY.md 8(d)(ii))"}
     del rroots, rrts
 
-    fetch = fetch_bench(g, src, dst, ts, cfg, device) if (args.config == "gdelt" and not args.no_fetch) else None
+    fetch = fetch_bench(g, src, dst, ts, cfg, device, world=world, rank=rank) \
+        if (args.config == "gdelt" and not args.no_fetch) else None
 
     ingest_eps = cfg["edges"] / (max_over_ranks(ingest_ms, world) / 1e3)
     info = g.info()
@@ -599,7 +600,7 @@ FETCH_MINIBATCH = 4000      # TGN minibatch edges -> 8,000 roots (harness.py:424
 FETCH_EDGE_TABLE = 5_000_000  # edge features held for the latest 5M edges (142 GB for all 191M)
 
 
-def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50) -> dict:
+def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50, world: int = 1, rank: int = 0) -> dict:
     """Feature-cache fetch block (harness.py:432-446) on GPU: per minibatch of the latest edges,
     2-hop recent f10 sample, then node keys = roots + last-layer neighbours through an LRU node cache
     (d_v 413) and edge keys = every layer's edge ids through an LRU edge cache (d_e 186); misses
@@ -618,8 +619,16 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50) -> dict:
     e_total = src.numel()
     e0 = e_total - FETCH_EDGE_TABLE
     etab = gf.EdgeFeatureTable(FETCH_DE, device=device)
-    etab.append(torch.arange(e0, e_total, device=device),
-                torch.rand(FETCH_EDGE_TABLE, FETCH_DE, device=device, generator=gen))
+    # N > 1: edge rows sharded by eid % N (each rank stores its share; misses are fetched from the
+    # owners over NCCL inside the fetch block); node rows are small and replicated
+    from paper_2311_17410_b200.distributed import ShardedFeatureTable, fetch_features_sharded
+
+    eids = torch.arange(e0, e_total, device=device)
+    erows = torch.rand(FETCH_EDGE_TABLE, FETCH_DE, device=device, generator=gen)
+    own = ShardedFeatureTable.owns(eids, world, rank)
+    etab.append(eids[own].contiguous(), erows[own].contiguous())
+    del erows
+    eshard = ShardedFeatureTable(etab)
     ncache = gf.VectorCache("lru", max(1, int(0.03 * nodes)), FETCH_DV, 0.2, device=device)
     ecache = gf.VectorCache("lru", max(1, int(0.003 * e_total)), FETCH_DE, 0.2, device=device)
     mb = []
@@ -639,25 +648,34 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50) -> dict:
     del held
     for nk, ek in mb[:2]:  # warm-up
         gf.fetch_features(ncache, ntab, nk)
-        gf.fetch_features(ecache, etab, ek)
+        fetch_features_sharded(ecache, eshard, ek)
     torch.cuda.synchronize()
+    # every pass starts from the same post-warm-up cache state (device snapshots), so passes 2 and
+    # 3 replay the streaming minibatches of pass 1 rather than a cache they already warmed
+    nsnap, esnap = ncache.device_snapshot(), ecache.device_snapshot()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     rows = sum(nk.numel() + ek.numel() for nk, ek in mb[2:])
     byts = sum(nk.numel() * (9 + 8 * FETCH_DV) + ek.numel() * (9 + 8 * FETCH_DE) for nk, ek in mb[2:])
-    passes = []
-    for _ in range(3):  # three passes over the minibatches (caches keep evolving); the median is reported
+    passes, hit_rates = [], []
+    for _ in range(3):
+        nsnap.restore_into(ncache)
+        esnap.restore_into(ecache)
+        ncache.reset_stats()
+        ecache.reset_stats()
+        torch.cuda.synchronize()
         a.record()
         for nk, ek in mb[2:]:
             gf.fetch_features(ncache, ntab, nk)
-            gf.fetch_features(ecache, etab, ek)
+            fetch_features_sharded(ecache, eshard, ek)
         b.record()
         torch.cuda.synchronize()
         passes.append(a.elapsed_time(b))
+        hit_rates.append((ncache.stats()["hit_rate"], ecache.stats()["hit_rate"]))
     ms = statistics.median(passes)
     _lib.profile_enable(True)
     for nk, ek in mb[2:6]:
         gf.fetch_features(ncache, ntab, nk)
-        gf.fetch_features(ecache, etab, ek)
+        fetch_features_sharded(ecache, eshard, ek)
     prof = _lib.profile_summary()
     _lib.profile_enable(False)
     tot = sum(v[1] for v in prof.values())
@@ -669,11 +687,15 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50) -> dict:
             "rows_per_minibatch": rows // batches, "achieved_gbs": round(gbs, 1), "frac": round(gbs / pk["hbm_gbs"], 4),
             "row_copy_share": round(gat / tot, 3) if tot else None,
             "passes_ms": [round(x, 3) for x in passes],
+            "pass1_rows_per_s": round(rows / (passes[0] / 1e3), 1),
+            "edge_rows": f"sharded by eid % {world} over the ranks (misses fetched from the owners)" if world > 1
+                         else "local table",
             "top_kernels": {k: round(v[1] / tot, 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])[:8]},
-            "node_hit_rate": round(ncache.stats()["hit_rate"], 4), "edge_hit_rate": round(ecache.stats()["hit_rate"], 4),
+            "node_hit_rate": round(hit_rates[0][0], 4), "edge_hit_rate": round(hit_rates[0][1], 4),
             "config": f"GDELT TGN minibatch {FETCH_MINIBATCH} edges -> {2 * FETCH_MINIBATCH} roots, 2-hop recent f10; "
                       f"node LRU cache 3% (d_v {FETCH_DV}), edge LRU cache 3 per mille (d_e {FETCH_DE}); "
-                      f"edge table = latest {FETCH_EDGE_TABLE // 1_000_000}M edges; median of 3 passes over {batches} minibatches"}
+                      f"edge table = latest {FETCH_EDGE_TABLE // 1_000_000}M edges; median of 3 passes over {batches} "
+                      f"minibatches, each pass from the same restored post-warm-up caches"}
 
 
 def cpu_baseline(cfg, src, dst, ts, roots, rts, args):

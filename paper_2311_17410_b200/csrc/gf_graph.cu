@@ -268,6 +268,8 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
   GF_TRY(grow_array(g->slots, g->slots_used, nc, s));
   GF_TRY(grow_array(g->sts, g->slots_used, nc + 2 * FENCE, s));  // window loads may read past the end
   GF_TRY(grow_array(g->fts, (g->slots_used + FENCE - 1) / FENCE, nc / FENCE + 8, s));  // chunk loads read up to 3 past
+  GF_TRY(grow_array(g->seid, g->slots_used, nc, s));
+  GF_TRY(grow_array(g->snbr, g->slots_used, nc, s));
   GF_TRY(grow_array(g->sts32, g->slots_used, nc + 2 * FENCE32, s));  // whole aligned lines are read
   GF_TRY(grow_array(g->fts32, (g->slots_used + FENCE32 - 1) / FENCE32, nc / FENCE32 + 16, s));  // chunk loads read up to 7 past
   // unused capacity slots must read as invalid (delete scans the whole pool)
@@ -591,8 +593,9 @@ __global__ void k_check_enumerate(const longlong4* __restrict__ off4, int64_t E,
   }
 }
 
-// The commit: one warp per segment writes its new blocks (handle and slot base from the trigger
-// scan), the directory, the node and its NodeRec; one thread per accepted event writes its slot.
+// The commit: one THREAD per segment writes its new blocks (handle and slot base from the trigger
+// scan), the directory, the node and its NodeRec (a warp per segment serialised millions of
+// segments per warp at 10M-edge batches); one thread per accepted event writes its slot.
 // The capacity check ran in an earlier kernel, so a set abort flag is seen here.
 __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const uint32_t* __restrict__ keys,
                          const int64_t* __restrict__ seg_start, SegPlan P, const longlong4* __restrict__ off4, Recs R,
@@ -600,17 +603,15 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
                          const int32_t* __restrict__ ce_seg, const int64_t* __restrict__ src,
                          const int64_t* __restrict__ dst, const int64_t* __restrict__ ts, const int64_t* __restrict__ eids,
                          int directed, const int64_t* __restrict__ old_tail, NodeArrays N, BlockArrays B, DirArrays D,
-                         int kind, Slot* slots, int64_t* sts, int64_t* fts, int32_t* sts32, int32_t* fts32) {
+                         int kind, Slot* slots, int64_t* sts, int64_t* seid, int32_t* snbr, int64_t* fts, int32_t* sts32,
+                         int32_t* fts32) {
   if (c->abort) return;
   const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used, nfree = S->nfree;
   const int64_t* __restrict__ freel = S->free_list;
   // the r-th allocation of the batch takes free_handles.pop() while any are left, then a fresh handle
   auto handle_of = [&](int64_t r) { return r < nfree ? freel[nfree - 1 - r] : blk_used + (r - nfree); };
-  const int lane = threadIdx.x & 31;
   const int64_t nseg = c->num_segs;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = warp; s < nseg; s += nwarps) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cnt = P.acc_cnt[s];
     if (!cnt) continue;
     const int64_t v = keys[seg_start[s]];
@@ -619,12 +620,12 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
     const int64_t dnew = P.plan4[s].z, r0 = off4[s].x;
     const int64_t doff = dnew > 0 ? dir_used + off4[s].z : oo;
     const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? ts[ev_edge(ce_ev[cs + fill - 1], directed)] : 0;
-    __syncwarp();
+    // the node's directory moves to a larger region when it grows past its capacity
     if (nb > 0 && dnew > 0)
-      for (int64_t w = lane; w < nb_old * DIRW; w += 32) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
-    __syncwarp();
-    int64_t h_last = GF_NO_BLOCK, tmin_last = 0, tmax_last = 0, base_last = 0;
-    for (int64_t k = lane; k < nb; k += 32) {
+      for (int64_t w = 0; w < nb_old * DIRW; w++) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
+    int64_t h_first = GF_NO_BLOCK, h_last = GF_NO_BLOCK, tmin_last = 0, tmax_last = 0, base_last = 0;
+    int64_t h_prev = t;
+    for (int64_t k = 0; k < nb; k++) {
       const int64_t r = r0 + k;
       const longlong2 tr = tscan[R.key[r]];
       const int64_t h = handle_of(tr.x), base = slots_used + tr.y;
@@ -636,72 +637,62 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
       B.tmin[h] = tmin;
       B.tmax[h] = tmax;
       B.base[h] = base;
-      B.prev[h] = (k == 0) ? t : handle_of(tscan[R.key[r - 1]].x);
-      B.next[h] = (k == nb - 1) ? GF_NO_BLOCK : handle_of(tscan[R.key[r + 1]].x);
+      B.prev[h] = h_prev;
+      B.next[h] = GF_NO_BLOCK;
+      if (k > 0) B.next[h_prev] = h;
       int64_t* e = D.e + (doff + nb_old + k) * DIRW;
       e[0] = tmin;
       e[1] = ns_old + f;
       e[2] = base;
       e[3] = tmax;
-      if (k == nb - 1) {
-        h_last = h;
-        tmin_last = tmin;
-        tmax_last = tmax;
-        base_last = base;
+      if (k == 0) h_first = h;
+      h_prev = h;
+      h_last = h;
+      tmin_last = tmin;
+      tmax_last = tmax;
+      base_last = base;
+    }
+    // a block allocated while live degree != slots written (a deletion happened) or by
+    // batch sizing leaves the closed-form position -> block law (SizingLaw)
+    if (nb > 0 && (kind == GF_SIZING_BATCH || deg_old != ns_old)) N.nflags[v] |= 1;
+    int64_t tl = t, tl_tmin = 0, tl_tmax = 0, tl_base = 0;
+    if (t != GF_NO_BLOCK) {
+      tl_tmin = B.tmin[t];
+      tl_base = B.base[t];
+      tl_tmax = fill > 0 ? t_tmax : B.tmax[t];
+    }
+    if (t != GF_NO_BLOCK && fill > 0) {
+      B.size[t] = P.tail_size[s] + fill;
+      B.tmax[t] = t_tmax;
+      D.e[(doff + nb_old - 1) * DIRW + 3] = t_tmax;  // old tail grew
+    }
+    if (nb > 0) {
+      if (t == GF_NO_BLOCK) N.head[v] = h_first;
+      else B.next[t] = h_first;
+      tl = h_last;
+      tl_tmin = tmin_last;
+      tl_tmax = tmax_last;
+      tl_base = base_last;
+      N.tail[v] = tl;
+      if (dnew > 0) {
+        N.dir_off[v] = doff;
+        N.dir_cap[v] = dnew;
       }
     }
-    // the lane that wrote the last new block hands its record to lane 0
-    const unsigned who = __ballot_sync(0xffffffffu, h_last != GF_NO_BLOCK);
-    const int src_lane = who ? __ffs(who) - 1 : 0;
-    h_last = __shfl_sync(0xffffffffu, h_last, src_lane);
-    tmin_last = __shfl_sync(0xffffffffu, tmin_last, src_lane);
-    tmax_last = __shfl_sync(0xffffffffu, tmax_last, src_lane);
-    base_last = __shfl_sync(0xffffffffu, base_last, src_lane);
-    const int64_t h_first = nb > 0 ? handle_of(tscan[R.key[r0]].x) : GF_NO_BLOCK;
-    __syncwarp();
-    if (lane == 0) {
-      // a block allocated while live degree != slots written (a deletion happened) or by
-      // batch sizing leaves the closed-form position -> block law (SizingLaw)
-      if (nb > 0 && (kind == GF_SIZING_BATCH || deg_old != ns_old)) N.nflags[v] |= 1;
-      int64_t tl = t, tl_tmin = 0, tl_tmax = 0, tl_base = 0;
-      if (t != GF_NO_BLOCK) {
-        tl_tmin = B.tmin[t];
-        tl_base = B.base[t];
-        tl_tmax = fill > 0 ? t_tmax : B.tmax[t];
-      }
-      if (t != GF_NO_BLOCK && fill > 0) {
-        B.size[t] = P.tail_size[s] + fill;
-        B.tmax[t] = t_tmax;
-        D.e[(doff + nb_old - 1) * DIRW + 3] = t_tmax;  // old tail grew
-      }
-      if (nb > 0) {
-        if (t == GF_NO_BLOCK) N.head[v] = h_first;
-        else B.next[t] = h_first;
-        tl = h_last;
-        tl_tmin = tmin_last;
-        tl_tmax = tmax_last;
-        tl_base = base_last;
-        N.tail[v] = tl;
-        if (dnew > 0) {
-          N.dir_off[v] = doff;
-          N.dir_cap[v] = dnew;
-        }
-      }
-      const int64_t nbt = nb_old + nb;
-      N.num_blocks[v] = nbt;
-      N.degree[v] = deg_old + cnt;
-      N.nslots[v] = ns_old + cnt;
-      int64_t* rr = N.nrec + v * NREC;
-      rr[0] = doff;
-      rr[1] = ns_old + cnt;
-      rr[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
-      rr[3] = D.e[doff * DIRW + 1];
-      rr[4] = D.e[(doff + nbt - 1) * DIRW + 1];
-      rr[5] = tl_base;
-      rr[6] = tl_tmin;
-      rr[7] = tl_tmax;
-      rr[8] = D.e[doff * DIRW];
-    }
+    const int64_t nbt = nb_old + nb;
+    N.num_blocks[v] = nbt;
+    N.degree[v] = deg_old + cnt;
+    N.nslots[v] = ns_old + cnt;
+    int64_t* rr = N.nrec + v * NREC;
+    rr[0] = doff;
+    rr[1] = ns_old + cnt;
+    rr[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
+    rr[3] = D.e[doff * DIRW + 1];
+    rr[4] = D.e[(doff + nbt - 1) * DIRW + 1];
+    rr[5] = tl_base;
+    rr[6] = tl_tmin;
+    rr[7] = tl_tmax;
+    rr[8] = D.e[doff * DIRW];
   }
   // slots: one thread per accepted event
   const int64_t nacc_ev = P.cstart[nseg - 1] + P.acc_cnt[nseg - 1];
@@ -733,6 +724,8 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
     sl.pad = 0;
     slots[pos] = sl;
     sts[pos] = sl.ts;
+    seid[pos] = sl.eid;
+    snbr[pos] = sl.nbr;
     if ((pos & (FENCE - 1)) == 0) fts[pos / FENCE] = sl.ts;
     const int32_t t32 = (int32_t)max(min(sl.ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);  // exact while ts32
     sts32[pos] = t32;
@@ -936,8 +929,8 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
                    g->nflags, g->nrec};
       BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
       DirArrays D{g->dir};
-      GF_LAUNCH(k_commit, grid_for(32 * E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, ce_seg, src,
-                dst, ts, out_eids, dir, old_tail, N, B, D, g->sizing_kind, g->slots, g->sts, g->fts, g->sts32, g->fts32);
+      GF_LAUNCH(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, ce_seg, src,
+                dst, ts, out_eids, dir, old_tail, N, B, D, g->sizing_kind, g->slots, g->sts, g->seid, g->snbr, g->fts, g->sts32, g->fts32);
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
     };
@@ -1055,7 +1048,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dir,
-                g->slots, g->sts, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf};
+                g->slots, g->sts, g->seid, g->snbr, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);
@@ -1196,7 +1189,7 @@ gf_status gf_graph_get_info(gf_graph* g, gf_graph_info* out) {
   out->sizing_kind = g->sizing_kind;
   out->sizing_param = g->sizing_param;
   out->device_bytes = g->node_cap * (8 * 7 + 2 + 8 * NREC) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * DIRW +
-                      g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8 + (g->slot_cap + 2 * FENCE32) * 4 + (g->slot_cap / FENCE32 + 16) * 4;
+                      g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8 + (g->slot_cap + 2 * FENCE32) * 4 + (g->slot_cap / FENCE32 + 16) * 4 + g->slot_cap * 12;
   return GF_OK;
 }
 

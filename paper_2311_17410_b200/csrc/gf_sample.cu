@@ -108,16 +108,11 @@ __device__ __forceinline__ Slot load_slot(const Slot* p) {
   return s;
 }
 
-// the three output fields only (ts, eid: one 128-bit load; nbr: one 32-bit load from the same sector)
-__device__ __forceinline__ Slot load_out3(const Slot* p) {
+__device__ __forceinline__ Slot load_soa3(const GraphView& GV, uint32_t sl) {
   Slot s;
-  long long a, b;
-  int c;
-  asm("ld.global.nc.v2.b64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
-  asm("ld.global.nc.b32 %0, [%1];" : "=r"(c) : "l"(reinterpret_cast<const char*>(p) + 16));
-  s.ts = a;
-  s.eid = b;
-  s.nbr = c;
+  s.ts = __ldg(GV.sts + sl);
+  s.eid = __ldg(GV.seid + sl);
+  s.nbr = __ldg(GV.snbr + sl);
   s.owner = 0;
   s.valid = 1;
   s.pad = 0;
@@ -782,7 +777,17 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   constexpr int FT = fused_threads<EARLY>();
   constexpr int NW = FT / 32;
   constexpr int GU = EARLY ? GF_GATHER_UNROLL_RECENT : GF_GATHER_UNROLL;  // record loads in flight per lane
-  __shared__ uint32_t s_sel[NW][32][KMAX];
+  // s_sel[w][lane][(r + lane) % KMAX]: pool slot of a query's r-th pick (rotated so the 32 lanes of a
+  // warp writing pick r hit different banks); recent runs inside one block keep only s_hi (slot of
+  // position hi-1, all picks are s_hi - r) and skip s_sel
+  __shared__ uint32_t s_sel[EARLY ? 1 : NW][32][KMAX];
+  // recent: per query the slot of position hi-1 and the positions of the boundary block up to t_end
+  // (a pick r < inb is slot s_hi - r); a run crossing into earlier blocks also keeps hi and the
+  // node's directory (offset, blocks) to map the older positions
+  __shared__ uint32_t s_hi[EARLY ? NW : 1][32];
+  __shared__ uint16_t s_inb[EARLY ? NW : 1][32];
+  __shared__ int64_t s_xhi[EARLY ? NW : 1][32];
+  __shared__ int64_t s_xd0[EARLY ? NW : 1][32];
   __shared__ uint8_t s_owner[NW][32 * KMAX];
   __shared__ uint64_t s_key[NW][32];
   __shared__ int32_t s_pre[NW][32];
@@ -914,9 +919,20 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
     if (EARLY || Q.policy == GF_POLICY_RECENT || k == nv) {  // EARLY: launched for recent only
       // newest first: output r is list position hi-1-r (sampling.py:188-190)
       const int64_t inblk = hi - cum;
+      if (EARLY) {
+        s_hi[EARLY ? w : 0][lane] = (uint32_t)slot_hi;
+        s_inb[EARLY ? w : 0][lane] = (uint16_t)min(inblk, (int64_t)KMAX);
+        if (k > inblk) {  // the run crosses into earlier blocks (short lists)
+          s_xhi[EARLY ? w : 0][lane] = hi;
+          s_xd0[EARLY ? w : 0][lane] = d0 | nb << 40;
+        }
+      } else {
 #pragma unroll
-      for (int r = 0; r < KMAX; r++) {
-        if (r < k) s_sel[w][lane][r] = (r < inblk) ? (uint32_t)(slot_hi - r) : pool_slot_of(GV, true, d0, nb, hi - 1 - r);
+        for (int r = 0; r < KMAX; r++) {
+          if (r < k)
+            s_sel[EARLY ? 0 : w][lane][(r + lane) & (KMAX - 1)] =
+                (r < inblk) ? (uint32_t)(slot_hi - r) : pool_slot_of(GV, true, d0, nb, hi - 1 - r);
+        }
       }
     } else {
       // uniform / time_window (k < nv): Floyd over candidate indices 0..nv-1,
@@ -943,9 +959,21 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
       }
 #pragma unroll
       for (int i = 0; i < KMAX; i++)
-        if (i < k) s_sel[w][lane][i] = pool_slot_of(GV, irregular, d0, nb, lo + pick[i]);
+        if (i < k) s_sel[EARLY ? 0 : w][lane][(i + lane) & (KMAX - 1)] = pool_slot_of(GV, irregular, d0, nb, lo + pick[i]);
     }
   }
+
+  // pool slot of warp output e (query j, pick i)
+  auto slot_of = [&](int j, int i) -> uint32_t {
+    if (EARLY) {
+      const int ww = EARLY ? w : 0;
+      if (i < s_inb[ww][j]) return s_hi[ww][j] - (uint32_t)i;
+      const int64_t xd = s_xd0[ww][j];
+      return pool_slot_of(GV, true, xd & ((1ll << 40) - 1), xd >> 40, s_xhi[ww][j] - 1 - i);
+    }
+    return s_sel[EARLY ? 0 : w][j][(i + j) & (KMAX - 1)];
+  };
+  const int total = __shfl_sync(0xffffffffu, incl, 31);  // the warp's outputs
 
   // ---- decoupled look-back: output base of this tile ----
   if (w == 0) {
@@ -983,12 +1011,13 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   // recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
   // (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
   // choice is the faster one for its policy)
+// recent: the three output columns from the SoA copies (a query's run is contiguous there, so a
+// warp's loads coalesce); uniform: the 32 B AoS record (one random line per pick)
 #if GF_AB_NOGATHER
-#define GF_LOAD_OUT(ptr) (O.last_hop ? Slot{(int64_t)(uintptr_t)(ptr), 1, 2, 3, 1, 0} : (EARLY ? load_out3(ptr) : load_slot(ptr)))
+#define GF_LOAD_OUT(sl) (O.last_hop ? Slot{(int64_t)(sl), 1, 2, 3, 1, 0} : (EARLY ? load_soa3(GV, sl) : load_slot(GV.slots + (sl))))
 #else
-#define GF_LOAD_OUT(ptr) (EARLY ? load_out3(ptr) : load_slot(ptr))
+#define GF_LOAD_OUT(sl) (EARLY ? load_soa3(GV, sl) : load_slot(GV.slots + (sl)))
 #endif
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
   const int64_t out0 = base + wpre;
   __syncwarp();
   int e = lane;
@@ -998,7 +1027,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
 #pragma unroll
     for (int u = 0; u < GU; u++) {
       j[u] = s_owner[w][e + 32 * u];
-      s[u] = GF_LOAD_OUT(GV.slots + s_sel[w][j[u]][e + 32 * u - s_pre[w][j[u]]]);
+      s[u] = GF_LOAD_OUT(slot_of(j[u], e + 32 * u - s_pre[w][j[u]]));
     }
 #pragma unroll
     for (int u = 0; u < GU; u++)
@@ -1007,7 +1036,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   for (; e < total; e += 32) {
     const int jj = s_owner[w][e];
     const int i = e - s_pre[w][jj];
-    store_out(O, out0 + e, GF_LOAD_OUT(GV.slots + s_sel[w][jj][i]), s_key[w][jj], i);
+    store_out(O, out0 + e, GF_LOAD_OUT(slot_of(jj, i)), s_key[w][jj], i);
   }
 #undef GF_LOAD_OUT
 }

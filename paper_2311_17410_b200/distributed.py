@@ -13,6 +13,11 @@
 * No collective on the sampling path; the reference's distributed sampler
   reaches the same invariance with its content-keyed RNG (sampling.py:140-142,
   cluster.py:226-292).
+* Features: tables too large to replicate (GDELT edge features are 142 GB) are
+  sharded by owner = id % world (``ShardedFeatureTable``); a rank's cache misses
+  are fetched from their owners with one id/row all-to-all round trip inside the
+  fetch block (``fetch_features_sharded``; cluster.py:296-325 routes feature
+  requests to the owner the same way).
 """
 
 from __future__ import annotations
@@ -112,3 +117,43 @@ class ReplicatedGraph:
 
         base, _ = exclusive_prefix(int(roots.numel()), device=roots.device)
         return TemporalSampler(self.graph, fanouts, strategy, delta, seed).sample(roots, ts, root_key_base=base)
+
+
+class ShardedFeatureTable:
+    """A feature table sharded over the ranks by owner = id % world.
+
+    ``table`` is this rank's NodeFeatureTable / EdgeFeatureTable holding the rows of the ids it
+    owns.  ``get`` answers any id: the ids are bucketed by owner on the GPU, exchanged with one
+    all-to-all (NCCL over NVLink), looked up by their owners and the rows returned with a second
+    all-to-all (partitioned.PartitionedFeatures).  With one rank it is the local table."""
+
+    def __init__(self, table, transport=None):
+        self.table = table
+        self.dim = table.dim
+        self.world, self.rank = world()
+        self.remote = None
+        if self.world > 1:
+            from .partitioned import DistTransport, PartitionedFeatures
+
+            self.remote = PartitionedFeatures(transport or DistTransport(), table, table.dim)
+
+    @staticmethod
+    def owns(ids, world_size: int, rank: int):
+        """Mask of the ids a rank stores."""
+        return (ids % world_size) == rank
+
+    def get(self, ids):
+        return self.remote.get(ids) if self.remote is not None else self.table.get(ids)
+
+
+def fetch_features_sharded(cache, sharded: ShardedFeatureTable, keys):
+    """The fetch block (harness.py:438-446) over a sharded table: one rank -> the fused local
+    block (gf_fetch_features); several -> cache probe, owner fetch of the distinct misses over
+    NCCL, insert.  Returns (values, hit_mask, n_miss, admitted) with complete rows either way."""
+    if sharded.remote is None:
+        from .features import fetch_features
+
+        return fetch_features(cache, sharded.table, keys)
+    from .partitioned import fetch_features_partitioned
+
+    return fetch_features_partitioned(cache, sharded.remote, keys)

@@ -177,11 +177,22 @@ class PartitionedFeatures:
 
 def fetch_features_partitioned(cache, features: PartitionedFeatures, keys):
     """The harness fetch block (harness.py:438-446) with peer-owned rows:
-    cache.fetch -> owner fetch of the misses -> cache.insert_batch(found)."""
-    values, hit, miss = cache.fetch_device(keys)
+    cache.fetch -> owner fetch of the distinct misses -> cache.insert_batch(found).
+
+    Like the local block (features.fetch_features / gf_fetch_features) it returns COMPLETE rows:
+    cached rows for hits, the owners' rows for misses (zeros for ids no owner holds)."""
+    import torch
+
+    k = keys.to(device=cache.device, dtype=torch.int64).contiguous()
+    values, hit, miss = cache.fetch_device(k)
     admitted = 0
     if miss.numel():
         rows, found = features.get(miss)
+        # every missed occurrence takes its distinct key's row (miss keys are unique)
+        order = torch.argsort(miss)
+        occ = (~hit).nonzero().reshape(-1)
+        pos = order[torch.searchsorted(miss[order], k[occ])]
+        values[occ] = rows[pos]
         if bool(found.any()):
             admitted = cache.insert_batch(miss[found].contiguous(), rows[found].contiguous())
     return values, hit, int(miss.numel()), admitted

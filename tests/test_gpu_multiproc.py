@@ -169,3 +169,68 @@ def test_partitioned_two_ranks_libgfb200_equal_unpartitioned(tmp_path, directed)
             for nm in ("neighbors", "edge_ids", "timestamps"):
                 got = np.concatenate([p[f"{pol}_{h}_{nm}"] for p in parts])
                 np.testing.assert_array_equal(got, getattr(lay, nm).cpu().numpy(), err_msg=f"{pol} hop{h} {nm}")
+
+
+def _feature_batches(seed, n_ids, dim):
+    rng = np.random.default_rng(seed)
+    rows = rng.random((n_ids, dim), dtype=np.float32)
+    # power-law-ish key batches with repeats and unknown ids (>= n_ids)
+    batches = [np.minimum(rng.zipf(1.3, 3_000) - 1, n_ids + 50).astype(np.int64) for _ in range(6)]
+    return rows, batches
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2311_17410_b200 as gf
+        from paper_2311_17410_b200.distributed import ShardedFeatureTable, fetch_features_sharded
+
+        dev = torch.device("cuda:0")
+        torch.cuda.set_device(dev)
+        n_ids, dim = 5_000, 186
+        rows, batches = _feature_batches(rank, n_ids, dim)
+        rows_all, _ = _feature_batches(0, n_ids, dim)  # the shared table contents (rank-0 seed)
+        ids = np.arange(n_ids, dtype=np.int64)
+        mine = ids[ShardedFeatureTable.owns(ids, world, rank)]
+        tab = gf.EdgeFeatureTable(dim, device=dev)
+        tab.append(mine, rows_all[mine])
+        sharded = ShardedFeatureTable(tab)
+        cache = gf.VectorCache("lru", 400, dim, 0.2, device=dev)
+        res = {}
+        for b, keys in enumerate(batches):
+            vals, hit, nm, adm = fetch_features_sharded(cache, sharded, torch.from_numpy(keys).to(dev))
+            res[f"v{b}"] = vals.cpu().numpy()
+            res[f"h{b}"] = hit.cpu().numpy()
+            res[f"c{b}"] = np.array([nm, adm])
+        res["keys"] = cache.keys
+        res["scores"] = cache.scores
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_feature_fetch_two_ranks_equal_local_table(tmp_path):
+    """Replicated mode, features sharded by id % world: each rank's fetch block (cache probe, owner
+    fetch of the misses over the all-to-all, insert) equals the fused local block over the whole
+    table -- rows, hit masks, miss / admitted counts and the final cache state."""
+    mp.spawn(_sharded_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    import paper_2311_17410_b200 as gf
+
+    dev = torch.device("cuda:0")
+    n_ids, dim = 5_000, 186
+    rows_all, _ = _feature_batches(0, n_ids, dim)
+    for rank in range(2):
+        _, batches = _feature_batches(rank, n_ids, dim)
+        got = np.load(tmp_path / f"rank{rank}.npz")
+        tab = gf.EdgeFeatureTable(dim, device=dev)
+        tab.append(np.arange(n_ids), rows_all)
+        cache = gf.VectorCache("lru", 400, dim, 0.2, device=dev)
+        for b, keys in enumerate(batches):
+            vals, hit, nm, adm = gf.fetch_features(cache, tab, torch.from_numpy(keys).to(dev))
+            np.testing.assert_array_equal(got[f"v{b}"], vals.cpu().numpy(), err_msg=f"rank {rank} batch {b} rows")
+            np.testing.assert_array_equal(got[f"h{b}"], hit.cpu().numpy())
+            assert list(got[f"c{b}"]) == [nm, adm]
+        np.testing.assert_array_equal(got["keys"], cache.keys)
+        np.testing.assert_array_equal(got["scores"], cache.scores)
