@@ -26,6 +26,11 @@ using namespace gf;
 
 namespace {
 
+// staged batch: one 32-byte record per edge {src, dst, ts, eid} -- after the sort by node every
+// per-event access is a random access by edge index, and one record is one sector (separate
+// src/dst/ts/eid arrays cost a random line each at 10M-edge batches)
+constexpr int ER = 4, ER_SRC = 0, ER_DST = 1, ER_TS = 2, ER_EID = 3;
+
 struct IngestCounters {
   long long minv, maxv;   // node id range of the batch
   long long viol;         // 1 if the batch may reject an edge
@@ -64,14 +69,14 @@ gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
 
 
 // one event per (edge, stored endpoint), in the reference's append order
-__global__ void k_make_events(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n, int directed,
-                              uint32_t* keys, uint32_t* vals, const IngestCounters* c, longlong2* trig) {
+__global__ void k_make_events(const int64_t* __restrict__ rec, int64_t n, int directed, uint32_t* keys, uint32_t* vals,
+                              const IngestCounters* c, longlong2* trig) {
   if (c->abort) return;
   int64_t E = directed ? n : 2 * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t j = directed ? e : (e >> 1);
     int side = directed ? 0 : (int)(e & 1);
-    keys[e] = (uint32_t)(side ? dst[j] : src[j]);
+    keys[e] = (uint32_t)rec[ER * j + (side ? ER_DST : ER_SRC)];
     vals[e] = (uint32_t)e;
     if (trig) trig[e] = make_longlong2(0, 0);
   }
@@ -92,19 +97,19 @@ __global__ void k_heads(const uint32_t* __restrict__ keys, int64_t E, int32_t* h
 
 // seg_id = inclusive_scan(heads) - 1; record segment starts, detect possible rejections
 __global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl,
-                           int64_t E, int directed, const int64_t* __restrict__ ts, const int64_t* tail, const int64_t* bsize,
+                           int64_t E, int directed, const int64_t* __restrict__ rec, const int64_t* tail, const int64_t* bsize,
                            const int64_t* btmax, int64_t* seg_start, IngestCounters* c) {
   if (c->abort) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t s = incl[i] - 1;
     bool head = (i == 0) || keys[i] != keys[i - 1];
-    int64_t t = ts[ev_edge(vals[i], directed)];
+    int64_t t = rec[ER * ev_edge(vals[i], directed) + ER_TS];
     bool viol;
     if (head) {
       seg_start[s] = i;
       viol = t < node_tmax(tail, bsize, btmax, keys[i]);
     } else {
-      viol = t < ts[ev_edge(vals[i - 1], directed)];
+      viol = t < rec[ER * ev_edge(vals[i - 1], directed) + ER_TS];
     }
     if (viol) atomicOr((unsigned long long*)&c->viol, 1ull);
     if (i == E - 1) c->num_segs = s + 1;
@@ -157,8 +162,8 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
                        int64_t param, SegPlan P, int64_t* old_tail) {
   if (c->abort) return;
   const int64_t nseg = c->num_segs;
-  for (int64_t s = nseg + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= E; s += (int64_t)gridDim.x * blockDim.x)
-    P.plan4[s] = make_longlong4(0, 0, 0, 0);
+  // the per-segment plan scan covers num_segs + 1 entries: only the last needs a zero
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.plan4[nseg] = make_longlong4(0, 0, 0, 0);
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     int64_t st = seg_start[s], en = (s + 1 < nseg) ? seg_start[s + 1] : E;
     int64_t cs = cpos[st], cnt = cpos[en] - cs;
@@ -329,10 +334,11 @@ __global__ void k_grow_nodes(IngestCounters* c, const IngestScalars* S, int64_t 
 // Exclusive sum scan of K-wide int64 records (the 4-wide block plan and the 2-wide allocation
 // triggers) in one pass: ticketed tiles with decoupled look-back.  Tile state (flags, ticket) is
 // zeroed by k_stage_minmax at the start of the same launch sequence.
-#ifndef GF_SCAN_ITEMS
-#define GF_SCAN_ITEMS 4
-#endif
-constexpr int SCAN_T = 256, SCAN_ITEMS = GF_SCAN_ITEMS, SCAN_TILE = SCAN_T * SCAN_ITEMS;
+// items per thread: 4 for the latency-bound small batches, 16 for batches of >= 1M events (fewer,
+// fuller tiles for the look-back chain)
+constexpr int SCAN_T = 256, SCAN_ITEMS_SMALL = 4, SCAN_ITEMS_LARGE = 16;
+constexpr int64_t SCAN_LARGE_EVENTS = 1 << 20;
+inline int scan_tile(int64_t E) { return SCAN_T * (E >= SCAN_LARGE_EVENTS ? SCAN_ITEMS_LARGE : SCAN_ITEMS_SMALL); }
 
 struct ScanState {
   int64_t* agg;   // [tiles][K]
@@ -351,7 +357,7 @@ __device__ __forceinline__ void st_flag(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int K>
+template <int K, int SCAN_ITEMS>
 __global__ void __launch_bounds__(SCAN_T) k_scan_sum(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
                                                       ScanState S, const IngestCounters* c, bool per_segment) {
   __shared__ unsigned s_tile;
@@ -364,6 +370,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_sum(const int64_t* __restrict__
   if (threadIdx.x == 0) s_tile = atomicAdd(S.ticket, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
+  constexpr int SCAN_TILE = SCAN_T * SCAN_ITEMS;
   if (tile * SCAN_TILE >= n) return;  // no later tile looks back at this one
   const int64_t i0 = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
   int64_t v[SCAN_ITEMS][K], run[K];
@@ -457,18 +464,14 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_sum(const int64_t* __restrict__
 
 // ---- fused kernels of the sync-free path -------------------------------------
 // staging + batch min/max (the counters were initialised by the H2D copy that starts the sequence)
-__global__ void k_stage_minmax(const IngestScalars* S, int64_t n, int64_t* src, int64_t* dst, int64_t* ts, int64_t* eids,
-                               IngestCounters* c, int* zero, int64_t nzero) {
+__global__ void k_stage_minmax(const IngestScalars* S, int64_t n, int64_t* rec, IngestCounters* c, int* zero, int64_t nzero) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nzero; j += (int64_t)gridDim.x * blockDim.x)
     zero[j] = 0;  // look-back scan flags and tickets of this launch sequence
   const bool has_eids = S->eids_in != nullptr;
   long long mn = LLONG_MAX, mx = LLONG_MIN, tn = LLONG_MAX, tx = LLONG_MIN;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const long long a = S->src[j], b = S->dst[j], t = S->ts[j];
-    src[j] = a;
-    dst[j] = b;
-    ts[j] = t;
-    if (has_eids) eids[j] = S->eids_in[j];
+    reinterpret_cast<longlong4*>(rec)[j] = make_longlong4(a, b, t, has_eids ? S->eids_in[j] : 0);
     mn = min(mn, min(a, b));
     mx = max(mx, max(a, b));
     tn = min(tn, t);
@@ -508,8 +511,8 @@ __global__ void k_stage_minmax(const IngestScalars* S, int64_t n, int64_t* src, 
 // chronology: accept all; only when some endpoint may see a decreasing timestamp, block 0 prepares
 // the per-node latest timestamps and resolves the batch serially (storage.py:426-437)
 __global__ void k_accept(uint8_t* acc, int64_t n, int64_t* tm, const int64_t* tail, const int64_t* bsize,
-                         const int64_t* btmax, const IngestCounters* c, const IngestScalars* S, const int64_t* src,
-                         const int64_t* dst, const int64_t* ts, int directed) {
+                         const int64_t* btmax, const IngestCounters* c, const IngestScalars* S, const int64_t* rec,
+                         int directed) {
   if (c->abort) return;
   if (!c->viol) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
@@ -521,7 +524,7 @@ __global__ void k_accept(uint8_t* acc, int64_t n, int64_t* tm, const int64_t* ta
   __syncthreads();
   if (threadIdx.x) return;
   for (int64_t j = 0; j < n; j++) {
-    const int64_t a = src[j], d = dst[j], t = ts[j];
+    const int64_t a = rec[ER * j + ER_SRC], d = rec[ER * j + ER_DST], t = rec[ER * j + ER_TS];
     const bool ok = t >= tm[a] && (directed || t >= tm[d]);
     acc[j] = ok;
     if (ok) {
@@ -533,7 +536,7 @@ __global__ void k_accept(uint8_t* acc, int64_t n, int64_t* tm, const int64_t* ta
 
 // edge ids (storage.py:438-442) and per-event keep flags in one pass
 __global__ void k_eids_keep(const uint8_t* __restrict__ acc, const int64_t* __restrict__ rank, int64_t n,
-                            const int64_t* __restrict__ eids_in, int64_t* out_eids, IngestCounters* c, const IngestScalars* S,
+                            bool has_eids, int64_t* rec, IngestCounters* c, const IngestScalars* S,
                             const uint32_t* __restrict__ vals, int64_t E, int directed, int64_t* keep) {
   if (c->abort) return;
   const int64_t next_id = S->next_edge_id;
@@ -541,10 +544,10 @@ __global__ void k_eids_keep(const uint8_t* __restrict__ acc, const int64_t* __re
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     int64_t e = -1;
     if (acc[j]) {
-      e = eids_in ? eids_in[j] : next_id + rank[j];
+      e = has_eids ? rec[ER * j + ER_EID] : next_id + rank[j];  // preassigned ids were staged in the record
       mx = max(mx, (long long)e);
     }
-    out_eids[j] = e;
+    rec[ER * j + ER_EID] = e;
     S->out_eids[j] = e;
     if (j == n - 1) c->n_acc = rank[j] + acc[j];
   }
@@ -600,11 +603,8 @@ __global__ void k_check_enumerate(const longlong4* __restrict__ off4, int64_t E,
 __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const uint32_t* __restrict__ keys,
                          const int64_t* __restrict__ seg_start, SegPlan P, const longlong4* __restrict__ off4, Recs R,
                          const longlong2* __restrict__ tscan, const uint32_t* __restrict__ ce_ev,
-                         const int32_t* __restrict__ ce_seg, const int64_t* __restrict__ src,
-                         const int64_t* __restrict__ dst, const int64_t* __restrict__ ts, const int64_t* __restrict__ eids,
-                         int directed, const int64_t* __restrict__ old_tail, NodeArrays N, BlockArrays B, DirArrays D,
-                         int kind, Slot* slots, int64_t* sts, int64_t* seid, int32_t* snbr, int64_t* fts, int32_t* sts32,
-                         int32_t* fts32) {
+                         const int64_t* __restrict__ rec, int directed, const int64_t* __restrict__ old_tail, NodeArrays N,
+                         BlockArrays B, DirArrays D, int kind) {
   if (c->abort) return;
   const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used, nfree = S->nfree;
   const int64_t* __restrict__ freel = S->free_list;
@@ -619,7 +619,7 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
     const int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v], deg_old = N.degree[v], oo = N.dir_off[v];
     const int64_t dnew = P.plan4[s].z, r0 = off4[s].x;
     const int64_t doff = dnew > 0 ? dir_used + off4[s].z : oo;
-    const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? ts[ev_edge(ce_ev[cs + fill - 1], directed)] : 0;
+    const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? rec[ER * ev_edge(ce_ev[cs + fill - 1], directed) + ER_TS] : 0;
     // the node's directory moves to a larger region when it grows past its capacity
     if (nb > 0 && dnew > 0)
       for (int64_t w = 0; w < nb_old * DIRW; w++) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
@@ -630,8 +630,8 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
       const longlong2 tr = tscan[R.key[r]];
       const int64_t h = handle_of(tr.x), base = slots_used + tr.y;
       const int64_t f = R.first[r], n_in = R.count[r];
-      const int64_t tmin = ts[ev_edge(ce_ev[cs + f], directed)];
-      const int64_t tmax = ts[ev_edge(ce_ev[cs + f + n_in - 1], directed)];
+      const int64_t tmin = rec[ER * ev_edge(ce_ev[cs + f], directed) + ER_TS];
+      const int64_t tmax = rec[ER * ev_edge(ce_ev[cs + f + n_in - 1], directed) + ER_TS];
       B.cap[h] = R.cap[r];
       B.size[h] = n_in;
       B.tmin[h] = tmin;
@@ -694,7 +694,20 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
     rr[7] = tl_tmax;
     rr[8] = D.e[doff * DIRW];
   }
-  // slots: one thread per accepted event
+}
+
+// slots: one thread per accepted event (a separate, register-light kernel: full occupancy for the
+// latency-bound per-event chain)
+__global__ void __launch_bounds__(256, 8)
+    k_commit_slots(const IngestCounters* c, const IngestScalars* S, const uint32_t* __restrict__ keys,
+                   const int64_t* __restrict__ seg_start, SegPlan P, const longlong4* __restrict__ off4, Recs R,
+                   const longlong2* __restrict__ tscan, const uint32_t* __restrict__ ce_ev,
+                   const int32_t* __restrict__ ce_seg, const int64_t* __restrict__ rec, int directed,
+                   const int64_t* __restrict__ old_tail, const int64_t* __restrict__ bbase, Slot* slots, int64_t* sts,
+                   int64_t* seid, int32_t* snbr, int64_t* fts, int32_t* sts32, int32_t* fts32) {
+  if (c->abort) return;
+  const int64_t slots_used = S->slots_used;
+  const int64_t nseg = c->num_segs;
   const int64_t nacc_ev = P.cstart[nseg - 1] + P.acc_cnt[nseg - 1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nacc_ev; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t sg = ce_seg[i];
@@ -705,7 +718,7 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
     const int64_t fill = P.fill[sg];
     int64_t pos;
     if (r < fill) {
-      pos = B.base[old_tail[sg]] + P.tail_size[sg] + r;  // the old tail's base does not change
+      pos = bbase[old_tail[sg]] + P.tail_size[sg] + r;  // the old tail's base does not change
     } else {
       int64_t lo = off4[sg].x, hi = lo + P.nb_new[sg];  // last rec with first <= r
       while (hi - lo > 1) {
@@ -715,10 +728,11 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
       }
       pos = slots_used + tscan[R.key[lo]].y + (r - R.first[lo]);
     }
+    const longlong4 er = reinterpret_cast<const longlong4*>(rec)[j];  // one sector
     Slot sl;
-    sl.ts = ts[j];
-    sl.eid = eids[j];
-    sl.nbr = (int32_t)(side ? src[j] : dst[j]);
+    sl.ts = er.z;
+    sl.eid = er.w;
+    sl.nbr = (int32_t)(side ? er.x : er.y);
     sl.owner = (int32_t)keys[seg_start[sg]];
     sl.valid = 1;
     sl.pad = 0;
@@ -788,7 +802,8 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     const int64_t node_cap = g->node_cap;
     const int endbit = bits_for(node_cap);
     size_t cub_bytes = 0;
-    const int64_t tiles4 = (E + 1 + SCAN_TILE - 1) / SCAN_TILE, tiles2 = (E + SCAN_TILE - 1) / SCAN_TILE;
+    const int64_t ST = scan_tile(E);
+    const int64_t tiles4 = (E + 1 + ST - 1) / ST, tiles2 = (E + ST - 1) / ST;
     {
       size_t b = 0;
       GF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
@@ -807,7 +822,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       size_t i = 0;
       p[i++] = a.take<IngestCounters>(1);
       p[i++] = a.take<IngestScalars>(1);
-      for (int q = 0; q < 5; q++) p[i++] = a.take<int64_t>(n);  // staged src, dst, ts, eids_in, out_eids
+      p[i++] = a.take<longlong4>(n);  // staged edge records {src, dst, ts, eid}
       p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E); p[i++] = a.take<uint32_t>(E);
       p[i++] = a.take<int32_t>(E); p[i++] = a.take<int32_t>(E); p[i++] = a.take<int64_t>(E + 1);
       p[i++] = a.take<uint8_t>(n); p[i++] = a.take<int64_t>(n + 1); p[i++] = a.take<int64_t>(node_cap);
@@ -842,12 +857,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     int i = 0;
     IngestCounters* dc = (IngestCounters*)P_[i++];
     IngestScalars* ds = (IngestScalars*)P_[i++];
-    int64_t* src = (int64_t*)P_[i++];
-    int64_t* dst = (int64_t*)P_[i++];
-    int64_t* ts = (int64_t*)P_[i++];
-    int64_t* eids_st = (int64_t*)P_[i++];
-    int64_t* out_eids = (int64_t*)P_[i++];
-    const int64_t* eids_in = eids_user ? eids_st : nullptr;
+    int64_t* rec = (int64_t*)P_[i++];
     uint32_t* keys_in = (uint32_t*)P_[i++];
     uint32_t* keys = (uint32_t*)P_[i++];
     uint32_t* vals_in = (uint32_t*)P_[i++];
@@ -901,36 +911,45 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       size_t tb = cub_bytes;
       GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
       GF_CUDA(cudaMemcpyAsync(dc, hci, sizeof(IngestCounters), cudaMemcpyHostToDevice, s));
-      GF_LAUNCH(k_stage_minmax, grid_for(std::max(n, nzero), T, G), T, 0, s, ds, n, src, dst, ts, eids_st, dc, zero, nzero);
+      GF_LAUNCH(k_stage_minmax, grid_for(std::max(n, nzero), T, G), T, 0, s, ds, n, rec, dc, zero, nzero);
       GF_LAUNCH(k_grow_nodes, grid_for(2 * n, T, G), T, 0, s, dc, ds, node_cap, g->head, g->tail, g->num_blocks,
                 g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
-      GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, src, dst, n, dir, keys_in, vals_in, dc, trig);
+      GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, rec, n, dir, keys_in, vals_in, dc, trig);
       GF_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, tb, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s));
       GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::InclusiveSum(cubtmp, tb, heads, incl, (int)E, s));
-      GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, ts, g->tail, g->bsize, g->btmax,
+      GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, rec, g->tail, g->bsize, g->btmax,
                 seg_start, dc);
-      GF_LAUNCH(k_accept, grid_for(n, T, G), T, 0, s, acc, n, tm, g->tail, g->bsize, g->btmax, dc, ds, src, dst, ts, dir);
+      GF_LAUNCH(k_accept, grid_for(n, T, G), T, 0, s, acc, n, tm, g->tail, g->bsize, g->btmax, dc, ds, rec, dir);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, acc, rank, (int)n, s));
-      GF_LAUNCH(k_eids_keep, grid_for(std::max(n, E), T, G), T, 0, s, acc, rank, n, eids_in, out_eids, dc, ds, vals, E,
+      GF_LAUNCH(k_eids_keep, grid_for(std::max(n, E), T, G), T, 0, s, acc, rank, n, eids_user != nullptr, rec, dc, ds, vals, E,
                 dir, keep);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, cpos, (int)(E + 1), s));
       GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
       GF_LAUNCH(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize,
                 g->bcap, g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, old_tail);
-      GF_LAUNCH(k_scan_sum<4>, tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
+      if (E >= SCAN_LARGE_EVENTS)
+        GF_LAUNCH((k_scan_sum<4, SCAN_ITEMS_LARGE>), tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
+      else
+        GF_LAUNCH((k_scan_sum<4, SCAN_ITEMS_SMALL>), tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
       GF_LAUNCH(k_check_enumerate, grid_for(E, T, G), T, 0, s, off4, E, ds, dc, ce_pend, ce_ev, P, keys, seg_start,
                 g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
-      GF_LAUNCH(k_scan_sum<2>, tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
+      if (E >= SCAN_LARGE_EVENTS)
+        GF_LAUNCH((k_scan_sum<2, SCAN_ITEMS_LARGE>), tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
+      else
+        GF_LAUNCH((k_scan_sum<2, SCAN_ITEMS_SMALL>), tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
       NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
                    g->nflags, g->nrec};
       BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
       DirArrays D{g->dir};
-      GF_LAUNCH(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, ce_seg, src,
-                dst, ts, out_eids, dir, old_tail, N, B, D, g->sizing_kind, g->slots, g->sts, g->seid, g->snbr, g->fts, g->sts32, g->fts32);
+      GF_LAUNCH(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, rec, dir,
+                old_tail, N, B, D, g->sizing_kind);
+      GF_LAUNCH(k_commit_slots, grid_for(E, T, 16 * num_sms()), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan,
+                ce_ev, ce_seg, rec, dir, old_tail, g->bbase, g->slots, g->sts, g->seid, g->snbr,
+                g->fts, g->sts32, g->fts32);
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
     };

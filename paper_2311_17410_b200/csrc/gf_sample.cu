@@ -238,32 +238,29 @@ __device__ __forceinline__ int64_t lane_block_lower_bound(const GraphView& GV, i
 #ifndef GF_NO_FENCE
   if (GV.ts32) {
     // 32-bit fences every 32 pool slots (fts32[f] = ts[32 f]; 8 per 256-bit probe) narrow the
-    // boundary to [a, b], which lies inside ONE aligned 32-slot group: its 32 timestamps are one
-    // 128 B line of sts32, read whole (four independent 256-bit loads) and counted
-    int64_t a = base, b = base + size;
+    // boundary to [a, b], which lies inside ONE aligned 32-slot group: one 128 B line of sts32
+    int64_t a = base, b = base + size, tl = t0 - 1, th = t1 + 1;
     const int64_t f0 = (base + FENCE32 - 1) / FENCE32, f1 = (base + size - 1) / FENCE32;
     if (f1 >= f0) {
       const int nf = (int)(f1 - f0) + 1;
       int flo = -1, fhi = nf;
-      int64_t ftl = t0 - 1, fth = t1 + 1;
+      int64_t ftl = tl, fth = th;
       bracket_search32(GV.fts32 + f0, (int)(f0 & 7), flo, fhi, ftl, fth, x);
-      if (flo >= 0) a = (f0 + flo) * FENCE32 + 1;  // ts[a - 1] < x
-      if (fhi < nf) b = (f0 + fhi) * FENCE32;      // ts[b] >= x
+      if (flo >= 0) {
+        a = (f0 + flo) * FENCE32 + 1;  // ts[a - 1] = ftl < x
+        tl = ftl;
+      }
+      if (fhi < nf) {
+        b = (f0 + fhi) * FENCE32;  // ts[b] = fth >= x
+        th = fth;
+      }
     }
     if (b <= a) return a - base;
-    const int64_t g = a & ~(int64_t)(FENCE32 - 1);
-    const int64_t* line = reinterpret_cast<const int64_t*>(GV.sts32 + g);
-    int64_t w[16];
-#pragma unroll
-    for (int c = 0; c < 4; c++) ld256(line + 4 * c, w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-    const int lo = (int)(a - g), hi = (int)(b - g);
-    int cnt = 0;
-#pragma unroll
-    for (int j = 0; j < 32; j++) {
-      const int64_t v = (int64_t)(int32_t)((j & 1) ? (uint64_t)w[j >> 1] >> 32 : (uint64_t)w[j >> 1]);
-      cnt += (j >= lo && j < hi && v < x) ? 1 : 0;
-    }
-    return a + cnt - base;
+    // inside the window: the same bracketed interpolation over sts32 (8 timestamps per 256-bit
+    // probe, usually one probe; a second one hits the line the first brought into L2)
+    int lo = -1, hi = (int)(b - a);
+    bracket_search32(GV.sts32 + a, (int)(a & 7), lo, hi, tl, th, x);
+    return a + hi - base;
   }
 #endif
   // bracket relative to base; block sizes are bounded by the sizing law / one ingest batch
