@@ -101,7 +101,10 @@ def load():
             raise ImportError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py` "
                               "(make -C paper_2311_17410_b200/csrc)")
         lib = ctypes.CDLL(LIB_PATH)
+        ab = os.environ.get("GF_LIB_AB") == "1"  # A/B against an older build: tolerate missing entry points
         for name, (res, args) in _SIGS.items():
+            if ab and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

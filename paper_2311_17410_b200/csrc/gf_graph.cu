@@ -273,8 +273,6 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
   GF_TRY(grow_array(g->slots, g->slots_used, nc, s));
   GF_TRY(grow_array(g->sts, g->slots_used, nc + 2 * FENCE, s));  // window loads may read past the end
   GF_TRY(grow_array(g->fts, (g->slots_used + FENCE - 1) / FENCE, nc / FENCE + 8, s));  // chunk loads read up to 3 past
-  GF_TRY(grow_array(g->seid, g->slots_used, nc, s));
-  GF_TRY(grow_array(g->snbr, g->slots_used, nc, s));
   GF_TRY(grow_array(g->sts32, g->slots_used, nc + 2 * FENCE32, s));  // whole aligned lines are read
   GF_TRY(grow_array(g->fts32, (g->slots_used + FENCE32 - 1) / FENCE32, nc / FENCE32 + 16, s));  // chunk loads read up to 7 past
   // unused capacity slots must read as invalid (delete scans the whole pool)
@@ -704,7 +702,7 @@ __global__ void __launch_bounds__(256, 8)
                    const longlong2* __restrict__ tscan, const uint32_t* __restrict__ ce_ev,
                    const int32_t* __restrict__ ce_seg, const int64_t* __restrict__ rec, int directed,
                    const int64_t* __restrict__ old_tail, const int64_t* __restrict__ bbase, Slot* slots, int64_t* sts,
-                   int64_t* seid, int32_t* snbr, int64_t* fts, int32_t* sts32, int32_t* fts32) {
+                   int64_t* fts, int32_t* sts32, int32_t* fts32) {
   if (c->abort) return;
   const int64_t slots_used = S->slots_used;
   const int64_t nseg = c->num_segs;
@@ -738,8 +736,6 @@ __global__ void __launch_bounds__(256, 8)
     sl.pad = 0;
     slots[pos] = sl;
     sts[pos] = sl.ts;
-    seid[pos] = sl.eid;
-    snbr[pos] = sl.nbr;
     if ((pos & (FENCE - 1)) == 0) fts[pos / FENCE] = sl.ts;
     const int32_t t32 = (int32_t)max(min(sl.ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);  // exact while ts32
     sts32[pos] = t32;
@@ -948,7 +944,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_LAUNCH(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, rec, dir,
                 old_tail, N, B, D, g->sizing_kind);
       GF_LAUNCH(k_commit_slots, grid_for(E, T, 16 * num_sms()), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan,
-                ce_ev, ce_seg, rec, dir, old_tail, g->bbase, g->slots, g->sts, g->seid, g->snbr,
+                ce_ev, ce_seg, rec, dir, old_tail, g->bbase, g->slots, g->sts,
                 g->fts, g->sts32, g->fts32);
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
@@ -1067,7 +1063,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dir,
-                g->slots, g->sts, g->seid, g->snbr, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf};
+                g->slots, g->sts, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);
@@ -1208,7 +1204,7 @@ gf_status gf_graph_get_info(gf_graph* g, gf_graph_info* out) {
   out->sizing_kind = g->sizing_kind;
   out->sizing_param = g->sizing_param;
   out->device_bytes = g->node_cap * (8 * 7 + 2 + 8 * NREC) + g->blk_cap * 8 * 7 + g->dir_cap_total * 8 * DIRW +
-                      g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8 + (g->slot_cap + 2 * FENCE32) * 4 + (g->slot_cap / FENCE32 + 16) * 4 + g->slot_cap * 12;
+                      g->slot_cap * (int64_t)(sizeof(Slot) + 8) + (g->slot_cap / FENCE + 1) * 8 + (g->slot_cap + 2 * FENCE32) * 4 + (g->slot_cap / FENCE32 + 16) * 4;
   return GF_OK;
 }
 

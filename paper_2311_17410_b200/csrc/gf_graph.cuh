@@ -13,10 +13,6 @@
 //   sts        (int64 per slot)                dense copy of the slot timestamps (window reads)
 //   fts        (int64 per 32 slots)            fence index: fts[i] = ts of pool slot 32*i, a sorted
 //                                              subsequence of every block's timestamps (L2-sized)
-//   seid, snbr (int64 / int32 per slot)       SoA copies of the slot edge ids and neighbours: with sts
-//                                              they let the recent policy's contiguous runs be read
-//                                              with coalesced 8/4-byte loads (uniform picks read the
-//                                              32 B AoS record: one line per random pick)
 //   sts32      (int32 per slot)                32-bit copy of the slot timestamps, exact while every
 //                                              timestamp fits int32 (ts32): 32 per 128 B line
 //   fts32      (int32 per 32 slots)            32-bit fence, fts32[i] = ts of pool slot 32*i (ts32):
@@ -60,8 +56,6 @@ struct gf_graph {
   gf::Slot* slots = nullptr;
   int64_t* sts = nullptr;
   int64_t* fts = nullptr;
-  int64_t* seid = nullptr;   // SoA edge ids
-  int32_t* snbr = nullptr;   // SoA neighbours
   int32_t* sts32 = nullptr;  // 32-bit slot timestamps (valid while ts32)
   int32_t* fts32 = nullptr;  // 32-bit fence every 32 slots (valid while ts32)
   int ts32 = 1;              // every timestamp ingested so far fits in int32
@@ -138,8 +132,6 @@ struct GraphView {
   const int64_t* dir;
   const Slot* slots;
   const int64_t* sts;
-  const int64_t* seid;
-  const int32_t* snbr;
   const int64_t* fts;
   const int32_t* sts32;
   const int32_t* fts32;
@@ -153,7 +145,7 @@ struct GraphView {
 
 inline GraphView view_of(const gf_graph* g) {
   return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off,   g->dir,
-                   g->slots,      g->sts,        g->seid,   g->snbr,      g->fts,       g->sts32,     g->fts32,     g->nflags,
+                   g->slots,      g->sts,        g->fts,       g->sts32,     g->fts32,     g->nflags,
                    g->nrec,       g->num_nodes,  g->any_deleted, g->ts32,
                    sizing_law(g->sizing_kind, g->tau, g->sizing_param)};
 }

@@ -108,11 +108,16 @@ __device__ __forceinline__ Slot load_slot(const Slot* p) {
   return s;
 }
 
-__device__ __forceinline__ Slot load_soa3(const GraphView& GV, uint32_t sl) {
+// the three output fields only (ts, eid: one 128-bit load; nbr: one 32-bit load from the same sector)
+__device__ __forceinline__ Slot load_out3(const Slot* p) {
   Slot s;
-  s.ts = __ldg(GV.sts + sl);
-  s.eid = __ldg(GV.seid + sl);
-  s.nbr = __ldg(GV.snbr + sl);
+  long long a, b;
+  int c;
+  asm("ld.global.nc.v2.b64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  asm("ld.global.nc.b32 %0, [%1];" : "=r"(c) : "l"(reinterpret_cast<const char*>(p) + 16));
+  s.ts = a;
+  s.eid = b;
+  s.nbr = c;
   s.owner = 0;
   s.valid = 1;
   s.pad = 0;
@@ -670,39 +675,6 @@ struct TileCtl {
   int64_t* total;               // layer total (written by the tile holding the last query)
 };
 
-// Boundary memo of the recent policy (one per sampling call, zeroed at its start, shared by its
-// hops: the graph does not change inside a call).  A query's answer depends only on (node, t_end)
-// when t_start = TS_MIN, and the harness's minibatches (latest edges as roots) repeat those pairs
-// heavily: on the GDELT bench only 4.7% of the recent hop-1 queries are distinct.  A hit replaces
-// the node-record / block / fence / window search chain with one L2 read.
-//   bucket = 32 B: two {key, value} entries; key = (node + 1) << 32 | (uint32) t_end (0 = empty;
-//   exact while timestamps fit int32), value = candidates (clamped to 16 bits) << 48 | positions of
-//   the boundary block up to t_end (clamped) << 32 | pool slot of the last candidate (all-ones when
-//   there is none), so a written value is never 0.  Values are deterministic per key, so racing
-//   writers store the same bits, and a reader that sees a key before its value treats it as a miss.
-struct RecentMemo {
-  uint64_t* table;  // NULL = off
-  uint64_t mask;    // buckets - 1
-  int shift;        // 64 - log2(buckets)
-};
-
-__device__ __forceinline__ uint64_t memo_bucket(const RecentMemo& M, uint64_t key) {
-  return (key * 0x9E3779B97F4A7C15ull) >> M.shift;
-}
-
-__device__ __forceinline__ void memo_insert(const RecentMemo& M, uint64_t key, uint64_t val) {
-  unsigned long long* b = reinterpret_cast<unsigned long long*>(M.table + 4 * memo_bucket(M, key));
-#pragma unroll
-  for (int e = 0; e < 2; e++) {
-    const unsigned long long old = atomicCAS(b + 2 * e, 0ull, (unsigned long long)key);
-    if (old == 0ull) {
-      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(b + 2 * e + 1), "l"(val) : "memory");
-      return;
-    }
-    if (old == key) return;  // another query of the same pair is writing it
-  }
-}
-
 // list position -> pool slot for a selected position (regular lists: closed form; else directory)
 __device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
   const int64_t* dd = GV.dir + d0 * DIRW;
@@ -770,7 +742,7 @@ template <bool EARLY>
 #endif
 __global__ void __launch_bounds__(fused_threads<EARLY>(),
                                   EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_MINB * 256 / fused_threads<EARLY>())
-    k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C, RecentMemo M) {
+    k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
   constexpr int FT = fused_threads<EARLY>();
   constexpr int NW = FT / 32;
   constexpr int GU = EARLY ? GF_GATHER_UNROLL_RECENT : GF_GATHER_UNROLL;  // record loads in flight per lane
@@ -822,38 +794,10 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
       k = 0;
     }
   };
-  uint64_t mkey = 0;  // memo key of a query that missed (0: no insert)
-  bool hit = false;
   if (q < n) {
     const int64_t v = Q.src[q];
     te = Q.t_end[q];
     if (v >= 0 && v < GV.num_nodes) {
-      if (EARLY && M.table) {
-        // the memo bucket (the memo is written during the launch: L2 loads, not the read-only path)
-        const uint64_t key = ((uint64_t)(v + 1) << 32) | (uint32_t)te;
-        unsigned long long k0, v0, k1, v1;
-        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];"
-                     : "=l"(k0), "=l"(v0) : "l"(M.table + 4 * memo_bucket(M, key)));
-        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];"
-                     : "=l"(k1), "=l"(v1) : "l"(M.table + 4 * memo_bucket(M, key) + 2));
-        const uint64_t val = (k0 == key && v0) ? v0 : ((k1 == key && v1) ? v1 : 0);
-        if (val) {
-          const int64_t cnt = (int64_t)(val >> 48), inb = (int64_t)((val >> 32) & 0xffff);
-          k = (int)min(cnt, Q.fanout);
-          if (k <= inb) {  // every selected position lies in the boundary block
-            hit = true;
-            slot_hi = (int64_t)(val & 0xffffffffull);
-            hi = k;  // selection below reads positions hi-1-r as slot_hi - r (inblk = hi - cum >= k)
-            lo = 0;
-            cum = 0;
-          } else {
-            k = 0;
-          }
-        }
-        if (!hit) mkey = key;
-      }
-    }
-    if (!hit && v >= 0 && v < GV.num_nodes) {
       const int64_t* r = GV.nrec + v * NREC;
       int64_t w2, w3;
       ld256(r, N.d0, N.ns, w2, N.first);
@@ -894,13 +838,6 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   if (early) tile_publish<NW>(k, lane, w, s_wsum, C, tile, incl, wpre, agg);
 
   if (EARLY && live) finish();
-  if (EARLY && mkey) {
-    // remember the answer: candidates and in-block positions up to t_end, slot of position hi-1
-    const uint64_t cnt = live && hi > lo ? (uint64_t)min(hi - lo, (int64_t)0xffff) : 0;
-    const uint64_t inb = cnt ? (uint64_t)min(hi - cum, (int64_t)0xffff) : 0;
-    const uint64_t sl = cnt ? (uint64_t)(uint32_t)slot_hi : 0xffffffffull;
-    memo_insert(M, mkey, cnt << 48 | inb << 32 | sl);
-  }
   if (!early) tile_publish<NW>(k, lane, w, s_wsum, C, tile, incl, wpre, agg);
 
   // ---- selection into shared memory (independent of the output base) ----
@@ -1008,12 +945,14 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   // recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
   // (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
   // choice is the faster one for its policy)
-// recent: the three output columns from the SoA copies (a query's run is contiguous there, so a
-// warp's loads coalesce); uniform: the 32 B AoS record (one random line per pick)
+// recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
+// (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
+// choice is the faster one for its policy; SoA copies of the columns made the recent runs cost more
+// lines on deep-boundary roots, profiles/README.md)
 #if GF_AB_NOGATHER
-#define GF_LOAD_OUT(sl) (O.last_hop ? Slot{(int64_t)(sl), 1, 2, 3, 1, 0} : (EARLY ? load_soa3(GV, sl) : load_slot(GV.slots + (sl))))
+#define GF_LOAD_OUT(sl) (O.last_hop ? Slot{(int64_t)(sl), 1, 2, 3, 1, 0} : (EARLY ? load_out3(GV.slots + (sl)) : load_slot(GV.slots + (sl))))
 #else
-#define GF_LOAD_OUT(sl) (EARLY ? load_soa3(GV, sl) : load_slot(GV.slots + (sl)))
+#define GF_LOAD_OUT(sl) (EARLY ? load_out3(GV.slots + (sl)) : load_slot(GV.slots + (sl)))
 #endif
   const int64_t out0 = base + wpre;
   __syncwarp();
@@ -1259,28 +1198,9 @@ int64_t tile_words(int64_t cap_q, int policy) {  // status words + ticket
   return (cap_q + tile_threads(policy) - 1) / tile_threads(policy) + 1;
 }
 
-// The recent-policy boundary memo applies when every query's window starts at TS_MIN (sample_khop,
-// sample_layer without t_start), timestamps fit int32 and the fused kernel runs.  Sized at one
-// entry per two queries of the call (at least 1K, at most 1M buckets = 32 MB; a full bucket just
-// means no memo for that pair), zeroed once per call.
-bool memo_enabled() {
-  static const bool on = getenv("GF_NO_MEMO") == nullptr;
-  return on;
-}
-int64_t memo_buckets(int64_t queries) {
-  int64_t b = 1024;
-  while (b < (1ll << 20) && 4 * b < queries) b <<= 1;
-  return b;
-}
-RecentMemo memo_view(void* p, int64_t buckets) {
-  int lg = 0;
-  while ((1ll << lg) < buckets) lg++;
-  return RecentMemo{reinterpret_cast<uint64_t*>(p), (uint64_t)(buckets - 1), 64 - lg};
-}
-
 // tile_state: (tiles + 1) zeroed words for the fused kernel, or NULL to allocate them here
 gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_offsets, const LayerOut& O, int64_t* total,
-                       cudaStream_t s, uint64_t* tile_state = nullptr, RecentMemo M = RecentMemo{nullptr, 0, 0}) {
+                       cudaStream_t s, uint64_t* tile_state = nullptr) {
   GraphView GV = view_of(g);
   const bool fast = !g->any_deleted;
   if (uses_fused(g, Q.fanout) && cap_q > 0) {
@@ -1294,8 +1214,8 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
       GF_CUDA(cudaMemsetAsync(tile_state, 0, sizeof(uint64_t) * (tiles + 1), s));
     }
     TileCtl C{tile_state, reinterpret_cast<unsigned long long*>(tile_state + tiles), total};
-    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, ft, 0, s, GV, Q, O, C, M);
-    else GF_LAUNCH(k_sample_fused<false>, tiles, ft, 0, s, GV, Q, O, C, RecentMemo{nullptr, 0, 0});
+    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, ft, 0, s, GV, Q, O, C);
+    else GF_LAUNCH(k_sample_fused<false>, tiles, ft, 0, s, GV, Q, O, C);
     return GF_OK;
   }
   GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
@@ -1344,15 +1264,7 @@ gf_status gf_sample_layer(gf_graph* g, const int64_t* d_src, const int64_t* d_t_
   GF_CUDA(cudaMemsetAsync(total, 0, 16, s));
   QueryIn Q{d_src, d_t_start, d_t_end, d_keys, key_base, n, nullptr, fanout, policy, delta, seed};
   LayerOut O{d_offsets, d_nbr, d_eid, d_ts, d_out_keys, out_cap, overflow, 0};
-  RecentMemo M{nullptr, 0, 0};
-  Scratch mb(s);
-  if (policy == GF_POLICY_RECENT && !d_t_start && g->ts32 && uses_fused(g, fanout) && memo_enabled() && n > 0) {
-    const int64_t nb = memo_buckets(n);
-    GF_TRY(mb.alloc((size_t)nb * 32));
-    GF_CUDA(cudaMemsetAsync(mb.p, 0, (size_t)nb * 32, s));
-    M = memo_view(mb.p, nb);
-  }
-  GF_TRY(layer_launch(g, Q, n, d_offsets, O, total, s, nullptr, M));
+  GF_TRY(layer_launch(g, Q, n, d_offsets, O, total, s));
   int64_t h[2] = {0, 0};
   GF_CUDA(cudaMemcpyAsync(h, total, 16, cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
@@ -1390,21 +1302,7 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
       zero_words += tile_words(cq, policy);
     }
   }
-  // recent boundary memo, shared by the call's hops
-  int64_t memo_b = 0;
-  if (policy == GF_POLICY_RECENT && g->ts32 && memo_enabled()) {
-    bool fused_any = false;
-    int64_t queries = 0;
-    for (int h = 0; h < n_hops; h++) {
-      const int64_t cq = (h == 0) ? n_roots : h_caps[h - 1];
-      if (uses_fused(g, h_fanouts[h]) && cq > 0) fused_any = true;
-      queries += cq;
-    }
-    if (fused_any) memo_b = memo_buckets(queries);
-  }
-  const size_t memo_off = (sizeof(int64_t) * (size_t)zero_words + 255) & ~size_t(255);
-  const size_t memo_bytes = (size_t)memo_b * 32;
-  const size_t bytes = memo_off + memo_bytes + 256 + 2 * sizeof(uint64_t) * (size_t)key_cap + 512;
+  const size_t bytes = sizeof(int64_t) * (size_t)zero_words + 256 + 2 * sizeof(uint64_t) * (size_t)key_cap + 512;
   Scratch sb(s);
   char* base = nullptr;
   int64_t* hbuf = nullptr;
@@ -1437,12 +1335,7 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
     hbuf = hvec.data();
   }
   int64_t* totals = reinterpret_cast<int64_t*>(base);
-  uint64_t* keys0 = reinterpret_cast<uint64_t*>(base + ((memo_off + memo_bytes + 255) & ~size_t(255)));
-  RecentMemo M{nullptr, 0, 0};
-  if (memo_b) {
-    GF_CUDA(cudaMemsetAsync(base + memo_off, 0, memo_bytes, s));
-    M = memo_view(base + memo_off, memo_b);
-  }
+  uint64_t* keys0 = reinterpret_cast<uint64_t*>(base + ((sizeof(int64_t) * zero_words + 255) & ~size_t(255)));
   uint64_t* keybuf[2] = {keys0, keys0 + key_cap};
   int* overflow = reinterpret_cast<int*>(totals + n_hops);
   GF_CUDA(cudaMemsetAsync(totals, 0, sizeof(int64_t) * zero_words, s));
@@ -1460,7 +1353,7 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
       g_prof_tag = std::string(policy == GF_POLICY_RECENT ? "recent" : policy == GF_POLICY_UNIFORM ? "uniform" : "tw") +
                    "/hop" + std::to_string(h);
     gf_status st = layer_launch(g, Q, cap_q, d_offsets[h], O, totals + h, s,
-                                tile_off[h] >= 0 ? reinterpret_cast<uint64_t*>(totals + tile_off[h]) : nullptr, M);
+                                tile_off[h] >= 0 ? reinterpret_cast<uint64_t*>(totals + tile_off[h]) : nullptr);
     g_prof_tag.clear();
     GF_TRY(st);
     src = d_nbr[h];
