@@ -123,6 +123,16 @@ class NodeFeatureTable(_DeviceTable):
         """features.py:60-61."""
         return self._stored_ids().cpu().numpy()
 
+    @property
+    def _rows(self) -> dict[int, np.ndarray]:
+        """Host snapshot {node: row} of the device table (the reference keeps its rows in this dict,
+        features.py:30; its harness tests read it)."""
+        ids = self._stored_ids()
+        if ids.numel() == 0:
+            return {}
+        rows = self.get(ids)[0].cpu().numpy()
+        return {int(i): r for i, r in zip(ids.cpu().numpy().tolist(), rows)}
+
 
 class EdgeFeatureTable(_DeviceTable):
     """features.py:64-120 (append-only, strictly increasing ids; binary-search lookup)."""
