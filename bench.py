@@ -381,6 +381,14 @@ def bench_ours(args, cfg, world, rank, local):
     src, dst, ts = make_stream(cfg, device)
     torch.cuda.synchronize()
     g, ingest_ms = build_graph(cfg, src, dst, ts, world, rank, device)
+    deleted = None
+    if args.deleted:
+        # the general (post-deletion) sampler: soft-delete 1% of the edges (storage.py:479-505); every
+        # later call scans candidate validity (sampling.py:178) instead of the fused fast path
+        gen = torch.Generator(device=device)
+        gen.manual_seed(3)
+        ids = torch.randperm(src.numel(), generator=gen, device=device)[: src.numel() // 100].sort().values
+        deleted = {"edges": int(g.delete_edges(ids)), "sampler": "general path (k_count_general / k_write_general)"}
     roots, rts = roots_for_rank(src, dst, ts, R, rank)
     key_base = rank * R
 
@@ -569,6 +577,7 @@ def bench_ours(args, cfg, world, rank, local):
             "per_policy": per_policy,
             "fetch": fetch,
             "replay": replay,
+            "deleted": deleted,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -581,8 +590,9 @@ def l2_fraction(cfg, info, alg_bytes, ms) -> dict | None:
     """Stores that fit the 126 MB L2 (WIKI/REDDIT shapes) are bound by L2, not HBM, bandwidth: report
     the kernel's algorithmic bytes against the measured L2 read bandwidth (profiles/l2_bandwidth.json,
     scripts/l2bw.cu) next to the HBM fraction."""
-    store_bytes = info.device_bytes
-    if store_bytes > 100e6:
+    # the sampler's working set: 32 B slot records + the int32 timestamp copy + 128 B node records
+    store_bytes = info.slots_allocated * 36 + info.num_nodes * 128
+    if store_bytes > 126e6:
         return None
     p = os.path.join(ROOT, "profiles", "l2_bandwidth.json")
     if not os.path.exists(p):
@@ -770,6 +780,7 @@ def main():
     ap.add_argument("--strong", type=int, default=0, metavar="TOTAL_ROOTS",
                     help="strong scaling: TOTAL_ROOTS split over the ranks (default: 2^20 roots per rank, weak)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--deleted", action="store_true", help="soft-delete 1%% of the edges first (general sampler path)")
     ap.add_argument("--ref-chunk", type=int, default=16)
     args = ap.parse_args()
     rc = self_launch(args)

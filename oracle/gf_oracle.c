@@ -575,6 +575,11 @@ static int64_t sample_one_faithful(const or_graph* g, int64_t node, int64_t t_st
   return k;
 }
 
+/* General-path uniform selection (graphs with deletions): see sample_one_fast */
+#define OR_GEN_EXACT 64
+#define OR_KREJ 32
+#define OR_REJ_TAG (1ull << 40)
+
 /* Early-exit path, same output: position-indexed view of the node list. */
 typedef struct {
   int64_t nb;
@@ -645,6 +650,36 @@ static int64_t sample_one_fast(const or_graph* g, int64_t node, int64_t t_start,
       o_ts[i] = g->edges[h].ts[j];
     }
     return k;
+  }
+  /* with deletions, uniform / time-window over a window of more than GEN_EXACT positions: draw
+   * positions (Philox draws REJ_TAG + d), keep a draw whose candidate is valid and new, stop at
+   * fanout keeps -- a uniform k-subset of the valid candidates (the CUDA general path,
+   * gf_sample.cu k_count_general, makes the same decisions in the same draw order).  After
+   * 8 * fanout + 32 draws without fanout keeps, the exact path below runs. */
+  if (policy != OR_RECENT && hi - lo > OR_GEN_EXACT && fanout <= OR_KREJ) {
+    int64_t npos = hi - lo, dmax = 8 * fanout + 32, acc = 0;
+    for (int64_t d = 0; d < dmax && acc < fanout; d++) {
+      int64_t p = lo + (int64_t)bounded(rand64(seed, qkey, OR_REJ_TAG + (uint64_t)d), (uint64_t)npos);
+      int64_t h, j;
+      nv_at(g, nv, p, &h, &j);
+      const or_edges* e = &g->edges[h];
+      if (!(e->valid[j] && g->node_valid[e->nbr[j]])) continue;
+      int dup = 0;
+      for (int64_t q = 0; q < acc; q++)
+        if (sel[q] == p) { dup = 1; break; }
+      if (!dup) sel[acc++] = p;
+    }
+    if (acc == fanout) {
+      if (!write) return fanout;
+      for (int64_t i = 0; i < fanout; i++) {
+        int64_t h, j;
+        nv_at(g, nv, sel[i], &h, &j);
+        o_nbr[i] = g->edges[h].nbr[j];
+        o_eid[i] = g->edges[h].eid[j];
+        o_ts[i] = g->edges[h].ts[j];
+      }
+      return fanout;
+    }
   }
   /* with deletions: list the valid positions (newest first) */
   int64_t nv_n = 0;
@@ -733,7 +768,9 @@ static void* sl_worker(void* arg) {
       }
     }
     int64_t k;
-    if (t->faithful)
+    /* with deletions the uniform / time-window selection is position-based (rejection draws over
+     * the window, see sample_one_fast), so it runs on the position-indexed view in both modes */
+    if (t->faithful && !(t->any_deleted && t->policy != OR_RECENT))
       k = sample_one_faithful(t->g, t->src[q], t->t_start[q], t->t_end[q], t->fanout, t->policy,
                               t->delta, t->seed, key, &cb, sel, on, oe, ot, write);
     else

@@ -74,7 +74,19 @@ struct QState {
   int64_t* d0;    // directory offset
   int64_t* meta;  // block index of hi-1 (low 32) | num_blocks << 32 | irregular << 63
   int64_t* nv;    // candidates the selection runs over
+  int64_t* sel;   // general uniform path: positions chosen by rejection (fanout per query), nv = -1 marks it
 };
+
+// General-path uniform / time-window selection over a window with deletions: for a
+// window of more than GEN_EXACT positions, positions are drawn uniformly (Philox draws REJ_TAG + d)
+// and a draw is kept when its candidate is valid (valid edge and valid neighbour, sampling.py:178)
+// and new; fanout keeps give a uniform k-subset of the valid candidates.  Only when REJ_MAX draws
+// do not yield them does the exact path run (count every valid candidate, Floyd over their ranks).
+// The oracle (oracle/gf_oracle.c) makes the same decisions.
+constexpr int64_t GEN_EXACT = 64;
+constexpr int KREJ = 32;  // the rejection path serves fanouts up to 32
+constexpr uint64_t REJ_TAG = 1ull << 40;
+__host__ __device__ constexpr int64_t rej_max(int64_t fanout) { return 8 * fanout + 32; }
 
 struct LayerOut {
   const int64_t* offsets;
@@ -676,7 +688,7 @@ struct TileCtl {
 };
 
 // list position -> pool slot for a selected position (regular lists: closed form; else directory)
-__device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
+__device__ __forceinline__ int64_t pool_slot_of64(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
   const int64_t* dd = GV.dir + d0 * DIRW;
   int64_t b, cum;
   if (irregular) {
@@ -686,7 +698,11 @@ __device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irreg
     b = law_block(GV.law, p);
     cum = law_cum(GV.law, b);
   }
-  return (uint32_t)(__ldg(dd + b * DIRW + 2) + (p - cum));
+  return __ldg(dd + b * DIRW + 2) + (p - cum);
+}
+// fused path (pool < 2^32 slots)
+__device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
+  return (uint32_t)pool_slot_of64(GV, irregular, d0, nb, p);
 }
 
 #ifndef GF_FUSED_MINB
@@ -1040,7 +1056,41 @@ __global__ void __launch_bounds__(THREADS) k_count_general(GraphView GV, QueryIn
       lo = (tsr == GF_TS_MIN) ? __ldg(GV.dir + d0 * DIRW + 1) : w_list_lower_bound(GV, d0, nb, ns, tsr).pos;
       hi = h.pos > lo ? h.pos : lo;
       blk = h.blk;
-      if (hi > lo) {
+      bool rej_done = false;
+      if (hi > lo && Q.policy != GF_POLICY_RECENT && hi - lo > GEN_EXACT && Q.fanout <= KREJ) {
+        // rejection draws over the window's positions, 32 at a time, accepted in draw order
+        const uint64_t qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
+        const int64_t npos = hi - lo, dmax = rej_max(Q.fanout);
+        const bool irregular = (GV.nflags[v] & 1) != 0;
+        int64_t chosen = -1;  // lane a holds the a-th accepted position
+        int acc = 0;
+        for (int64_t r0 = 0; r0 < dmax && acc < Q.fanout; r0 += 32) {
+          const int64_t d = r0 + lane;
+          int64_t p = -1;
+          bool ok = false;
+          if (d < dmax) {
+            p = (int64_t)bounded64(rand64(Q.seed, qkey, REJ_TAG + (uint64_t)d), (uint64_t)npos);
+            // deletions leave the block layout on the sizing law until the next allocation
+            ok = slot_ok(GV, load_slot(GV.slots + pool_slot_of64(GV, irregular, d0, nb, lo + p)));
+          }
+          for (int j = 0; j < 32 && acc < Q.fanout; j++) {
+            const int64_t pj = __shfl_sync(0xffffffffu, p, j);
+            const bool okj = __shfl_sync(0xffffffffu, ok, j);
+            const bool dup = __any_sync(0xffffffffu, lane < acc && chosen == pj);
+            if (okj && !dup) {
+              if (lane == acc) chosen = pj;
+              acc++;
+            }
+          }
+        }
+        if (acc == Q.fanout) {
+          rej_done = true;
+          k = acc;
+          nv = -1;
+          if (lane < acc) S.sel[q * Q.fanout + lane] = lo + chosen;
+        }
+      }
+      if (hi > lo && !rej_done) {
         // valid candidates (sampling.py:178); recent needs at most `fanout`
         int64_t limit = (Q.policy == GF_POLICY_RECENT) ? Q.fanout : INT64_MAX;
         int64_t b = blk, p = hi, cnt = 0;
@@ -1081,6 +1131,12 @@ __global__ void __launch_bounds__(THREADS) k_write_general(GraphView GV, QueryIn
     int64_t d0 = GV.dir_off[v], nb = GV.num_blocks[v];
     uint64_t qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
     const int64_t lo = S.lo[q], hi = S.hi[q], nv = S.nv[q];
+    if (nv == -1) {  // positions chosen by the rejection draws of the count pass
+      const bool irregular = (GV.nflags[v] & 1) != 0;
+      for (int64_t i = lane; i < k; i += 32)
+        store_out(O, out + i, load_slot(GV.slots + pool_slot_of64(GV, irregular, d0, nb, S.sel[q * Q.fanout + i])), qkey, i);
+      continue;
+    }
     if (Q.policy == GF_POLICY_RECENT || k == nv) {
       const unsigned lt = (1u << lane) - 1u;
       int64_t b = S.meta[q], p = hi, done = 0;
@@ -1225,10 +1281,12 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   }
   Scratch sb(s);
   Arena A;
-  GF_TRY(sb.alloc((size_t)cap_q * 8 * 8 + 8192));
+  const bool rej = !fast && Q.policy != GF_POLICY_RECENT && Q.fanout <= KREJ;
+  GF_TRY(sb.alloc((size_t)cap_q * 8 * (8 + (rej ? Q.fanout : 0)) + 8192));
   A.base = sb.as<char>();
   QState S{A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q),
-           A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q)};
+           A.take<int64_t>(cap_q), A.take<int64_t>(cap_q), A.take<int64_t>(cap_q),
+           rej ? A.take<int64_t>(cap_q * Q.fanout) : nullptr};
   int64_t* counts = A.take<int64_t>(cap_q);
   if (fast) GF_LAUNCH(k_count_lane, grid_for_queries(cap_q, 1), THREADS, 0, s, GV, Q, S, counts, cap_q);
   else GF_LAUNCH(k_count_general, grid_for_queries(cap_q, 32), THREADS, 0, s, GV, Q, S, counts, cap_q);

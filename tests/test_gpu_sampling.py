@@ -305,3 +305,41 @@ def test_recent_khop_duplicate_heavy_roots_bitwise(cuda_device, tau):
     w = o.sample_layer(roots, np.full(len(roots), TS_MIN), rts, 10, "recent")
     for nm, ww in zip(("offsets", "neighbors", "edge_ids", "timestamps"), w):
         np.testing.assert_array_equal(_host(getattr(lay, nm)), ww)
+
+
+@pytest.mark.parametrize("policy", ["uniform", "time_window"])
+def test_general_path_long_windows_rejection_and_fallback_bitwise(cuda_device, policy):
+    """Post-deletion uniform selection over windows of > 64 positions (gf_sample.cu GEN_EXACT):
+    rejection draws over the positions when deletions are sparse, the exact count + Floyd
+    fallback when most candidates are invalid (a deleted neighbour holding 95% of a hub's
+    edges) -- bitwise vs the oracle, which makes the same decisions."""
+    import paper_2311_17410_b200 as gf
+    from oracle import OracleGraph
+
+    rng = np.random.default_rng(31)
+    n_hub, m = 6, 60_000
+    src = rng.integers(0, n_hub, m)
+    dst = np.where(rng.random(m) < 0.95, n_hub, rng.integers(n_hub + 1, n_hub + 400, m))  # node n_hub dominates
+    ts = np.sort(rng.integers(0, 50_000, m))
+    g = gf.DynamicGraph(directed=True, tau=512)
+    o = OracleGraph(True, 512)
+    for lo in range(0, m, 20_000):
+        g.add_edges_arrays(src[lo:lo + 20_000], dst[lo:lo + 20_000], ts[lo:lo + 20_000])
+        o.add_edges(src[lo:lo + 20_000], dst[lo:lo + 20_000], ts[lo:lo + 20_000])
+    dels = rng.choice(m, m // 50, replace=False)
+    assert g.delete_edges(dels) == o.delete_edges(dels)
+    q = np.repeat(np.arange(n_hub), 400)
+    t1 = rng.integers(10_000, 50_010, len(q))
+    t0 = np.full(len(q), TS_MIN)
+    delta = 40_000
+    pol = gf.SamplingPolicy(policy, delta if policy == "time_window" else 0)
+    for case in ("sparse", "dominant_neighbour_deleted"):
+        if case == "dominant_neighbour_deleted":
+            assert g.delete_node(n_hub) == o.delete_node(n_hub)
+        for f in (1, 10, 25):
+            lay = gf.sample_layer(g, q, t0, t1, f, pol, seed=77 + f)
+            want = o.sample_layer(q, t0, t1, f, policy, delta, seed=77 + f)
+            for nm, w in zip(("offsets", "neighbors", "edge_ids", "timestamps"), want):
+                np.testing.assert_array_equal(getattr(lay, nm), w, err_msg=f"{case} f{f} {nm}")
+            if case == "dominant_neighbour_deleted":
+                assert not np.isin(lay.neighbors, [n_hub]).any()
