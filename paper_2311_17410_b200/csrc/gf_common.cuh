@@ -57,6 +57,37 @@ void prof_stop(const char* name, cudaStream_t s, cudaEvent_t e0);
     }                                                                            \
   } while (0)
 
+// Programmatic dependent launch (PDL) for dependent kernel sequences (the ingest graph): a kernel
+// launched with GF_LAUNCH_PDL may start while its predecessor is still running; it calls
+// gf::pdl_enter() first, which lets its own successor launch early and then waits until the
+// predecessor grid has completed and its writes are visible (griddepcontrol; a no-op for
+// kernels launched without the attribute).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+#define GF_LAUNCH_PDL(kernel, grid, block, smem, strm_, ...)                                     \
+  do {                                                                                            \
+    if ((grid) > 0) {                                                                             \
+      cudaEvent_t _gf_e0 = nullptr;                                                               \
+      if (::gf::g_profile.load(std::memory_order_relaxed)) _gf_e0 = ::gf::prof_start(strm_);     \
+      cudaLaunchConfig_t _gf_cfg = {};                                                            \
+      cudaLaunchAttribute _gf_attr[1];                                                            \
+      _gf_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                        \
+      _gf_attr[0].val.programmaticStreamSerializationAllowed = 1;                                 \
+      _gf_cfg.gridDim = dim3((unsigned)(grid));                                                   \
+      _gf_cfg.blockDim = dim3((unsigned)(block));                                                 \
+      _gf_cfg.dynamicSmemBytes = (smem);                                                          \
+      _gf_cfg.stream = (strm_);                                                                  \
+      _gf_cfg.attrs = _gf_attr;                                                                   \
+      _gf_cfg.numAttrs = 1;                                                                       \
+      GF_CUDA(cudaLaunchKernelEx(&_gf_cfg, kernel, __VA_ARGS__));                                 \
+      ::gf::g_launches.fetch_add(1, std::memory_order_relaxed);                                   \
+      if (_gf_e0) ::gf::prof_stop(#kernel, strm_, _gf_e0);                                       \
+    }                                                                                             \
+  } while (0)
+
 inline void init_device_pool(int dev);
 
 struct DeviceGuard {

@@ -71,6 +71,7 @@ gf_status grow_array(T*& p, int64_t keep, int64_t new_cap, cudaStream_t s) {
 // one event per (edge, stored endpoint), in the reference's append order
 __global__ void k_make_events(const int64_t* __restrict__ rec, int64_t n, int directed, uint32_t* keys, uint32_t* vals,
                               const IngestCounters* c, longlong2* trig) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   int64_t E = directed ? n : 2 * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
@@ -91,6 +92,7 @@ __device__ __forceinline__ int64_t node_tmax(const int64_t* tail, const int64_t*
 }
 
 __global__ void k_heads(const uint32_t* __restrict__ keys, int64_t E, int32_t* heads) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x)
     heads[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
 }
@@ -99,6 +101,7 @@ __global__ void k_heads(const uint32_t* __restrict__ keys, int64_t E, int32_t* h
 __global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl,
                            int64_t E, int directed, const int64_t* __restrict__ rec, const int64_t* tail, const int64_t* bsize,
                            const int64_t* btmax, int64_t* seg_start, IngestCounters* c) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t s = incl[i] - 1;
@@ -125,6 +128,7 @@ __global__ void k_segments(const uint32_t* __restrict__ keys, const uint32_t* __
 __global__ void k_compact(const uint32_t* __restrict__ vals, const int32_t* __restrict__ incl, const int64_t* __restrict__ cpos,
                           const int64_t* __restrict__ keep, const int64_t* __restrict__ seg_start, int64_t E,
                           const IngestCounters* c, uint32_t* ce_ev, int64_t* ce_pend, int32_t* ce_seg) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   int64_t nseg = c->num_segs;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
@@ -160,6 +164,7 @@ __global__ void k_plan(const uint32_t* __restrict__ keys, const int64_t* __restr
                        const IngestCounters* c, const int64_t* tail, const int64_t* bsize, const int64_t* bcap,
                        const int64_t* degree, const int64_t* num_blocks, const int64_t* dir_cap, int kind, int64_t tau,
                        int64_t param, SegPlan P, int64_t* old_tail) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   const int64_t nseg = c->num_segs;
   // the per-segment plan scan covers num_segs + 1 entries: only the last needs a zero
@@ -305,6 +310,7 @@ gf_status ensure_dir(gf_graph* g, int64_t need, cudaStream_t s) {
 __global__ void k_grow_nodes(IngestCounters* c, const IngestScalars* S, int64_t cap, int64_t* head, int64_t* tail,
                              int64_t* nb, int64_t* deg, uint8_t* valid, int64_t* nslots, int64_t* doff, int64_t* dcap,
                              uint8_t* nflags, int64_t* nrec) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   const int64_t lo = S->num_nodes;
   const long long hi = c->maxv + 1;
   if (c->minv < 0 || hi > cap) {
@@ -358,6 +364,7 @@ __device__ __forceinline__ void st_flag(int* p, int v) {
 template <int K, int SCAN_ITEMS>
 __global__ void __launch_bounds__(SCAN_T) k_scan_sum(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
                                                       ScanState S, const IngestCounters* c, bool per_segment) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   __shared__ unsigned s_tile;
   __shared__ int64_t s_w[SCAN_T / 32][K];
   __shared__ int64_t s_base[K];
@@ -463,6 +470,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_sum(const int64_t* __restrict__
 // ---- fused kernels of the sync-free path -------------------------------------
 // staging + batch min/max (the counters were initialised by the H2D copy that starts the sequence)
 __global__ void k_stage_minmax(const IngestScalars* S, int64_t n, int64_t* rec, IngestCounters* c, int* zero, int64_t nzero) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nzero; j += (int64_t)gridDim.x * blockDim.x)
     zero[j] = 0;  // look-back scan flags and tickets of this launch sequence
   const bool has_eids = S->eids_in != nullptr;
@@ -511,6 +519,7 @@ __global__ void k_stage_minmax(const IngestScalars* S, int64_t n, int64_t* rec, 
 __global__ void k_accept(uint8_t* acc, int64_t n, int64_t* tm, const int64_t* tail, const int64_t* bsize,
                          const int64_t* btmax, const IngestCounters* c, const IngestScalars* S, const int64_t* rec,
                          int directed) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   if (!c->viol) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) acc[j] = 1;
@@ -536,6 +545,7 @@ __global__ void k_accept(uint8_t* acc, int64_t n, int64_t* tm, const int64_t* ta
 __global__ void k_eids_keep(const uint8_t* __restrict__ acc, const int64_t* __restrict__ rank, int64_t n,
                             bool has_eids, int64_t* rec, IngestCounters* c, const IngestScalars* S,
                             const uint32_t* __restrict__ vals, int64_t E, int directed, int64_t* keep) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   const int64_t next_id = S->next_edge_id;
   long long mx = LLONG_MIN;
@@ -561,6 +571,7 @@ __global__ void k_check_enumerate(const longlong4* __restrict__ off4, int64_t E,
                                   const int64_t* __restrict__ ce_pend, const uint32_t* __restrict__ ce_ev, SegPlan P,
                                   const uint32_t* __restrict__ keys, const int64_t* __restrict__ seg_start,
                                   const int64_t* degree, int kind, int64_t tau, int64_t param, Recs R, longlong2* trig) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t ns = c->num_segs;  // off4 holds the scan up to num_segs (the total)
@@ -603,6 +614,7 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
                          const longlong2* __restrict__ tscan, const uint32_t* __restrict__ ce_ev,
                          const int64_t* __restrict__ rec, int directed, const int64_t* __restrict__ old_tail, NodeArrays N,
                          BlockArrays B, DirArrays D, int kind) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used, nfree = S->nfree;
   const int64_t* __restrict__ freel = S->free_list;
@@ -703,6 +715,7 @@ __global__ void __launch_bounds__(256, 8)
                    const int32_t* __restrict__ ce_seg, const int64_t* __restrict__ rec, int directed,
                    const int64_t* __restrict__ old_tail, const int64_t* __restrict__ bbase, Slot* slots, int64_t* sts,
                    int64_t* fts, int32_t* sts32, int32_t* fts32) {
+  pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   const int64_t slots_used = S->slots_used;
   const int64_t nseg = c->num_segs;
@@ -907,43 +920,43 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       size_t tb = cub_bytes;
       GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
       GF_CUDA(cudaMemcpyAsync(dc, hci, sizeof(IngestCounters), cudaMemcpyHostToDevice, s));
-      GF_LAUNCH(k_stage_minmax, grid_for(std::max(n, nzero), T, G), T, 0, s, ds, n, rec, dc, zero, nzero);
-      GF_LAUNCH(k_grow_nodes, grid_for(2 * n, T, G), T, 0, s, dc, ds, node_cap, g->head, g->tail, g->num_blocks,
+      GF_LAUNCH_PDL(k_stage_minmax, grid_for(std::max(n, nzero), T, G), T, 0, s, ds, n, rec, dc, zero, nzero);
+      GF_LAUNCH_PDL(k_grow_nodes, grid_for(2 * n, T, G), T, 0, s, dc, ds, node_cap, g->head, g->tail, g->num_blocks,
                 g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap, g->nflags, g->nrec);
-      GF_LAUNCH(k_make_events, grid_for(E, T, G), T, 0, s, rec, n, dir, keys_in, vals_in, dc, trig);
+      GF_LAUNCH_PDL(k_make_events, grid_for(E, T, G), T, 0, s, rec, n, dir, keys_in, vals_in, dc, trig);
       GF_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, tb, keys_in, keys, vals_in, vals, (int)E, 0, endbit, s));
-      GF_LAUNCH(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
+      GF_LAUNCH_PDL(k_heads, grid_for(E, T, G), T, 0, s, keys, E, heads);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::InclusiveSum(cubtmp, tb, heads, incl, (int)E, s));
-      GF_LAUNCH(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, rec, g->tail, g->bsize, g->btmax,
+      GF_LAUNCH_PDL(k_segments, grid_for(E, T, G), T, 0, s, keys, vals, incl, E, dir, rec, g->tail, g->bsize, g->btmax,
                 seg_start, dc);
-      GF_LAUNCH(k_accept, grid_for(n, T, G), T, 0, s, acc, n, tm, g->tail, g->bsize, g->btmax, dc, ds, rec, dir);
+      GF_LAUNCH_PDL(k_accept, grid_for(n, T, G), T, 0, s, acc, n, tm, g->tail, g->bsize, g->btmax, dc, ds, rec, dir);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, acc, rank, (int)n, s));
-      GF_LAUNCH(k_eids_keep, grid_for(std::max(n, E), T, G), T, 0, s, acc, rank, n, eids_user != nullptr, rec, dc, ds, vals, E,
+      GF_LAUNCH_PDL(k_eids_keep, grid_for(std::max(n, E), T, G), T, 0, s, acc, rank, n, eids_user != nullptr, rec, dc, ds, vals, E,
                 dir, keep);
       tb = cub_bytes;
       GF_CUDA(cub::DeviceScan::ExclusiveSum(cubtmp, tb, keep, cpos, (int)(E + 1), s));
-      GF_LAUNCH(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
-      GF_LAUNCH(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize,
+      GF_LAUNCH_PDL(k_compact, grid_for(E, T, G), T, 0, s, vals, incl, cpos, keep, seg_start, E, dc, ce_ev, ce_pend, ce_seg);
+      GF_LAUNCH_PDL(k_plan, grid_for(E + 1, T, G), T, 0, s, keys, seg_start, cpos, ce_pend, E, dc, g->tail, g->bsize,
                 g->bcap, g->degree, g->num_blocks, g->dir_cap, g->sizing_kind, g->tau, g->sizing_param, P, old_tail);
       if (E >= SCAN_LARGE_EVENTS)
-        GF_LAUNCH((k_scan_sum<4, SCAN_ITEMS_LARGE>), tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
+        GF_LAUNCH_PDL((k_scan_sum<4, SCAN_ITEMS_LARGE>), tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
       else
-        GF_LAUNCH((k_scan_sum<4, SCAN_ITEMS_SMALL>), tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
-      GF_LAUNCH(k_check_enumerate, grid_for(E, T, G), T, 0, s, off4, E, ds, dc, ce_pend, ce_ev, P, keys, seg_start,
+        GF_LAUNCH_PDL((k_scan_sum<4, SCAN_ITEMS_SMALL>), tiles4, SCAN_T, 0, s, (const int64_t*)P.plan4, (int64_t*)off4, E + 1, S4, dc, true);
+      GF_LAUNCH_PDL(k_check_enumerate, grid_for(E, T, G), T, 0, s, off4, E, ds, dc, ce_pend, ce_ev, P, keys, seg_start,
                 g->degree, g->sizing_kind, g->tau, g->sizing_param, R, trig);
       if (E >= SCAN_LARGE_EVENTS)
-        GF_LAUNCH((k_scan_sum<2, SCAN_ITEMS_LARGE>), tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
+        GF_LAUNCH_PDL((k_scan_sum<2, SCAN_ITEMS_LARGE>), tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
       else
-        GF_LAUNCH((k_scan_sum<2, SCAN_ITEMS_SMALL>), tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
+        GF_LAUNCH_PDL((k_scan_sum<2, SCAN_ITEMS_SMALL>), tiles2, SCAN_T, 0, s, (const int64_t*)trig, (int64_t*)tscan, E, S2, dc, false);
       NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
                    g->nflags, g->nrec};
       BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
       DirArrays D{g->dir};
-      GF_LAUNCH(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, rec, dir,
+      GF_LAUNCH_PDL(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, rec, dir,
                 old_tail, N, B, D, g->sizing_kind);
-      GF_LAUNCH(k_commit_slots, grid_for(E, T, 16 * num_sms()), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan,
+      GF_LAUNCH_PDL(k_commit_slots, grid_for(E, T, 16 * num_sms()), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan,
                 ce_ev, ce_seg, rec, dir, old_tail, g->bbase, g->slots, g->sts,
                 g->fts, g->sts32, g->fts32);
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
