@@ -44,6 +44,27 @@
 #ifndef GF_AB_NOSTORE
 #define GF_AB_NOSTORE 0
 #endif
+// measurement only: per-tile phase timestamps of the fused kernel (globaltimer, ns)
+#ifndef GF_AB_TRACE
+#define GF_AB_TRACE 0
+#endif
+#if GF_AB_TRACE
+constexpr int TRACE_TILES = 1 << 18;
+__device__ unsigned long long g_trace[TRACE_TILES][5];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GF_TRACE(tile, i)                                                   \
+  do {                                                                      \
+    if (threadIdx.x == 0 && (tile) < TRACE_TILES) g_trace[tile][i] = gtimer(); \
+  } while (0)
+#else
+#define GF_TRACE(tile, i) \
+  do {                    \
+  } while (0)
+#endif
 
 using namespace gf;
 
@@ -787,6 +808,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   const int64_t n = query_count(Q);
   if (tile * FT >= n) return;
   const int64_t q = tile * FT + threadIdx.x;
+  GF_TRACE(tile, 0);
 
   // ---- node record + boundary block; the count is often known here already ----
   int k = 0;
@@ -853,6 +875,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   const bool early = EARLY && __syncthreads_and(known);
   if (early) tile_publish<NW>(k, lane, w, s_wsum, C, tile, incl, wpre, agg);
 
+  GF_TRACE(tile, 1);
   if (EARLY && live) finish();
   if (!early) tile_publish<NW>(k, lane, w, s_wsum, C, tile, incl, wpre, agg);
 
@@ -925,6 +948,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   };
   const int total = __shfl_sync(0xffffffffu, incl, 31);  // the warp's outputs
 
+  GF_TRACE(tile, 2);
   // ---- decoupled look-back: output base of this tile ----
   if (w == 0) {
     int64_t excl = 0;
@@ -951,6 +975,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
   }
   __syncthreads();
   const int64_t base = s_base;
+  GF_TRACE(tile, 3);
   const int64_t out = base + wpre + pre;
   if (q < n) {
     const_cast<int64_t*>(O.offsets)[q + 1] = out + k;
@@ -991,6 +1016,9 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
     store_out(O, out0 + e, GF_LOAD_OUT(slot_of(jj, i)), s_key[w][jj], i);
   }
 #undef GF_LOAD_OUT
+#if GF_AB_TRACE
+  if (lane == 0 && tile < TRACE_TILES) atomicMax(&g_trace[tile][4], gtimer());
+#endif
 }
 
 // ========================== general path (deletions) =========================
@@ -1305,6 +1333,18 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
 }  // namespace
 
 extern "C" {
+
+#if GF_AB_TRACE
+// measurement-only export of the A/B trace variant (not in include/gfb200.h)
+__attribute__((visibility("default"))) int gf_ab_trace_dump(unsigned long long* host, int tiles) {
+  if (tiles > TRACE_TILES) tiles = TRACE_TILES;
+  return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 5 * (size_t)tiles);
+}
+__attribute__((visibility("default"))) int gf_ab_trace_clear() {
+  static unsigned long long z[TRACE_TILES][5];
+  return (int)cudaMemcpyToSymbol(g_trace, z, sizeof(z));
+}
+#endif
 
 gf_status gf_sample_layer(gf_graph* g, const int64_t* d_src, const int64_t* d_t_start, const int64_t* d_t_end, int64_t n,
                           int64_t fanout, int policy, int64_t delta, uint64_t seed, const uint64_t* d_keys,
