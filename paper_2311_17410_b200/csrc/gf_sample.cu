@@ -947,6 +947,33 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
     return s_sel[EARLY ? 0 : w][j][(i + j) & (KMAX - 1)];
   };
   const int total = __shfl_sync(0xffffffffu, incl, 31);  // the warp's outputs
+  // ---- cooperative gather + CSR store of the warp's contiguous range ----
+  // recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
+  // (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
+  // choice is the faster one for its policy)
+// recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
+// (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
+// choice is the faster one for its policy; SoA copies of the columns made the recent runs cost more
+// lines on deep-boundary roots, profiles/README.md)
+#if GF_AB_NOGATHER
+#define GF_LOAD_OUT(sl) (O.last_hop ? Slot{(int64_t)(sl), 1, 2, 3, 1, 0} : (EARLY ? load_out3(GV.slots + (sl)) : load_slot(GV.slots + (sl))))
+#else
+#define GF_LOAD_OUT(sl) (EARLY ? load_out3(GV.slots + (sl)) : load_slot(GV.slots + (sl)))
+#endif
+  // the first gather round is issued before the look-back barrier: its record loads (which need no
+  // output base) are in flight while warp 0 resolves the tile's base
+  __syncwarp();
+  Slot s0[GU];
+  int j0[GU];
+  int e = lane;
+  const bool round0 = e + 32 * (GU - 1) < total;
+  if (round0) {
+#pragma unroll
+    for (int u = 0; u < GU; u++) {
+      j0[u] = s_owner[w][e + 32 * u];
+      s0[u] = GF_LOAD_OUT(slot_of(j0[u], e + 32 * u - s_pre[w][j0[u]]));
+    }
+  }
 
   GF_TRACE(tile, 2);
   // ---- decoupled look-back: output base of this tile ----
@@ -982,22 +1009,13 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
     if (q == n - 1) *C.total = out + k;
   }
 
-  // ---- cooperative gather + CSR store of the warp's contiguous range ----
-  // recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
-  // (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
-  // choice is the faster one for its policy)
-// recent (contiguous, L2-friendly records): the three output fields with narrow loads; uniform
-// (one random line per record): one 256-bit evict-first load, so the line leaves L2 early (A/B: each
-// choice is the faster one for its policy; SoA copies of the columns made the recent runs cost more
-// lines on deep-boundary roots, profiles/README.md)
-#if GF_AB_NOGATHER
-#define GF_LOAD_OUT(sl) (O.last_hop ? Slot{(int64_t)(sl), 1, 2, 3, 1, 0} : (EARLY ? load_out3(GV.slots + (sl)) : load_slot(GV.slots + (sl))))
-#else
-#define GF_LOAD_OUT(sl) (EARLY ? load_out3(GV.slots + (sl)) : load_slot(GV.slots + (sl)))
-#endif
   const int64_t out0 = base + wpre;
-  __syncwarp();
-  int e = lane;
+  if (round0) {
+#pragma unroll
+    for (int u = 0; u < GU; u++)
+      store_out(O, out0 + e + 32 * u, s0[u], s_key[w][j0[u]], e + 32 * u - s_pre[w][j0[u]]);
+    e += 32 * GU;
+  }
   for (; e + 32 * (GU - 1) < total; e += 32 * GU) {
     Slot s[GU];
     int j[GU];
