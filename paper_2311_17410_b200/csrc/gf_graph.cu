@@ -12,17 +12,20 @@
 //   freed by offload are reused LIFO first) -> metadata/directory/slot writes.
 // Nothing is read back mid-call (see add_edges_fast), and the launch sequence
 // is replayed as a CUDA graph.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <string.h>
 
 #include <algorithm>
 #include <chrono>
+#include <tuple>
 #include <vector>
 
 #include "gf_graph.cuh"
 
 using namespace gf;
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -42,8 +45,12 @@ struct IngestCounters {
   long long max_eid;      // max preassigned accepted id
   long long abort;        // sync-free path: ABORT_* bits, nothing was mutated
   long long tsmin, tsmax; // timestamp range of the batch (32-bit fence validity)
+  long long num_big;      // cooperative path: segments with more than 32 events
+  long long phase_ns[12]; // cooperative path: globaltimer at each phase start (GF_INGEST_TIMING)
 };
-constexpr long long ABORT_NODES = 1, ABORT_CAP = 2;
+// ABORT_SLOW (cooperative path only): the batch needs the general launch sequence -- an endpoint
+// may see a decreasing timestamp (possible rejection), or a segment exceeds what one CTA sorts
+constexpr long long ABORT_NODES = 1, ABORT_CAP = 2, ABORT_SLOW = 4;
 
 // per-call values of the sync-free path, read on the device so that its captured launch
 // sequence can be replayed unchanged (one H2D copy of this struct per call)
@@ -605,6 +612,114 @@ __global__ void k_check_enumerate(const longlong4* __restrict__ off4, int64_t E,
   }
 }
 
+// One segment's commit (shared by k_commit and the cooperative path): its new blocks (handle and
+// slot base from the allocation order), the directory, the node row and its NodeRec.
+//   ev_ts(r): timestamp of the segment's r-th accepted event
+//   blk(k):   NewBlk of the segment's k-th new block
+struct NewBlk {
+  int64_t h, base, first, count, cap;
+};
+template <class EvTs, class Blk>
+__device__ __forceinline__ void commit_segment(int64_t v, int64_t cnt, int64_t t, int64_t fill, int64_t nb, int64_t dnew,
+                                               int64_t dir_new_off, int64_t tail_size, EvTs ev_ts, Blk blk,
+                                               const NodeArrays& N, const BlockArrays& B, const DirArrays& D, int kind) {
+  const int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v], deg_old = N.degree[v], oo = N.dir_off[v];
+  const int64_t doff = dnew > 0 ? dir_new_off : oo;
+  const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? ev_ts(fill - 1) : 0;
+  // the node's directory moves to a larger region when it grows past its capacity
+  if (nb > 0 && dnew > 0)
+    for (int64_t w = 0; w < nb_old * DIRW; w++) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
+  int64_t h_first = GF_NO_BLOCK, h_last = GF_NO_BLOCK, tmin_last = 0, tmax_last = 0, base_last = 0;
+  int64_t h_prev = t;
+  for (int64_t k = 0; k < nb; k++) {
+    const NewBlk nbk = blk(k);
+    const int64_t h = nbk.h;
+    const int64_t tmin = ev_ts(nbk.first), tmax = ev_ts(nbk.first + nbk.count - 1);
+    B.cap[h] = nbk.cap;
+    B.size[h] = nbk.count;
+    B.tmin[h] = tmin;
+    B.tmax[h] = tmax;
+    B.base[h] = nbk.base;
+    B.prev[h] = h_prev;
+    B.next[h] = GF_NO_BLOCK;
+    if (k > 0) B.next[h_prev] = h;
+    int64_t* e = D.e + (doff + nb_old + k) * DIRW;
+    e[0] = tmin;
+    e[1] = ns_old + nbk.first;
+    e[2] = nbk.base;
+    e[3] = tmax;
+    if (k == 0) h_first = h;
+    h_prev = h;
+    h_last = h;
+    tmin_last = tmin;
+    tmax_last = tmax;
+    base_last = nbk.base;
+  }
+  // a block allocated while live degree != slots written (a deletion happened) or by
+  // batch sizing leaves the closed-form position -> block law (SizingLaw)
+  if (nb > 0 && (kind == GF_SIZING_BATCH || deg_old != ns_old)) N.nflags[v] |= 1;
+  int64_t tl_tmin = 0, tl_tmax = 0, tl_base = 0;
+  if (t != GF_NO_BLOCK) {
+    tl_tmin = B.tmin[t];
+    tl_base = B.base[t];
+    tl_tmax = fill > 0 ? t_tmax : B.tmax[t];
+  }
+  if (t != GF_NO_BLOCK && fill > 0) {
+    B.size[t] = tail_size + fill;
+    B.tmax[t] = t_tmax;
+    D.e[(doff + nb_old - 1) * DIRW + 3] = t_tmax;  // old tail grew
+  }
+  if (nb > 0) {
+    if (t == GF_NO_BLOCK) N.head[v] = h_first;
+    else B.next[t] = h_first;
+    tl_tmin = tmin_last;
+    tl_tmax = tmax_last;
+    tl_base = base_last;
+    N.tail[v] = h_last;
+    if (dnew > 0) {
+      N.dir_off[v] = doff;
+      N.dir_cap[v] = dnew;
+    }
+  }
+  const int64_t nbt = nb_old + nb;
+  N.num_blocks[v] = nbt;
+  N.degree[v] = deg_old + cnt;
+  N.nslots[v] = ns_old + cnt;
+  int64_t* rr = N.nrec + v * NREC;
+  rr[0] = doff;
+  rr[1] = ns_old + cnt;
+  rr[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
+  rr[3] = D.e[doff * DIRW + 1];
+  rr[4] = D.e[(doff + nbt - 1) * DIRW + 1];
+  rr[5] = tl_base;
+  rr[6] = tl_tmin;
+  rr[7] = tl_tmax;
+  rr[8] = D.e[doff * DIRW];
+}
+
+struct SlotArrays {
+  Slot* slots;
+  int64_t *sts, *fts;
+  int32_t *sts32, *fts32;
+};
+
+// one slot record plus its timestamp copies and fences
+__device__ __forceinline__ void write_slot(const SlotArrays& SA, int64_t pos, int64_t ts, int64_t eid, int32_t nbr, int32_t owner) {
+  Slot sl;
+  sl.ts = ts;
+  sl.eid = eid;
+  sl.nbr = nbr;
+  sl.owner = owner;
+  sl.valid = 1;
+  sl.pad = 0;
+  SA.slots[pos] = sl;
+  SA.sts[pos] = ts;
+  if ((pos & (FENCE - 1)) == 0) SA.fts[pos / FENCE] = ts;
+  const int32_t t32 = (int32_t)max(min(ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);  // exact while ts32
+  SA.sts32[pos] = t32;
+  if ((pos & (FENCE32 - 1)) == 0) SA.fts32[pos / FENCE32] = t32;
+}
+
 // The commit: one THREAD per segment writes its new blocks (handle and slot base from the trigger
 // scan), the directory, the node and its NodeRec (a warp per segment serialised millions of
 // segments per warp at 10M-edge batches); one thread per accepted event writes its slot.
@@ -624,85 +739,15 @@ __global__ void k_commit(const IngestCounters* c, const IngestScalars* S, const 
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cnt = P.acc_cnt[s];
     if (!cnt) continue;
-    const int64_t v = keys[seg_start[s]];
-    const int64_t t = old_tail[s], fill = P.fill[s], nb = P.nb_new[s], cs = P.cstart[s];
-    const int64_t nb_old = N.num_blocks[v], ns_old = N.nslots[v], deg_old = N.degree[v], oo = N.dir_off[v];
-    const int64_t dnew = P.plan4[s].z, r0 = off4[s].x;
-    const int64_t doff = dnew > 0 ? dir_used + off4[s].z : oo;
-    const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? rec[ER * ev_edge(ce_ev[cs + fill - 1], directed) + ER_TS] : 0;
-    // the node's directory moves to a larger region when it grows past its capacity
-    if (nb > 0 && dnew > 0)
-      for (int64_t w = 0; w < nb_old * DIRW; w++) D.e[doff * DIRW + w] = D.e[oo * DIRW + w];
-    int64_t h_first = GF_NO_BLOCK, h_last = GF_NO_BLOCK, tmin_last = 0, tmax_last = 0, base_last = 0;
-    int64_t h_prev = t;
-    for (int64_t k = 0; k < nb; k++) {
+    const int64_t cs = P.cstart[s], r0 = off4[s].x;
+    auto ev_ts = [&](int64_t r) { return rec[ER * ev_edge(ce_ev[cs + r], directed) + ER_TS]; };
+    auto blk = [&](int64_t k) {
       const int64_t r = r0 + k;
       const longlong2 tr = tscan[R.key[r]];
-      const int64_t h = handle_of(tr.x), base = slots_used + tr.y;
-      const int64_t f = R.first[r], n_in = R.count[r];
-      const int64_t tmin = rec[ER * ev_edge(ce_ev[cs + f], directed) + ER_TS];
-      const int64_t tmax = rec[ER * ev_edge(ce_ev[cs + f + n_in - 1], directed) + ER_TS];
-      B.cap[h] = R.cap[r];
-      B.size[h] = n_in;
-      B.tmin[h] = tmin;
-      B.tmax[h] = tmax;
-      B.base[h] = base;
-      B.prev[h] = h_prev;
-      B.next[h] = GF_NO_BLOCK;
-      if (k > 0) B.next[h_prev] = h;
-      int64_t* e = D.e + (doff + nb_old + k) * DIRW;
-      e[0] = tmin;
-      e[1] = ns_old + f;
-      e[2] = base;
-      e[3] = tmax;
-      if (k == 0) h_first = h;
-      h_prev = h;
-      h_last = h;
-      tmin_last = tmin;
-      tmax_last = tmax;
-      base_last = base;
-    }
-    // a block allocated while live degree != slots written (a deletion happened) or by
-    // batch sizing leaves the closed-form position -> block law (SizingLaw)
-    if (nb > 0 && (kind == GF_SIZING_BATCH || deg_old != ns_old)) N.nflags[v] |= 1;
-    int64_t tl = t, tl_tmin = 0, tl_tmax = 0, tl_base = 0;
-    if (t != GF_NO_BLOCK) {
-      tl_tmin = B.tmin[t];
-      tl_base = B.base[t];
-      tl_tmax = fill > 0 ? t_tmax : B.tmax[t];
-    }
-    if (t != GF_NO_BLOCK && fill > 0) {
-      B.size[t] = P.tail_size[s] + fill;
-      B.tmax[t] = t_tmax;
-      D.e[(doff + nb_old - 1) * DIRW + 3] = t_tmax;  // old tail grew
-    }
-    if (nb > 0) {
-      if (t == GF_NO_BLOCK) N.head[v] = h_first;
-      else B.next[t] = h_first;
-      tl = h_last;
-      tl_tmin = tmin_last;
-      tl_tmax = tmax_last;
-      tl_base = base_last;
-      N.tail[v] = tl;
-      if (dnew > 0) {
-        N.dir_off[v] = doff;
-        N.dir_cap[v] = dnew;
-      }
-    }
-    const int64_t nbt = nb_old + nb;
-    N.num_blocks[v] = nbt;
-    N.degree[v] = deg_old + cnt;
-    N.nslots[v] = ns_old + cnt;
-    int64_t* rr = N.nrec + v * NREC;
-    rr[0] = doff;
-    rr[1] = ns_old + cnt;
-    rr[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((N.nflags[v] & 1) ? NREC_IRREG : 0);
-    rr[3] = D.e[doff * DIRW + 1];
-    rr[4] = D.e[(doff + nbt - 1) * DIRW + 1];
-    rr[5] = tl_base;
-    rr[6] = tl_tmin;
-    rr[7] = tl_tmax;
-    rr[8] = D.e[doff * DIRW];
+      return NewBlk{handle_of(tr.x), slots_used + tr.y, R.first[r], R.count[r], R.cap[r]};
+    };
+    commit_segment(keys[seg_start[s]], cnt, old_tail[s], P.fill[s], P.nb_new[s], P.plan4[s].z, dir_used + off4[s].z,
+                   P.tail_size[s], ev_ts, blk, N, B, D, kind);
   }
 }
 
@@ -713,8 +758,7 @@ __global__ void __launch_bounds__(256, 8)
                    const int64_t* __restrict__ seg_start, SegPlan P, const longlong4* __restrict__ off4, Recs R,
                    const longlong2* __restrict__ tscan, const uint32_t* __restrict__ ce_ev,
                    const int32_t* __restrict__ ce_seg, const int64_t* __restrict__ rec, int directed,
-                   const int64_t* __restrict__ old_tail, const int64_t* __restrict__ bbase, Slot* slots, int64_t* sts,
-                   int64_t* fts, int32_t* sts32, int32_t* fts32) {
+                   const int64_t* __restrict__ old_tail, const int64_t* __restrict__ bbase, SlotArrays SA) {
   pdl_enter();  // PDL: launched early by the previous kernel of the ingest graph
   if (c->abort) return;
   const int64_t slots_used = S->slots_used;
@@ -740,20 +784,605 @@ __global__ void __launch_bounds__(256, 8)
       pos = slots_used + tscan[R.key[lo]].y + (r - R.first[lo]);
     }
     const longlong4 er = reinterpret_cast<const longlong4*>(rec)[j];  // one sector
-    Slot sl;
-    sl.ts = er.z;
-    sl.eid = er.w;
-    sl.nbr = (int32_t)(side ? er.x : er.y);
-    sl.owner = (int32_t)keys[seg_start[sg]];
-    sl.valid = 1;
-    sl.pad = 0;
-    slots[pos] = sl;
-    sts[pos] = sl.ts;
-    if ((pos & (FENCE - 1)) == 0) fts[pos / FENCE] = sl.ts;
-    const int32_t t32 = (int32_t)max(min(sl.ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);  // exact while ts32
-    sts32[pos] = t32;
-    if ((pos & (FENCE32 - 1)) == 0) fts32[pos / FENCE32] = t32;
+    write_slot(SA, pos, er.z, er.w, (int32_t)(side ? er.x : er.y), (int32_t)keys[seg_start[sg]]);
   }
+}
+
+// ---- cooperative single-launch ingest (the common case) ----------------------------
+// One cooperative kernel replaces the ~20-node launch sequence when the batch can be planned
+// without the rejection machinery (K1).  Its phases are separated by grid barriers:
+//   A  stage the edge records; node / timestamp / id ranges; per-node event counts (persistent
+//      zeroed counters; one atomic per node per 1024-event sub-chunk, aggregated in a shared-memory
+//      hash) and the list of touched nodes, one segment each, in first-touch order
+//   C  rows of new nodes; segment starts: a grid scan of the counts
+//   D  events scattered into their segments (the same aggregation; the counters count back to 0)
+//   E  each segment's events sorted by event index -- a warp bitonic sort up to 32 events, a rank
+//      count up to 1024, a CTA radix sort up to CO_SORT -- so a segment lists its node's events in
+//      append order
+//   F  chronology check (any endpoint that could see a decreasing timestamp sends the batch to the
+//      general sequence, storage.py:426-437); per-segment block plan (storage.py:449-459), which marks
+//      the events that allocate, inside the reduce pass of its grid scan; then a grid scan over the
+//      events in event order gives each new block its handle rank and slot base (the reference's
+//      allocation order)
+//   I  commit: blocks, directory, node rows, NodeRecs (a thread per segment), slots (a thread per
+//      event; both walk the capacity law again instead of storing per-block records), edge ids
+// Nothing is mutated before phase I except the rows of new nodes, which the general sequence
+// initialises the same way, so every abort leaves the store as it was.
+constexpr int CO_T = 1024;                  // threads per CTA
+constexpr int CO_ITEMS = 8;                 // CTA radix sort: CO_T x CO_ITEMS keys
+constexpr int CO_SORT = CO_T * CO_ITEMS;    // events per segment on this path
+constexpr int CO_BITMAP_WORDS = 8 * CO_T;   // E-phase bitmap: batches of up to 2^18 events
+constexpr int64_t CO_MAX_EVENTS = 1 << 22;
+
+
+struct CoopBufs {
+  uint32_t* sev;      // [E] event index per sorted position (segment-major, append order inside)
+  int32_t* sseg;      // [E] segment of each sorted position
+  int32_t* touched;   // [E] node of each segment
+  int32_t* sstart;    // [E + 1] segment starts
+  int32_t* big;       // [E] segments with more than 32 events
+  int64_t* ctot;      // [grid * 8] per-CTA partial sums of the grid scans
+  int64_t *fill, *tail_size, *old_tail, *nb_new, *deg0;  // [E] per segment
+  longlong4 *plan4, *off4;                                // [E + 1] per segment
+  int64_t *trig, *trank, *tbase;  // [E] per event: capacity of the block it allocates (0: none), rank, slot base
+  int32_t *ncnt, *nseg;           // per node (persistent)
+};
+
+template <class T>
+__device__ __forceinline__ T ldl2(const T* p) { return __ldcg(p); }
+
+__device__ __forceinline__ long long gtimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define COOP_MARK(i)                                            \
+  do {                                                          \
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->phase_ns[i] = gtimer_ns(); \
+  } while (0)  // data another CTA wrote in this launch
+
+// exclusive scan of K int64 fields over the CTA (CO_T threads); returns the CTA total.  sm holds
+// 33 rows: the 32 warp totals, scanned in place by warp 0, and the CTA total.
+template <int K>
+__device__ __forceinline__ void cta_scan(const int64_t (&x)[K], int64_t (&excl)[K], int64_t (&tot)[K], int64_t (*sm)[K]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t inc[K];
+#pragma unroll
+  for (int f = 0; f < K; f++) {
+    int64_t v = x[f];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    inc[f] = v;
+  }
+  __syncthreads();  // sm may still be read by a previous call
+  if (lane == 31)
+#pragma unroll
+    for (int f = 0; f < K; f++) sm[w][f] = inc[f];
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int f = 0; f < K; f++) {
+      const int64_t y = sm[lane][f];
+      int64_t v = y;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t z = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += z;
+      }
+      sm[lane][f] = v - y;  // exclusive prefix of the warp totals
+      if (lane == 31) sm[32][f] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int f = 0; f < K; f++) {
+    excl[f] = sm[w][f] + inc[f] - x[f];
+    tot[f] = sm[32][f];
+  }
+}
+
+// Grid-wide exclusive scan (reduce, barrier, scan) of n items of K fields: val1(i, out[K]) gives
+// item i in the reduce pass (it may compute and store it), val2 in the scan pass, put(i, excl[K])
+// receives its exclusive prefix; gtot receives the total on every CTA.
+template <int K, class V1, class V2, class O>
+__device__ __forceinline__ void grid_scan(cg::grid_group& grid, int64_t n, V1 val1, V2 val2, O put, int64_t* ctot,
+                                          int64_t (*sm)[K], int64_t (&gtot)[K]) {
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t chunk = ((n + G - 1) / G + CO_T - 1) / CO_T * CO_T;
+  const int64_t lo = min(n, b * chunk), hi = min(n, lo + chunk);
+  int64_t part[K];
+#pragma unroll
+  for (int f = 0; f < K; f++) part[f] = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += CO_T) {
+    int64_t x[K];
+    val1(i, x);
+#pragma unroll
+    for (int f = 0; f < K; f++) part[f] += x[f];
+  }
+  int64_t ex[K], t[K];
+  cta_scan<K>(part, ex, t, sm);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int f = 0; f < K; f++) ctot[b * K + f] = t[f];
+  grid.sync();
+  // the CTA totals (G <= CO_T) are scanned by one CTA scan: thread i holds CTA i's total
+  __shared__ int64_t s_base[K];
+  int64_t base[K];
+  {
+    int64_t y[K];
+#pragma unroll
+    for (int f = 0; f < K; f++) y[f] = threadIdx.x < G ? ldl2(ctot + threadIdx.x * K + f) : 0;
+    cta_scan<K>(y, ex, gtot, sm);
+    if (threadIdx.x == b)
+#pragma unroll
+      for (int f = 0; f < K; f++) s_base[f] = ex[f];
+    __syncthreads();
+#pragma unroll
+    for (int f = 0; f < K; f++) base[f] = s_base[f];
+  }
+  for (int64_t i0 = lo; i0 < hi; i0 += CO_T) {
+    const int64_t i = i0 + threadIdx.x;
+    int64_t x[K];
+    if (i < hi) val2(i, x);
+    else
+#pragma unroll
+      for (int f = 0; f < K; f++) x[f] = 0;
+    cta_scan<K>(x, ex, t, sm);
+    if (i < hi) {
+      int64_t o[K];
+#pragma unroll
+      for (int f = 0; f < K; f++) o[f] = base[f] + ex[f];
+      put(i, o);
+    }
+#pragma unroll
+    for (int f = 0; f < K; f++) base[f] += t[f];
+  }
+}
+
+__device__ __forceinline__ int64_t ev_node(const int64_t* rec, uint32_t e, int directed) {
+  const int64_t j = ev_edge(e, directed);
+  return rec[ER * j + ((!directed && (e & 1)) ? ER_DST : ER_SRC)];
+}
+
+__global__ void __launch_bounds__(CO_T, 1)
+    k_ingest_coop(const IngestScalars* S, IngestCounters* c, int64_t* rec, int64_t n, int directed, int64_t node_cap,
+                  int sort_bits, CoopBufs CB, NodeArrays N, BlockArrays B, DirArrays D, SlotArrays SA, int kind,
+                  int64_t tau, int64_t param) {
+  cg::grid_group grid = cg::this_grid();
+  typedef cub::BlockRadixSort<uint32_t, CO_T, CO_ITEMS> BSortK;
+  constexpr int HC = 2 * CO_T;  // per-CTA node hash: at most CO_T distinct nodes per sub-chunk
+  __shared__ union {
+    typename BSortK::TempStorage sortk;
+    struct {
+      int32_t key[HC], cnt[HC], base[HC], seg[HC];
+    } h;
+    uint32_t bits[CO_BITMAP_WORDS];  // E-phase rank bitmap over event indices
+  } sm;
+  __shared__ int64_t s_scan[CO_T / 32 + 1][4];
+  __shared__ long long red[4][CO_T / 32];
+  __shared__ uint32_t s_key[CO_T];
+  const int64_t E = directed ? n : 2 * n;
+  const int64_t gtid = blockIdx.x * (int64_t)CO_T + threadIdx.x, gstride = (int64_t)gridDim.x * CO_T;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool has_eids = S->eids_in != nullptr;
+  // each CTA aggregates a contiguous chunk of events, CO_T at a time, in a shared-memory node hash
+  const int64_t L = (E + gridDim.x - 1) / gridDim.x;
+  const int64_t c_lo = min(E, (int64_t)blockIdx.x * L), c_hi = min(E, c_lo + L);
+  auto node_in = [&](int64_t e) -> int64_t {
+    const int64_t j = ev_edge((uint32_t)e, directed);
+    return (!directed && (e & 1)) ? S->dst[j] : S->src[j];
+  };
+  auto h_clear = [&]() {
+    for (int i = threadIdx.x; i < HC; i += CO_T) {
+      sm.h.key[i] = -1;
+      sm.h.cnt[i] = 0;
+    }
+  };
+  auto h_insert = [&](int32_t v, int& slot) -> int {  // returns the event's rank among the sub-chunk's events of v
+    unsigned hh = ((unsigned)v * 2654435761u) & (HC - 1);
+    while (true) {
+      const int k = atomicCAS(&sm.h.key[hh], -1, v);
+      if (k == -1 || k == v) {
+        slot = (int)hh;
+        return atomicAdd(&sm.h.cnt[hh], 1);
+      }
+      hh = (hh + 1) & (HC - 1);
+    }
+  };
+
+  COOP_MARK(0);
+  // ---- A: stage; node / timestamp / id ranges; per-node counts, touched nodes ----
+  {
+    long long mn = LLONG_MAX, mx = LLONG_MIN, tn = LLONG_MAX, tx = LLONG_MIN, ex = LLONG_MIN;
+    for (int64_t j = gtid; j < n; j += gstride) {
+      const long long a = S->src[j], b = S->dst[j], t = S->ts[j], id = has_eids ? S->eids_in[j] : 0;
+      reinterpret_cast<longlong4*>(rec)[j] = make_longlong4(a, b, t, id);
+      mn = min(mn, min(a, b));
+      mx = max(mx, max(a, b));
+      tn = min(tn, t);
+      tx = max(tx, t);
+      ex = max(ex, id);
+    }
+    for (int64_t e = gtid; e < E; e += gstride) CB.trig[e] = 0;
+    for (int o = 16; o; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      tn = min(tn, __shfl_xor_sync(0xffffffffu, tn, o));
+      tx = max(tx, __shfl_xor_sync(0xffffffffu, tx, o));
+      ex = max(ex, __shfl_xor_sync(0xffffffffu, ex, o));
+    }
+    if (lane == 0) {
+      red[0][w] = mn;
+      red[1][w] = mx;
+      red[2][w] = tn;
+      red[3][w] = tx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < CO_T / 32; i++) {
+        mn = min(mn, red[0][i]);
+        mx = max(mx, red[1][i]);
+        tn = min(tn, red[2][i]);
+        tx = max(tx, red[3][i]);
+      }
+      if (mn != LLONG_MAX) {
+        atomicMin(&c->minv, mn);
+        atomicMax(&c->maxv, mx);
+        atomicMin(&c->tsmin, tn);
+        atomicMax(&c->tsmax, tx);
+      }
+    }
+    if (has_eids && lane == 0 && ex != LLONG_MIN) atomicMax(&c->max_eid, ex);
+  }
+  for (int64_t s0 = c_lo; s0 < c_hi; s0 += CO_T) {
+    __syncthreads();
+    h_clear();
+    __syncthreads();
+    const int64_t e = s0 + threadIdx.x;
+    if (e < c_hi) {
+      const int64_t v = node_in(e);
+      int slot;
+      if (v < 0 || v >= node_cap) atomicOr((unsigned long long*)&c->abort, (unsigned long long)ABORT_NODES);
+      else h_insert((int32_t)v, slot);
+    }
+    __syncthreads();
+    // one counter atomic per (sub-chunk, node); the first to count a node lists it (one segment)
+    for (int i0 = 0; i0 < HC; i0 += CO_T) {
+      const int i = i0 + threadIdx.x;
+      const int32_t k = sm.h.key[i];
+      const bool fresh = k >= 0 && atomicAdd(&CB.ncnt[k], sm.h.cnt[i]) == 0;
+      const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+      unsigned long long base = 0;
+      if (fm && lane == __ffs(fm) - 1) base = atomicAdd((unsigned long long*)&c->num_segs, (unsigned long long)__popc(fm));
+      base = __shfl_sync(0xffffffffu, base, fm ? __ffs(fm) - 1 : 0);
+      if (fresh) CB.touched[base + __popc(fm & ((1u << lane) - 1))] = k;
+    }
+  }
+  grid.sync();
+
+  COOP_MARK(1);
+  const int64_t nseg = ldl2(&c->num_segs);
+  if (ldl2(&c->abort) & ABORT_NODES) {  // node ids beyond the table (or negative): undo the counts
+    for (int64_t i = gtid; i < nseg; i += gstride) CB.ncnt[ldl2(&CB.touched[i])] = 0;
+    return;
+  }
+  // ---- C: rows of new nodes; segment starts ----
+  const long long maxv = ldl2(&c->maxv);
+  for (int64_t v = S->num_nodes + gtid; v < maxv + 1; v += gstride) {
+    N.head[v] = GF_NO_BLOCK;
+    N.tail[v] = GF_NO_BLOCK;
+    N.num_blocks[v] = 0;
+    N.degree[v] = 0;
+    const_cast<uint8_t*>(N.valid)[v] = 1;
+    N.nslots[v] = 0;
+    N.dir_off[v] = -1;
+    N.dir_cap[v] = 0;
+    N.nflags[v] = 0;
+    int64_t* r = N.nrec + v * NREC;
+    r[0] = -1;
+    r[1] = 0;
+    r[2] = NREC_VALID;
+    for (int k = 3; k < NREC; k++) r[k] = 0;
+  }
+  {
+    auto cnt_of = [&](int64_t i, int64_t (&x)[1]) { x[0] = ldl2(&CB.ncnt[ldl2(&CB.touched[i])]); };
+    int64_t tot[1];
+    grid_scan<1>(
+        grid, nseg, cnt_of, cnt_of,
+        [&](int64_t i, int64_t (&o)[1]) {
+          const int32_t v = ldl2(&CB.touched[i]);
+          const int64_t m = ldl2(&CB.ncnt[v]);
+          CB.sstart[i] = (int32_t)o[0];
+          CB.nseg[v] = (int32_t)i;
+          if (m > 32) {
+            CB.big[atomicAdd((unsigned long long*)&c->num_big, 1ull)] = (int32_t)i;
+            if (m > CO_SORT) atomicOr((unsigned long long*)&c->abort, (unsigned long long)ABORT_SLOW);
+          }
+        },
+        CB.ctot, reinterpret_cast<int64_t(*)[1]>(s_scan), tot);
+    if (gtid == 0) CB.sstart[nseg] = (int32_t)E;
+  }
+  grid.sync();
+
+  COOP_MARK(2);
+  // ---- D: scatter, one counter atomic per (sub-chunk, node); the counters count back to zero ----
+  for (int64_t s0 = c_lo; s0 < c_hi; s0 += CO_T) {
+    __syncthreads();
+    h_clear();
+    __syncthreads();
+    const int64_t e = s0 + threadIdx.x;
+    int slot = 0, lr = 0;
+    if (e < c_hi) lr = h_insert((int32_t)node_in(e), slot);
+    __syncthreads();
+    for (int i = threadIdx.x; i < HC; i += CO_T) {
+      const int32_t k = sm.h.key[i];
+      if (k >= 0) {
+        const int m = sm.h.cnt[i];
+        const int top = atomicSub(&CB.ncnt[k], m);  // this sub-chunk takes [top - m, top) of the segment
+        const int32_t sg = ldl2(&CB.nseg[k]);
+        sm.h.base[i] = ldl2(&CB.sstart[sg]) + top - m;
+        sm.h.seg[i] = sg;
+      }
+    }
+    __syncthreads();
+    if (e < c_hi) {
+      const int64_t p = sm.h.base[slot] + lr;
+      CB.sev[p] = (uint32_t)e;
+      CB.sseg[p] = sm.h.seg[slot];
+    }
+  }
+  grid.sync();
+  if (ldl2(&c->abort)) return;  // a segment beyond one CTA's sort
+
+  COOP_MARK(3);
+  // ---- E: each segment in append order ----
+  {
+    const int64_t gw = gtid >> 5, nw = gstride >> 5;
+    for (int64_t sg = gw; sg < nseg; sg += nw) {
+      const int32_t st = ldl2(&CB.sstart[sg]), m = ldl2(&CB.sstart[sg + 1]) - st;
+      if (m < 2 || m > 32) continue;
+      uint32_t x = lane < m ? ldl2(&CB.sev[st + lane]) : 0xffffffffu;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+          x = (((lane & j) == 0) == ((lane & k) == 0)) ? min(x, y) : max(x, y);
+        }
+      if (lane < m) CB.sev[st + lane] = x;
+    }
+    __syncthreads();
+    COOP_MARK(7);
+    const int64_t nbig = ldl2(&c->num_big);
+    for (int64_t bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+      const int32_t sg = ldl2(&CB.big[bi]);
+      const int32_t st = ldl2(&CB.sstart[sg]), m = ldl2(&CB.sstart[sg + 1]) - st;
+      if (m <= 256) {
+        // event indices are distinct: a key's rank is the number of smaller keys in the segment
+        const uint32_t x = threadIdx.x < m ? ldl2(&CB.sev[st + threadIdx.x]) : 0u;
+        __syncthreads();
+        if (threadIdx.x < m) s_key[threadIdx.x] = x;
+        __syncthreads();
+        if (threadIdx.x < m) {
+          int rank = 0;
+          for (int i = 0; i < m; i++) rank += s_key[i] < x ? 1 : 0;
+          CB.sev[st + rank] = x;
+        }
+        continue;
+      }
+      if (E <= 32 * CO_BITMAP_WORDS) {
+        // a bitmap over [0, E): a key's rank is the number of set bits below it (thread t owns words
+        // 8t .. 8t+7 and their prefix count in s_key[t])
+        const int nw = (int)((E + 31) >> 5);
+        uint32_t keys[CO_ITEMS];
+#pragma unroll
+        for (int k = 0; k < CO_ITEMS; k++) {
+          const int i = k * CO_T + threadIdx.x;
+          keys[k] = i < m ? ldl2(&CB.sev[st + i]) : 0xffffffffu;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nw; i += CO_T) sm.bits[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < CO_ITEMS; k++)
+          if (keys[k] != 0xffffffffu) atomicOr(&sm.bits[keys[k] >> 5], 1u << (keys[k] & 31));
+        __syncthreads();
+        int64_t cnt8[1] = {0};
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const int wi = threadIdx.x * 8 + q;
+          cnt8[0] += wi < nw ? __popc(sm.bits[wi]) : 0;
+        }
+        int64_t ex1[1], tt1[1];
+        cta_scan<1>(cnt8, ex1, tt1, reinterpret_cast<int64_t(*)[1]>(s_scan));
+        s_key[threadIdx.x] = (uint32_t)ex1[0];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < CO_ITEMS; k++) {
+          const uint32_t x = keys[k];
+          if (x == 0xffffffffu) continue;
+          const int wi = (int)(x >> 5), g0 = wi & ~7;
+          int rank = (int)s_key[wi >> 3] + __popc(sm.bits[wi] & ((1u << (x & 31)) - 1));
+          for (int q = g0; q < wi; q++) rank += __popc(sm.bits[q]);
+          CB.sev[st + rank] = x;
+        }
+        __syncthreads();
+        continue;
+      }
+      uint32_t keys[CO_ITEMS];
+#pragma unroll
+      for (int k = 0; k < CO_ITEMS; k++) {
+        const int i = threadIdx.x * CO_ITEMS + k;
+        keys[k] = i < m ? ldl2(&CB.sev[st + i]) : 0xffffffffu;
+      }
+      __syncthreads();
+      BSortK(sm.sortk).Sort(keys, 0, sort_bits);
+#pragma unroll
+      for (int k = 0; k < CO_ITEMS; k++) {
+        const int i = threadIdx.x * CO_ITEMS + k;
+        if (i < m) CB.sev[st + i] = keys[k];
+      }
+    }
+  }
+  grid.sync();
+
+  COOP_MARK(4);
+  // ---- F: chronology; per-segment block plan, its allocation triggers and its scan ----
+  for (int64_t p = gtid; p < E; p += gstride) {
+    const int32_t sg = ldl2(&CB.sseg[p]);
+    const uint32_t e = ldl2(&CB.sev[p]);
+    const int64_t t = rec[ER * ev_edge(e, directed) + ER_TS];
+    bool viol;
+    if (p == ldl2(&CB.sstart[sg])) viol = t < node_tmax(N.tail, B.size, B.tmax, ev_node(rec, e, directed));
+    else viol = t < rec[ER * ev_edge(ldl2(&CB.sev[p - 1]), directed) + ER_TS];
+    if (viol) atomicOr((unsigned long long*)&c->abort, (unsigned long long)ABORT_SLOW);
+  }
+  __syncthreads();
+  COOP_MARK(8);
+  int64_t tot3[3];
+  grid_scan<3>(
+      grid, nseg,
+      [&](int64_t sg, int64_t (&x)[3]) {  // pass 1: the plan (storage.py:449-459 capacity law per allocation)
+        const int64_t v = ldl2(&CB.touched[sg]);
+        const int64_t st = ldl2(&CB.sstart[sg]), cnt = ldl2(&CB.sstart[sg + 1]) - st;
+        const int64_t t = ldl2(&N.tail[v]), deg0 = ldl2(&N.degree[v]);
+        int64_t fill = 0, tsz = 0;
+        if (t != GF_NO_BLOCK) {
+          tsz = B.size[t];
+          fill = min(B.cap[t] - tsz, cnt);
+        }
+        CB.old_tail[sg] = t;
+        CB.fill[sg] = fill;
+        CB.tail_size[sg] = tsz;
+        CB.deg0[sg] = deg0;
+        int64_t deg = deg0 + fill, used = fill, blocks = 0, slots = 0;
+        while (used < cnt) {
+          const int64_t cap = sizing_cap(kind, tau, param, deg, cnt - used);  // pending: no rejections here
+          const int64_t take = min(cap, cnt - used);
+          CB.trig[ldl2(&CB.sev[st + used])] = cap;  // the event that allocates this block
+          blocks++;
+          slots += cap;
+          deg += take;
+          used += take;
+        }
+        CB.nb_new[sg] = blocks;
+        const int64_t need = ldl2(&N.num_blocks[v]) + blocks;
+        int64_t dnew = 0;
+        if (need > ldl2(&N.dir_cap[v])) {
+          dnew = 8;
+          while (dnew < need) dnew <<= 1;
+        }
+        CB.plan4[sg] = make_longlong4(blocks, slots, dnew, 0);
+        x[0] = blocks;
+        x[1] = slots;
+        x[2] = dnew;
+      },
+      [&](int64_t sg, int64_t (&x)[3]) {  // pass 2: the stored plan
+        x[0] = ldl2(&CB.plan4[sg].x);
+        x[1] = ldl2(&CB.plan4[sg].y);
+        x[2] = ldl2(&CB.plan4[sg].z);
+      },
+      [&](int64_t i, int64_t (&o)[3]) { CB.off4[i] = make_longlong4(o[0], o[1], o[2], 0); },
+      CB.ctot, reinterpret_cast<int64_t(*)[3]>(s_scan), tot3);
+  COOP_MARK(9);
+  if (ldl2(&c->abort)) return;  // a possible rejection: the general sequence resolves the batch
+  if (tot3[1] > S->slots_free || tot3[2] > S->dir_free) {
+    if (gtid == 0) {
+      c->new_blocks = tot3[0];
+      c->new_slots = tot3[1];
+      c->dir_need = tot3[2];
+      c->abort |= ABORT_CAP;
+    }
+    return;  // every CTA holds the same totals
+  }
+  if (gtid == 0) {
+    c->new_blocks = tot3[0];
+    c->new_slots = tot3[1];
+    c->dir_need = tot3[2];
+    c->n_acc = n;
+  }
+  {
+    // handle rank and slot base of each new block: a scan of (1, capacity) over the triggering
+    // events in event order = the reference's allocation order
+    auto trig_of = [&](int64_t e, int64_t (&x)[2]) {
+      const int64_t cap = ldl2(&CB.trig[e]);
+      x[0] = cap > 0 ? 1 : 0;
+      x[1] = cap;
+    };
+    int64_t tot2[2];
+    grid_scan<2>(
+        grid, E, trig_of, trig_of,
+        [&](int64_t e, int64_t (&o)[2]) {
+          if (ldl2(&CB.trig[e]) > 0) {
+            CB.trank[e] = o[0];
+            CB.tbase[e] = o[1];
+          }
+        },
+        CB.ctot + 4 * gridDim.x, reinterpret_cast<int64_t(*)[2]>(s_scan), tot2);
+  }
+  __syncthreads();
+  COOP_MARK(10);
+  grid.sync();
+
+  COOP_MARK(5);
+  // ---- I: commit (segments and slots share the grid) ----
+  const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used, nfree = S->nfree;
+  const int64_t* __restrict__ freel = S->free_list;
+  auto handle_of = [&](int64_t r) { return r < nfree ? freel[nfree - 1 - r] : blk_used + (r - nfree); };
+  const int64_t next_id = S->next_edge_id;
+  for (int64_t idx = gtid; idx < nseg + E; idx += gstride) {
+    if (idx < nseg) {
+      const int64_t sg = idx;
+      const int64_t st = ldl2(&CB.sstart[sg]), cnt = ldl2(&CB.sstart[sg + 1]) - st;
+      const int64_t fill = ldl2(&CB.fill[sg]);
+      int64_t used = fill, deg = ldl2(&CB.deg0[sg]) + fill;
+      auto ev_ts = [&](int64_t r) { return rec[ER * ev_edge(ldl2(&CB.sev[st + r]), directed) + ER_TS]; };
+      auto blk = [&](int64_t) {  // called for k = 0, 1, ... in order
+        const int64_t cap = sizing_cap(kind, tau, param, deg, cnt - used);
+        const int64_t take = min(cap, cnt - used);
+        const uint32_t e = ldl2(&CB.sev[st + used]);
+        const NewBlk nb{handle_of(ldl2(&CB.trank[e])), slots_used + ldl2(&CB.tbase[e]), used, take, cap};
+        used += take;
+        deg += take;
+        return nb;
+      };
+      commit_segment(ldl2(&CB.touched[sg]), cnt, ldl2(&CB.old_tail[sg]), fill, ldl2(&CB.nb_new[sg]),
+                     ldl2(&CB.plan4[sg].z), dir_used + ldl2(&CB.off4[sg].z), ldl2(&CB.tail_size[sg]), ev_ts, blk, N, B,
+                     D, kind);
+    } else {
+      const int64_t p = idx - nseg;
+      const int32_t sg = ldl2(&CB.sseg[p]);
+      const int64_t st = ldl2(&CB.sstart[sg]), cnt = ldl2(&CB.sstart[sg + 1]) - st, r = p - st;
+      const uint32_t e = ldl2(&CB.sev[p]);
+      const int64_t j = ev_edge(e, directed), fill = ldl2(&CB.fill[sg]);
+      int64_t pos;
+      if (r < fill) {
+        pos = B.base[ldl2(&CB.old_tail[sg])] + ldl2(&CB.tail_size[sg]) + r;  // the old tail's base does not change
+      } else {  // walk the segment's new blocks (the capacity law again) to the one holding rank r
+        int64_t used = fill, deg = ldl2(&CB.deg0[sg]) + fill;
+        while (true) {
+          const int64_t cap = sizing_cap(kind, tau, param, deg, cnt - used);
+          const int64_t take = min(cap, cnt - used);
+          if (r < used + take) {
+            pos = slots_used + ldl2(&CB.tbase[ldl2(&CB.sev[st + used])]) + (r - used);
+            break;
+          }
+          used += take;
+          deg += take;
+        }
+      }
+      const longlong4 er = reinterpret_cast<const longlong4*>(rec)[j];
+      const int side = directed ? 0 : (int)(e & 1);
+      write_slot(SA, pos, er.z, has_eids ? er.w : next_id + j, (int32_t)(side ? er.x : er.y),
+                 (int32_t)(side ? er.y : er.x));
+    }
+  }
+  for (int64_t j = gtid; j < n; j += gstride) S->out_eids[j] = has_eids ? rec[ER * j + ER_EID] : next_id + j;
+  __syncthreads();
+  COOP_MARK(6);
 }
 
 // node capacity only (rows are initialised on the device by k_grow_nodes)
@@ -776,11 +1405,183 @@ gf_status grow_node_cap(gf_graph* g, int64_t need, cudaStream_t s) {
   return GF_OK;
 }
 
+// Host state after a committed batch (both paths): cursors, id counter, node count, 32-bit fences.
+void apply_ingest(gf_graph* g, const IngestCounters& hc, int64_t nfree, bool user_eids, int64_t n, int64_t* h_rej) {
+  if (hc.maxv + 1 > g->num_nodes) g->num_nodes = hc.maxv + 1;  // storage.py:410-412
+  const int64_t nrec = hc.new_blocks;
+  g->blk_used += std::max<int64_t>(0, nrec - nfree);  // fresh handles only
+  g->free_handles.resize(nfree - std::min(nfree, nrec));
+  g->slots_used += hc.new_slots;
+  g->dir_used += hc.dir_need;
+  if (user_eids) {
+    if (hc.n_acc > 0 && hc.max_eid + 1 > g->next_edge_id) g->next_edge_id = hc.max_eid + 1;
+  } else {
+    g->next_edge_id += hc.n_acc;
+  }
+  g->total_edges_inserted += hc.n_acc;
+  if (hc.tsmin < INT32_MIN || hc.tsmax > INT32_MAX) g->ts32 = 0;  // the 32-bit fence is no longer exact
+  if (h_rej) *h_rej = n - hc.n_acc;
+}
+
+// handles freed by offload, copied for the commit (read on the device)
+gf_status stage_free_handles(gf_graph* g, cudaStream_t s) {
+  const int64_t nfree = (int64_t)g->free_handles.size();
+  if (nfree > g->free_dev_cap) {
+    if (g->free_dev) GF_CUDA(cudaFreeAsync(g->free_dev, s));
+    g->free_dev = nullptr;
+    g->free_dev_cap = 0;
+    GF_CUDA(cudaMallocAsync(&g->free_dev, sizeof(int64_t) * (size_t)(2 * nfree), s));
+    g->free_dev_cap = 2 * nfree;
+  }
+  if (nfree) GF_CUDA(cudaMemcpyAsync(g->free_dev, g->free_handles.data(), sizeof(int64_t) * nfree, cudaMemcpyHostToDevice, s));
+  return GF_OK;
+}
+
+bool coop_enabled() {
+  const char* e = getenv("GF_INGEST_NO_COOP");  // A/B and tests: force the general launch sequence
+  return !(e && *e && *e != '0');
+}
+
+// The cooperative single-launch path.  *done = false sends the batch to add_edges_fast (ABORT_SLOW,
+// oversized batch, or no co-resident grid); nothing was mutated in that case.
+gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_in, const int64_t* ts_in, int64_t n,
+                         const int64_t* eids_user, int64_t* out_user, int64_t* h_rej, cudaStream_t s, bool* done) {
+  *done = false;
+  const int dir = g->directed;
+  const int64_t E = dir ? n : 2 * n;
+  if (E > CO_MAX_EVENTS || !coop_enabled()) return GF_OK;
+  static int occ = -1;
+  if (occ < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ingest_coop, CO_T, 0) != cudaSuccess) occ = 0;
+    cudaGetLastError();
+  }
+  if (occ < 1) return GF_OK;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * occ, (E + CO_T - 1) / CO_T));
+  GF_TRY(ensure_blocks(g, g->blk_used + E, s));  // new blocks <= events
+  if (g->node_cap == 0) GF_TRY(grow_node_cap(g, 1024, s));
+  if (!g->ing_host) GF_CUDA(cudaMallocHost(&g->ing_host, 4096));
+  GF_TRY(stage_free_handles(g, s));
+  const int64_t nfree = (int64_t)g->free_handles.size();
+  IngestScalars* hs = (IngestScalars*)g->ing_host;
+  IngestCounters* hci = (IngestCounters*)((char*)g->ing_host + 1024);
+  IngestCounters* hcp = (IngestCounters*)((char*)g->ing_host + 2048);
+  IngestCounters hc;
+  for (int attempt = 0;; attempt++) {
+    if (g->co_node_cap < g->node_cap) {  // per-node counters (zero between batches) and segment indices
+      if (g->co_ncnt) GF_CUDA(cudaFreeAsync(g->co_ncnt, s));
+      if (g->co_nseg) GF_CUDA(cudaFreeAsync(g->co_nseg, s));
+      g->co_ncnt = g->co_nseg = nullptr;
+      g->co_node_cap = 0;
+      GF_CUDA(cudaMallocAsync(&g->co_ncnt, sizeof(int32_t) * (size_t)g->node_cap, s));
+      GF_CUDA(cudaMallocAsync(&g->co_nseg, sizeof(int32_t) * (size_t)g->node_cap, s));
+      GF_CUDA(cudaMemsetAsync(g->co_ncnt, 0, sizeof(int32_t) * (size_t)g->node_cap, s));
+      g->co_node_cap = g->node_cap;
+    }
+    CoopBufs CB;
+    auto layout = [&](Arena& a) {
+      void* p0 = a.take<IngestScalars>(1);
+      void* p1 = a.take<IngestCounters>(1);
+      void* p2 = a.take<longlong4>(n);
+      CB.sev = a.take<uint32_t>(E);
+      CB.sseg = a.take<int32_t>(E);
+      CB.touched = a.take<int32_t>(E);
+      CB.sstart = a.take<int32_t>(E + 1);
+      CB.big = a.take<int32_t>(E);
+      CB.ctot = a.take<int64_t>(grid * 8);
+      CB.fill = a.take<int64_t>(E);
+      CB.tail_size = a.take<int64_t>(E);
+      CB.old_tail = a.take<int64_t>(E);
+      CB.nb_new = a.take<int64_t>(E);
+      CB.deg0 = a.take<int64_t>(E);
+      CB.plan4 = a.take<longlong4>(E + 1);
+      CB.off4 = a.take<longlong4>(E + 1);
+      CB.trig = a.take<int64_t>(E);
+      CB.trank = a.take<int64_t>(E);
+      CB.tbase = a.take<int64_t>(E);
+      CB.ncnt = g->co_ncnt;
+      CB.nseg = g->co_nseg;
+      return std::make_tuple((IngestScalars*)p0, (IngestCounters*)p1, (int64_t*)p2);
+    };
+    Arena probe;
+    layout(probe);
+    if (probe.off + 4096 > g->co_bytes) {
+      if (g->co_buf) GF_CUDA(cudaFreeAsync(g->co_buf, s));
+      g->co_buf = nullptr;
+      g->co_bytes = 0;
+      const size_t want = probe.off + 4096 + (probe.off + 4096) / 4;
+      GF_CUDA(cudaMallocAsync(&g->co_buf, want, s));
+      g->co_bytes = want;
+    }
+    Arena A;
+    A.base = (char*)g->co_buf;
+    auto [ds, dc, rec] = layout(A);
+    *hs = IngestScalars{src_in, dst_in, ts_in, eids_user, out_user, g->num_nodes, g->blk_used, g->slots_used,
+                        g->dir_used, g->next_edge_id, g->slot_cap - g->slots_used, g->dir_cap_total - g->dir_used,
+                        g->free_dev, nfree};
+    memset(hci, 0, sizeof(IngestCounters));
+    hci->minv = hci->tsmin = LLONG_MAX;
+    hci->maxv = hci->tsmax = hci->max_eid = LLONG_MIN;
+    GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
+    GF_CUDA(cudaMemcpyAsync(dc, hci, sizeof(IngestCounters), cudaMemcpyHostToDevice, s));
+    NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
+                 g->nflags, g->nrec};
+    BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
+    DirArrays D{g->dir};
+    SlotArrays SA{g->slots, g->sts, g->fts, g->sts32, g->fts32};
+    const IngestScalars* a_S = ds;
+    int64_t a_n = n, a_cap = g->node_cap, a_tau = g->tau, a_param = g->sizing_param;
+    int a_dir = dir, a_bits = bits_for(E + 1), a_kind = g->sizing_kind;
+    void* args[] = {(void*)&a_S, (void*)&dc, (void*)&rec, (void*)&a_n, (void*)&a_dir, (void*)&a_cap, (void*)&a_bits,
+                    (void*)&CB, (void*)&N, (void*)&B, (void*)&D, (void*)&SA, (void*)&a_kind, (void*)&a_tau,
+                    (void*)&a_param};
+    cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
+    GF_CUDA(cudaLaunchCooperativeKernel((const void*)k_ingest_coop, dim3((unsigned)grid), dim3(CO_T), args, 0, s));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e0) prof_stop("k_ingest_coop", s, e0);
+    GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
+    GF_CUDA(cudaStreamSynchronize(s));
+    hc = *hcp;
+    static const bool timing = getenv("GF_INGEST_TIMING") != nullptr;
+    if (timing && !hc.abort) {  // per-phase device time of the cooperative launch (CTA 0's view)
+      static double acc[10] = {0};
+      static int calls = 0;
+      // A C D E F I, then E's warp part, F's chronology, plan scan and trigger scan
+      const long long* t = hc.phase_ns;
+      const double d[10] = {double(t[1] - t[0]), double(t[2] - t[1]), double(t[3] - t[2]), double(t[4] - t[3]),
+                            double(t[5] - t[4]), double(t[6] - t[5]), double(t[7] - t[3]), double(t[8] - t[4]),
+                            double(t[9] - t[8]), double(t[10] - t[9])};
+      for (int i = 0; i < 10; i++) acc[i] += d[i] * 1e-3;
+      if (++calls % 100 == 0) {
+        fprintf(stderr, "ingest coop: %d calls, us/call A C D E F I | E.warp F.chrono F.plan F.trig:", calls);
+        for (int i = 0; i < 10; i++) fprintf(stderr, " %.1f", acc[i] / calls);
+        fprintf(stderr, "\n");
+      }
+    }
+    if (!hc.abort) break;
+    if (hc.abort & ABORT_NODES) {
+      if (hc.minv < 0) return fail(GF_EINVAL, "node ids must be non-negative");  // storage.py:408-409
+      if (hc.maxv + 1 > ((int64_t)1 << 31)) return fail(GF_EINVAL, "node ids must be < 2^31");
+    }
+    if ((hc.abort & ABORT_SLOW) || attempt >= 3) return GF_OK;  // the general sequence takes the batch
+    if (hc.abort & ABORT_NODES) GF_TRY(grow_node_cap(g, hc.maxv + 1, s));
+    if (hc.abort & ABORT_CAP) {
+      GF_TRY(ensure_slots(g, g->slots_used + hc.new_slots, s));
+      GF_TRY(ensure_dir(g, g->dir_used + hc.dir_need, s));
+    }
+  }
+  apply_ingest(g, hc, nfree, eids_user != nullptr, n, h_rej);
+  *done = true;
+  return GF_OK;
+}
+
 gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_in, const int64_t* ts_in, int64_t n,
                          const int64_t* eids_user, int64_t* out_user, int64_t* h_rej, cudaStream_t s) {
   if (h_rej) *h_rej = 0;
   if (n == 0) return GF_OK;
   if (n < 0 || n >= ((int64_t)1 << 30)) return fail(GF_EINVAL, "batch size must be in [0, 2^30)");
+  bool done = false;
+  GF_TRY(add_edges_coop(g, src_in, dst_in, ts_in, n, eids_user, out_user, h_rej, s, &done));
+  if (done) return GF_OK;
   const int dir = g->directed;
   const int64_t E = dir ? n : 2 * n;
   GF_TRY(ensure_blocks(g, g->blk_used + E, s));  // new blocks <= accepted events
@@ -796,15 +1597,8 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
   const int T = 256;
   const int64_t G = 8 * num_sms();
   // handles freed by offload: their device copy is read by the commit (outside the captured graph)
+  GF_TRY(stage_free_handles(g, s));
   const int64_t nfree = (int64_t)g->free_handles.size();
-  if (nfree > g->free_dev_cap) {
-    if (g->free_dev) GF_CUDA(cudaFreeAsync(g->free_dev, s));
-    g->free_dev = nullptr;
-    g->free_dev_cap = 0;
-    GF_CUDA(cudaMallocAsync(&g->free_dev, sizeof(int64_t) * (size_t)(2 * nfree), s));
-    g->free_dev_cap = 2 * nfree;
-  }
-  if (nfree) GF_CUDA(cudaMemcpyAsync(g->free_dev, g->free_handles.data(), sizeof(int64_t) * nfree, cudaMemcpyHostToDevice, s));
   IngestCounters hc;
   const auto t_start = std::chrono::steady_clock::now();
   for (int attempt = 0;; attempt++) {
@@ -957,8 +1751,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_LAUNCH_PDL(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, rec, dir,
                 old_tail, N, B, D, g->sizing_kind);
       GF_LAUNCH_PDL(k_commit_slots, grid_for(E, T, 16 * num_sms()), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan,
-                ce_ev, ce_seg, rec, dir, old_tail, g->bbase, g->slots, g->sts,
-                g->fts, g->sts32, g->fts32);
+                ce_ev, ce_seg, rec, dir, old_tail, g->bbase, SlotArrays{g->slots, g->sts, g->fts, g->sts32, g->fts32});
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
     };
@@ -1015,20 +1808,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_TRY(ensure_dir(g, g->dir_used + hc.dir_need, s));
     }
   }
-  if (hc.maxv + 1 > g->num_nodes) g->num_nodes = hc.maxv + 1;  // storage.py:410-412
-  const int64_t nrec = hc.new_blocks;
-  g->blk_used += std::max<int64_t>(0, nrec - nfree);  // fresh handles only
-  g->free_handles.resize(nfree - std::min(nfree, nrec));
-  g->slots_used += hc.new_slots;
-  g->dir_used += hc.dir_need;
-  if (eids_user) {
-    if (hc.n_acc > 0 && hc.max_eid + 1 > g->next_edge_id) g->next_edge_id = hc.max_eid + 1;
-  } else {
-    g->next_edge_id += hc.n_acc;
-  }
-  g->total_edges_inserted += hc.n_acc;
-  if (hc.tsmin < INT32_MIN || hc.tsmax > INT32_MAX) g->ts32 = 0;  // the 32-bit fence is no longer exact
-  if (h_rej) *h_rej = n - hc.n_acc;
+  apply_ingest(g, hc, nfree, eids_user != nullptr, n, h_rej);
   return GF_OK;
 }
 
@@ -1076,7 +1856,8 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dir,
-                g->slots, g->sts, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf};
+                g->slots, g->sts, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf,
+                g->co_buf, g->co_ncnt, g->co_nseg};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (g->ing_exec) cudaGraphExecDestroy(g->ing_exec);

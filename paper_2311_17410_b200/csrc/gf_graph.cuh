@@ -71,6 +71,13 @@ struct gf_graph {
   int64_t free_dev_cap = 0;
   int64_t ing_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   int64_t ing_nodes = 0;      // kernel launches per replay
+  // cooperative single-launch ingest (gf_graph.cu k_ingest_coop): its own scratch, and two
+  // per-node int32 arrays -- event counters (all zero between batches) and segment indices
+  void* co_buf = nullptr;
+  size_t co_bytes = 0;
+  int32_t* co_ncnt = nullptr;
+  int32_t* co_nseg = nullptr;
+  int64_t co_node_cap = 0;
   // persistent sampling scratch (totals, per-hop tile state, child keys) + pinned totals; a call
   // that finds it busy (another stream) allocates its own
   void* smp_buf = nullptr;

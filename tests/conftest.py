@@ -40,3 +40,14 @@ def cuda_device():
     if not torch.cuda.is_available():
         pytest.fail("gpu-marked test run without a CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture(params=["coop", "general"])
+def ingest_path(request, monkeypatch):
+    """K1 has two device paths: the cooperative single launch (common case) and the general launch
+    sequence (rejections, oversized segments); GF_INGEST_NO_COOP=1 forces the general one."""
+    if request.param == "general":
+        monkeypatch.setenv("GF_INGEST_NO_COOP", "1")
+    else:
+        monkeypatch.delenv("GF_INGEST_NO_COOP", raising=False)
+    return request.param

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("directed", [True, False])
-def test_replayed_batches_with_growth_match_oracle(cuda_device, directed):
+def test_replayed_batches_with_growth_match_oracle(cuda_device, ingest_path, directed):
     import torch
 
     import paper_2311_17410_b200 as gf

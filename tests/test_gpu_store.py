@@ -15,7 +15,7 @@ from fixtures import load, replay_build
 pytestmark = pytest.mark.gpu
 
 
-def test_store_layout_matches_reference_fixtures(cuda_device):
+def test_store_layout_matches_reference_fixtures(cuda_device, ingest_path):
     from gpu_helpers import assert_store_equal, export_store, gpu_factory
 
     fx, meta = load("store_cases.npz")
@@ -33,7 +33,7 @@ def test_store_layout_matches_reference_fixtures(cuda_device):
 
 @pytest.mark.parametrize("directed", [True, False])
 @pytest.mark.parametrize("sizing", ["adaptive", "fixed", "batch"])
-def test_store_matches_oracle_random_streams(cuda_device, directed, sizing):
+def test_store_matches_oracle_random_streams(cuda_device, ingest_path, directed, sizing):
     from gpu_helpers import GpuGraphAdapter, assert_store_equal, export_store, oracle_store
     from oracle import OracleGraph
 
@@ -94,3 +94,42 @@ def test_preassigned_ids_and_empty_batches(cuda_device):
     assert r.edge_ids == [40, 41] and g.next_edge_id == 42
     with pytest.raises(ValueError):
         g.add_edges([(0, 1, 3)], edge_ids=[1, 2])
+
+
+@pytest.mark.parametrize("directed", [True, False])
+def test_cooperative_ingest_taken_and_equal(cuda_device, directed):
+    """A time-sorted stream is committed by the cooperative single launch (k_ingest_coop), with hub
+    segments above one warp (CTA radix sort), node-table growth and pool growth on the way; a batch
+    with an out-of-order edge falls back to the general sequence.  Both equal the oracle."""
+    import paper_2311_17410_b200 as gf
+    from paper_2311_17410_b200 import _lib
+    from gpu_helpers import assert_store_equal, export_store, oracle_store
+    from oracle import OracleGraph
+
+    rng = np.random.default_rng(11 + directed)
+    g = gf.DynamicGraph(directed=directed, tau=48)
+    o = OracleGraph(directed, 48)
+    w = np.arange(1, 3001, dtype=np.float64) ** -1.2
+    w /= w.sum()
+    t0 = 0
+    for b in range(8):
+        m = int(rng.integers(1000, 20_000))
+        nn = 500 * (b + 1)
+        src = rng.choice(3000, size=m, p=w) % nn
+        dst = rng.integers(0, nn, m)
+        ts = np.sort(rng.integers(t0, t0 + 1000, m))
+        t0 += 1000
+        if b == 6:  # the same source earlier in the batch at a later time: a rejection, general sequence
+            ts = ts.copy()
+            src[m // 2] = src[0]
+            ts[m // 2] = ts[0] - 1
+        _lib.profile_enable(True)
+        out, rej = g.add_edges_arrays(src, dst, ts)
+        prof = _lib.profile_summary()
+        _lib.profile_enable(False)
+        want = o.add_edges(src, dst, ts)
+        np.testing.assert_array_equal(out.cpu().numpy(), want, err_msg=f"batch {b}")
+        assert rej == int((want < 0).sum())
+        assert "k_ingest_coop" in prof
+        assert ("k_commit" in prof) == (b == 6), (b, sorted(prof))
+    assert_store_equal(export_store(g), oracle_store(o), f"directed={directed}")
