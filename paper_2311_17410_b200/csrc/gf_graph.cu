@@ -46,6 +46,7 @@ struct IngestCounters {
   long long abort;        // sync-free path: ABORT_* bits, nothing was mutated
   long long tsmin, tsmax; // timestamp range of the batch (32-bit fence validity)
   long long num_big;      // cooperative path: segments with more than 32 events
+  long long num_moves;    // cooperative path: directories that move to a larger region
   long long phase_ns[12]; // cooperative path: globaltimer at each phase start (GF_INGEST_TIMING)
 };
 // ABORT_SLOW (cooperative path only): the batch needs the general launch sequence -- an endpoint
@@ -60,6 +61,7 @@ struct IngestScalars {
   int64_t num_nodes, blk_used, slots_used, dir_used, next_edge_id, slots_free, dir_free;
   const int64_t* free_list;  // handles freed by offload, reused LIFO (storage.py:171-181)
   int64_t nfree;
+  int64_t blocks_free;       // cooperative path: block-arena capacity left (checked on the device)
 };
 
 template <class T>
@@ -823,6 +825,8 @@ struct CoopBufs {
   int32_t* big;       // [E] segments with more than 32 events
   int64_t* ctot;      // [grid * 8] per-CTA partial sums of the grid scans
   int64_t *fill, *tail_size, *old_tail, *nb_new, *deg0;  // [E] per segment
+  int64_t *nb_old, *ns_old, *dir_old;                     // [E] per segment: node row before the batch
+  int32_t* moves;                                         // [E] segments whose directory moves
   longlong4 *plan4, *off4;                                // [E + 1] per segment
   int64_t *trig, *trank, *tbase;  // [E] per event: capacity of the block it allocates (0: none), rank, slot base
   int32_t *ncnt, *nseg;           // per node (persistent)
@@ -1269,11 +1273,15 @@ __global__ void __launch_bounds__(CO_T, 1)
           used += take;
         }
         CB.nb_new[sg] = blocks;
-        const int64_t need = ldl2(&N.num_blocks[v]) + blocks;
+        const int64_t nbo = ldl2(&N.num_blocks[v]), need = nbo + blocks;
+        CB.nb_old[sg] = nbo;
+        CB.ns_old[sg] = ldl2(&N.nslots[v]);
+        CB.dir_old[sg] = ldl2(&N.dir_off[v]);
         int64_t dnew = 0;
         if (need > ldl2(&N.dir_cap[v])) {
           dnew = 8;
           while (dnew < need) dnew <<= 1;
+          if (nbo > 0) CB.moves[atomicAdd((unsigned long long*)&c->num_moves, 1ull)] = (int32_t)sg;
         }
         CB.plan4[sg] = make_longlong4(blocks, slots, dnew, 0);
         x[0] = blocks;
@@ -1289,7 +1297,7 @@ __global__ void __launch_bounds__(CO_T, 1)
       CB.ctot, reinterpret_cast<int64_t(*)[3]>(s_scan), tot3);
   COOP_MARK(9);
   if (ldl2(&c->abort)) return;  // a possible rejection: the general sequence resolves the batch
-  if (tot3[1] > S->slots_free || tot3[2] > S->dir_free) {
+  if (tot3[1] > S->slots_free || tot3[2] > S->dir_free || tot3[0] - S->nfree > S->blocks_free) {
     if (gtid == 0) {
       c->new_blocks = tot3[0];
       c->new_slots = tot3[1];
@@ -1328,53 +1336,134 @@ __global__ void __launch_bounds__(CO_T, 1)
   grid.sync();
 
   COOP_MARK(5);
-  // ---- I: commit (segments and slots share the grid) ----
+  // ---- I: commit ----
+  // Work is spread so that no thread walks a long serial chain: a directory that moves is copied by
+  // one whole CTA; each new block is written by the thread of its allocating event; a segment's own
+  // thread writes only the node row, the old tail and the NodeRec (storage.py:449-477).
   const int64_t blk_used = S->blk_used, slots_used = S->slots_used, dir_used = S->dir_used, nfree = S->nfree;
   const int64_t* __restrict__ freel = S->free_list;
   auto handle_of = [&](int64_t r) { return r < nfree ? freel[nfree - 1 - r] : blk_used + (r - nfree); };
+  auto ts_of = [&](uint32_t e) { return rec[ER * ev_edge(e, directed) + ER_TS]; };
   const int64_t next_id = S->next_edge_id;
+  const int64_t nmov = ldl2(&c->num_moves);
+  for (int64_t mi = blockIdx.x; mi < nmov; mi += gridDim.x) {
+    const int32_t sg = ldl2(&CB.moves[mi]);
+    const int64_t from = ldl2(&CB.dir_old[sg]) * DIRW, to = (dir_used + ldl2(&CB.off4[sg].z)) * DIRW;
+    const int64_t words = ldl2(&CB.nb_old[sg]) * DIRW, fill = ldl2(&CB.fill[sg]);
+    // the old tail's tmax (its entry's last word) grows when the batch fills the tail
+    const int64_t t_tmax = fill > 0 ? ts_of(ldl2(&CB.sev[ldl2(&CB.sstart[sg]) + fill - 1])) : 0;
+    for (int64_t wd = threadIdx.x; wd < words; wd += CO_T) D.e[to + wd] = (fill > 0 && wd == words - 1) ? t_tmax : D.e[from + wd];
+  }
   for (int64_t idx = gtid; idx < nseg + E; idx += gstride) {
     if (idx < nseg) {
       const int64_t sg = idx;
+      const int64_t v = ldl2(&CB.touched[sg]);
       const int64_t st = ldl2(&CB.sstart[sg]), cnt = ldl2(&CB.sstart[sg + 1]) - st;
-      const int64_t fill = ldl2(&CB.fill[sg]);
-      int64_t used = fill, deg = ldl2(&CB.deg0[sg]) + fill;
-      auto ev_ts = [&](int64_t r) { return rec[ER * ev_edge(ldl2(&CB.sev[st + r]), directed) + ER_TS]; };
-      auto blk = [&](int64_t) {  // called for k = 0, 1, ... in order
-        const int64_t cap = sizing_cap(kind, tau, param, deg, cnt - used);
-        const int64_t take = min(cap, cnt - used);
-        const uint32_t e = ldl2(&CB.sev[st + used]);
-        const NewBlk nb{handle_of(ldl2(&CB.trank[e])), slots_used + ldl2(&CB.tbase[e]), used, take, cap};
+      const int64_t fill = ldl2(&CB.fill[sg]), deg0 = ldl2(&CB.deg0[sg]), nb = ldl2(&CB.nb_new[sg]);
+      const int64_t dnew = ldl2(&CB.plan4[sg].z), t = ldl2(&CB.old_tail[sg]), tsz = ldl2(&CB.tail_size[sg]);
+      const int64_t nb_old = ldl2(&CB.nb_old[sg]), ns_old = ldl2(&CB.ns_old[sg]), oo = ldl2(&CB.dir_old[sg]);
+      const int64_t doff = dnew > 0 ? dir_used + ldl2(&CB.off4[sg].z) : oo;
+      const int64_t t_tmax = (t != GF_NO_BLOCK && fill > 0) ? ts_of(ldl2(&CB.sev[st + fill - 1])) : 0;
+      int64_t used = fill, deg = deg0 + fill, used_last = fill;
+      for (int64_t k = 0; k < nb; k++) {  // the capacity law again: first rank of the last new block
+        const int64_t cap = sizing_cap(kind, tau, param, deg, cnt - used), take = min(cap, cnt - used);
+        used_last = used;
         used += take;
         deg += take;
-        return nb;
-      };
-      commit_segment(ldl2(&CB.touched[sg]), cnt, ldl2(&CB.old_tail[sg]), fill, ldl2(&CB.nb_new[sg]),
-                     ldl2(&CB.plan4[sg].z), dir_used + ldl2(&CB.off4[sg].z), ldl2(&CB.tail_size[sg]), ev_ts, blk, N, B,
-                     D, kind);
+      }
+      int64_t tl_tmin = 0, tl_tmax = 0, tl_base = 0;
+      if (t != GF_NO_BLOCK) {
+        tl_tmin = B.tmin[t];
+        tl_base = B.base[t];
+        tl_tmax = fill > 0 ? t_tmax : B.tmax[t];
+      }
+      if (t != GF_NO_BLOCK && fill > 0) {
+        B.size[t] = tsz + fill;
+        B.tmax[t] = t_tmax;
+        if (dnew == 0) D.e[(oo + nb_old - 1) * DIRW + 3] = t_tmax;  // a moving directory's copy carries it
+      }
+      uint8_t fl = N.nflags[v];
+      if (nb > 0) {
+        const uint32_t ef = ldl2(&CB.sev[st + fill]), el = ldl2(&CB.sev[st + used_last]);
+        const int64_t h_first = handle_of(ldl2(&CB.trank[ef])), h_last = handle_of(ldl2(&CB.trank[el]));
+        if (t == GF_NO_BLOCK) N.head[v] = h_first;
+        else B.next[t] = h_first;
+        N.tail[v] = h_last;
+        tl_tmin = ts_of(el);
+        tl_tmax = ts_of(ldl2(&CB.sev[st + cnt - 1]));
+        tl_base = slots_used + ldl2(&CB.tbase[el]);
+        if (dnew > 0) {
+          N.dir_off[v] = doff;
+          N.dir_cap[v] = dnew;
+        }
+        // a block allocated while live degree != slots written (a deletion happened) or by batch
+        // sizing leaves the closed-form position -> block law (SizingLaw)
+        if (kind == GF_SIZING_BATCH || deg0 != ns_old) {
+          fl |= 1;
+          N.nflags[v] = fl;
+        }
+      }
+      const int64_t nbt = nb_old + nb;
+      N.num_blocks[v] = nbt;
+      N.degree[v] = deg0 + cnt;
+      N.nslots[v] = ns_old + cnt;
+      int64_t* rr = N.nrec + v * NREC;
+      rr[0] = doff;
+      rr[1] = ns_old + cnt;
+      rr[2] = nbt | (N.valid[v] ? NREC_VALID : 0) | ((fl & 1) ? NREC_IRREG : 0);
+      rr[3] = nb_old > 0 ? D.e[oo * DIRW + 1] : ns_old;  // entries of the old location: never rewritten
+      rr[4] = nb > 0 ? ns_old + used_last : D.e[(oo + nb_old - 1) * DIRW + 1];
+      rr[5] = tl_base;
+      rr[6] = tl_tmin;
+      rr[7] = tl_tmax;
+      rr[8] = nb_old > 0 ? D.e[oo * DIRW] : ts_of(ldl2(&CB.sev[st]));
     } else {
       const int64_t p = idx - nseg;
       const int32_t sg = ldl2(&CB.sseg[p]);
       const int64_t st = ldl2(&CB.sstart[sg]), cnt = ldl2(&CB.sstart[sg + 1]) - st, r = p - st;
       const uint32_t e = ldl2(&CB.sev[p]);
       const int64_t j = ev_edge(e, directed), fill = ldl2(&CB.fill[sg]);
+      const longlong4 er = reinterpret_cast<const longlong4*>(rec)[j];
       int64_t pos;
       if (r < fill) {
         pos = B.base[ldl2(&CB.old_tail[sg])] + ldl2(&CB.tail_size[sg]) + r;  // the old tail's base does not change
       } else {  // walk the segment's new blocks (the capacity law again) to the one holding rank r
-        int64_t used = fill, deg = ldl2(&CB.deg0[sg]) + fill;
+        int64_t used = fill, deg = ldl2(&CB.deg0[sg]) + fill, prev_used = -1, k = 0;
         while (true) {
           const int64_t cap = sizing_cap(kind, tau, param, deg, cnt - used);
           const int64_t take = min(cap, cnt - used);
           if (r < used + take) {
-            pos = slots_used + ldl2(&CB.tbase[ldl2(&CB.sev[st + used])]) + (r - used);
+            const uint32_t et = (r == used) ? e : ldl2(&CB.sev[st + used]);  // the block's allocating event
+            const int64_t base = slots_used + ldl2(&CB.tbase[et]);
+            pos = base + (r - used);
+            if (r == used) {  // this event allocates block k of the segment: write it
+              const int64_t h = handle_of(ldl2(&CB.trank[e]));
+              const int64_t nbk = ldl2(&CB.nb_new[sg]), dnew = ldl2(&CB.plan4[sg].z);
+              const int64_t doff = dnew > 0 ? dir_used + ldl2(&CB.off4[sg].z) : ldl2(&CB.dir_old[sg]);
+              const int64_t tmax = ts_of(ldl2(&CB.sev[st + used + take - 1]));
+              const int64_t prev = k == 0 ? ldl2(&CB.old_tail[sg]) : handle_of(ldl2(&CB.trank[ldl2(&CB.sev[st + prev_used])]));
+              const int64_t next = k == nbk - 1 ? GF_NO_BLOCK : handle_of(ldl2(&CB.trank[ldl2(&CB.sev[st + used + take])]));
+              B.cap[h] = cap;
+              B.size[h] = take;
+              B.tmin[h] = er.z;
+              B.tmax[h] = tmax;
+              B.base[h] = base;
+              B.prev[h] = prev;
+              B.next[h] = next;
+              int64_t* de = D.e + (doff + ldl2(&CB.nb_old[sg]) + k) * DIRW;
+              de[0] = er.z;
+              de[1] = ldl2(&CB.ns_old[sg]) + used;
+              de[2] = base;
+              de[3] = tmax;
+            }
             break;
           }
+          prev_used = used;
           used += take;
           deg += take;
+          k++;
         }
       }
-      const longlong4 er = reinterpret_cast<const longlong4*>(rec)[j];
       const int side = directed ? 0 : (int)(e & 1);
       write_slot(SA, pos, er.z, has_eids ? er.w : next_id + j, (int32_t)(side ? er.x : er.y),
                  (int32_t)(side ? er.y : er.x));
@@ -1442,6 +1531,74 @@ bool coop_enabled() {
   return !(e && *e && *e != '0');
 }
 
+int coop_occupancy() {
+  static int occ = -1;
+  if (occ < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ingest_coop, CO_T, 0) != cudaSuccess) occ = 0;
+    cudaGetLastError();
+  }
+  return occ;
+}
+
+// scratch of the cooperative path for a batch of n edges on `grid` CTAs
+std::tuple<IngestScalars*, IngestCounters*, int64_t*> coop_layout(Arena& a, const gf_graph* g, int64_t n, int64_t grid,
+                                                                  CoopBufs& CB) {
+  const int64_t E = g->directed ? n : 2 * n;
+  void* p0 = a.take<IngestScalars>(1);
+  void* p1 = a.take<IngestCounters>(1);
+  void* p2 = a.take<longlong4>(n);
+  CB.sev = a.take<uint32_t>(E);
+  CB.sseg = a.take<int32_t>(E);
+  CB.touched = a.take<int32_t>(E);
+  CB.sstart = a.take<int32_t>(E + 1);
+  CB.big = a.take<int32_t>(E);
+  CB.ctot = a.take<int64_t>(grid * 8);
+  CB.fill = a.take<int64_t>(E);
+  CB.tail_size = a.take<int64_t>(E);
+  CB.old_tail = a.take<int64_t>(E);
+  CB.nb_new = a.take<int64_t>(E);
+  CB.deg0 = a.take<int64_t>(E);
+  CB.nb_old = a.take<int64_t>(E);
+  CB.ns_old = a.take<int64_t>(E);
+  CB.dir_old = a.take<int64_t>(E);
+  CB.moves = a.take<int32_t>(E);
+  CB.plan4 = a.take<longlong4>(E + 1);
+  CB.off4 = a.take<longlong4>(E + 1);
+  CB.trig = a.take<int64_t>(E);
+  CB.trank = a.take<int64_t>(E);
+  CB.tbase = a.take<int64_t>(E);
+  CB.ncnt = g->co_ncnt;
+  CB.nseg = g->co_nseg;
+  return std::make_tuple((IngestScalars*)p0, (IngestCounters*)p1, (int64_t*)p2);
+}
+
+// per-node counters (zero between batches) and segment indices for the node table's capacity;
+// scratch for a batch of n edges
+gf_status ensure_coop(gf_graph* g, int64_t n, int64_t grid, cudaStream_t s) {
+  if (g->co_node_cap < g->node_cap) {
+    if (g->co_ncnt) GF_CUDA(cudaFreeAsync(g->co_ncnt, s));
+    if (g->co_nseg) GF_CUDA(cudaFreeAsync(g->co_nseg, s));
+    g->co_ncnt = g->co_nseg = nullptr;
+    g->co_node_cap = 0;
+    GF_CUDA(cudaMallocAsync(&g->co_ncnt, sizeof(int32_t) * (size_t)g->node_cap, s));
+    GF_CUDA(cudaMallocAsync(&g->co_nseg, sizeof(int32_t) * (size_t)g->node_cap, s));
+    GF_CUDA(cudaMemsetAsync(g->co_ncnt, 0, sizeof(int32_t) * (size_t)g->node_cap, s));
+    g->co_node_cap = g->node_cap;
+  }
+  Arena probe;
+  CoopBufs CB;
+  coop_layout(probe, g, n, grid, CB);
+  if (probe.off + 4096 > g->co_bytes) {
+    if (g->co_buf) GF_CUDA(cudaFreeAsync(g->co_buf, s));
+    g->co_buf = nullptr;
+    g->co_bytes = 0;
+    const size_t want = probe.off + 4096 + (probe.off + 4096) / 4;
+    GF_CUDA(cudaMallocAsync(&g->co_buf, want, s));
+    g->co_bytes = want;
+  }
+  return GF_OK;
+}
+
 // The cooperative single-launch path.  *done = false sends the batch to add_edges_fast (ABORT_SLOW,
 // oversized batch, or no co-resident grid); nothing was mutated in that case.
 gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_in, const int64_t* ts_in, int64_t n,
@@ -1450,14 +1607,10 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
   const int dir = g->directed;
   const int64_t E = dir ? n : 2 * n;
   if (E > CO_MAX_EVENTS || !coop_enabled()) return GF_OK;
-  static int occ = -1;
-  if (occ < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ingest_coop, CO_T, 0) != cudaSuccess) occ = 0;
-    cudaGetLastError();
-  }
+  const int occ = coop_occupancy();
   if (occ < 1) return GF_OK;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * occ, (E + CO_T - 1) / CO_T));
-  GF_TRY(ensure_blocks(g, g->blk_used + E, s));  // new blocks <= events
+  // enough threads for one segment or event each in the commit phase (segments <= events)
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * occ, (2 * E + CO_T - 1) / CO_T));
   if (g->node_cap == 0) GF_TRY(grow_node_cap(g, 1024, s));
   if (!g->ing_host) GF_CUDA(cudaMallocHost(&g->ing_host, 4096));
   GF_TRY(stage_free_handles(g, s));
@@ -1467,57 +1620,14 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
   IngestCounters* hcp = (IngestCounters*)((char*)g->ing_host + 2048);
   IngestCounters hc;
   for (int attempt = 0;; attempt++) {
-    if (g->co_node_cap < g->node_cap) {  // per-node counters (zero between batches) and segment indices
-      if (g->co_ncnt) GF_CUDA(cudaFreeAsync(g->co_ncnt, s));
-      if (g->co_nseg) GF_CUDA(cudaFreeAsync(g->co_nseg, s));
-      g->co_ncnt = g->co_nseg = nullptr;
-      g->co_node_cap = 0;
-      GF_CUDA(cudaMallocAsync(&g->co_ncnt, sizeof(int32_t) * (size_t)g->node_cap, s));
-      GF_CUDA(cudaMallocAsync(&g->co_nseg, sizeof(int32_t) * (size_t)g->node_cap, s));
-      GF_CUDA(cudaMemsetAsync(g->co_ncnt, 0, sizeof(int32_t) * (size_t)g->node_cap, s));
-      g->co_node_cap = g->node_cap;
-    }
+    GF_TRY(ensure_coop(g, n, grid, s));
     CoopBufs CB;
-    auto layout = [&](Arena& a) {
-      void* p0 = a.take<IngestScalars>(1);
-      void* p1 = a.take<IngestCounters>(1);
-      void* p2 = a.take<longlong4>(n);
-      CB.sev = a.take<uint32_t>(E);
-      CB.sseg = a.take<int32_t>(E);
-      CB.touched = a.take<int32_t>(E);
-      CB.sstart = a.take<int32_t>(E + 1);
-      CB.big = a.take<int32_t>(E);
-      CB.ctot = a.take<int64_t>(grid * 8);
-      CB.fill = a.take<int64_t>(E);
-      CB.tail_size = a.take<int64_t>(E);
-      CB.old_tail = a.take<int64_t>(E);
-      CB.nb_new = a.take<int64_t>(E);
-      CB.deg0 = a.take<int64_t>(E);
-      CB.plan4 = a.take<longlong4>(E + 1);
-      CB.off4 = a.take<longlong4>(E + 1);
-      CB.trig = a.take<int64_t>(E);
-      CB.trank = a.take<int64_t>(E);
-      CB.tbase = a.take<int64_t>(E);
-      CB.ncnt = g->co_ncnt;
-      CB.nseg = g->co_nseg;
-      return std::make_tuple((IngestScalars*)p0, (IngestCounters*)p1, (int64_t*)p2);
-    };
-    Arena probe;
-    layout(probe);
-    if (probe.off + 4096 > g->co_bytes) {
-      if (g->co_buf) GF_CUDA(cudaFreeAsync(g->co_buf, s));
-      g->co_buf = nullptr;
-      g->co_bytes = 0;
-      const size_t want = probe.off + 4096 + (probe.off + 4096) / 4;
-      GF_CUDA(cudaMallocAsync(&g->co_buf, want, s));
-      g->co_bytes = want;
-    }
     Arena A;
     A.base = (char*)g->co_buf;
-    auto [ds, dc, rec] = layout(A);
+    auto [ds, dc, rec] = coop_layout(A, g, n, grid, CB);
     *hs = IngestScalars{src_in, dst_in, ts_in, eids_user, out_user, g->num_nodes, g->blk_used, g->slots_used,
                         g->dir_used, g->next_edge_id, g->slot_cap - g->slots_used, g->dir_cap_total - g->dir_used,
-                        g->free_dev, nfree};
+                        g->free_dev, nfree, g->blk_cap - g->blk_used};
     memset(hci, 0, sizeof(IngestCounters));
     hci->minv = hci->tsmin = LLONG_MAX;
     hci->maxv = hci->tsmax = hci->max_eid = LLONG_MIN;
@@ -1567,6 +1677,7 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     if (hc.abort & ABORT_CAP) {
       GF_TRY(ensure_slots(g, g->slots_used + hc.new_slots, s));
       GF_TRY(ensure_dir(g, g->dir_used + hc.dir_need, s));
+      GF_TRY(ensure_blocks(g, g->blk_used + std::max<int64_t>(0, hc.new_blocks - nfree), s));
     }
   }
   apply_ingest(g, hc, nfree, eids_user != nullptr, n, h_rej);
@@ -1707,7 +1818,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     // per-call values: read on the device through ds
     *hs = IngestScalars{src_in, dst_in, ts_in, eids_user, out_user, g->num_nodes, g->blk_used, g->slots_used,
                         g->dir_used, g->next_edge_id, g->slot_cap - g->slots_used, g->dir_cap_total - g->dir_used,
-                        g->free_dev, nfree};
+                        g->free_dev, nfree, g->blk_cap - g->blk_used};
 
     // the launch sequence: identical for every call with the same key
     auto enqueue = [&](cudaStream_t s) -> gf_status {
@@ -1923,6 +2034,12 @@ gf_status gf_graph_reserve(gf_graph* g, int64_t nodes, int64_t blocks, int64_t s
   GF_TRY(ensure_blocks(g, blocks, s));
   GF_TRY(ensure_slots(g, slots, s));
   GF_TRY(ensure_dir(g, blocks * 2, s));
+  // the cooperative ingest's one-time setup (occupancy query, pinned staging, per-node counters,
+  // scratch for batches of up to 2^17 edges), so that a stream's first batches do not pay it
+  if (!g->ing_host) GF_CUDA(cudaMallocHost(&g->ing_host, 4096));
+  const int occ = coop_occupancy();
+  if (occ > 0 && g->node_cap > 0) GF_TRY(ensure_coop(g, std::min<int64_t>(std::max<int64_t>(slots, 1), 1 << 17),
+                                                     (int64_t)num_sms() * occ, s));
   GF_CUDA(cudaStreamSynchronize(s));
   return GF_OK;
 }

@@ -2,7 +2,7 @@
 
 Prints edges/s (device events around the loop), the per-kernel device time from the library's
 launch profiler, and host wall time per batch.
-Usage: python scripts/ingest_profile.py [edges] [batch] [nodes] [span]
+Usage: python scripts/ingest_profile.py [edges] [batch] [nodes] [span] [d|u]
 (GDELT: 17000 nodes, span 175200 -- the defaults; mag8: 15250000 nodes, span 120, 10M batches)
 """
 
@@ -20,10 +20,12 @@ E = int(sys.argv[1]) if len(sys.argv) > 1 else 20_000_000
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 100_000
 NODES = int(sys.argv[3]) if len(sys.argv) > 3 else 17_000
 SPAN = int(sys.argv[4]) if len(sys.argv) > 4 else 175_200
+DIRECTED = (sys.argv[5] != "u") if len(sys.argv) > 5 else True  # "u": undirected stream (WIKI / REDDIT law)
 dev = torch.device("cuda", 0)
-src, dst, ts = gf.generate_synthetic_device(NODES, E, 2.2, SPAN, seed=0, src_skew=2.2, device=dev)
-g = gf.DynamicGraph(directed=True, tau=8192, device=dev)
-g.reserve(NODES, NODES * 16 + E // 8192 + 1024, E + min(NODES * 8192, E // 2))
+src, dst, ts = gf.generate_synthetic_device(NODES, E, 2.2, SPAN, seed=0, src_skew=2.2 if DIRECTED else None, device=dev)
+TAU = 8192 if DIRECTED else 48
+g = gf.DynamicGraph(directed=DIRECTED, tau=TAU, device=dev)
+g.reserve(NODES, NODES * 16 + 2 * E // TAU + 1024, 2 * E + min(NODES * TAU, E))
 half = E // 2
 for lo in range(0, half, B):  # warm half
     g.add_edges_arrays(src[lo:lo + B], dst[lo:lo + B], ts[lo:lo + B])
@@ -50,8 +52,8 @@ for k, (c, kms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
 print(f"  kernel sum {tot:.1f} ms = {tot / nb * 1e3:.0f} us/batch")
 # unprofiled rate
 torch.cuda.synchronize()
-g2 = gf.DynamicGraph(directed=True, tau=8192, device=dev)
-g2.reserve(NODES, NODES * 16 + E // 8192 + 1024, E + min(NODES * 8192, E // 2))
+g2 = gf.DynamicGraph(directed=DIRECTED, tau=TAU, device=dev)
+g2.reserve(NODES, NODES * 16 + 2 * E // TAU + 1024, 2 * E + min(NODES * TAU, E))
 a.record()
 for lo in range(0, E, B):
     g2.add_edges_arrays(src[lo:lo + B], dst[lo:lo + B], ts[lo:lo + B])
