@@ -388,7 +388,7 @@ def bench_ours(args, cfg, world, rank, local):
         gen = torch.Generator(device=device)
         gen.manual_seed(3)
         ids = torch.randperm(src.numel(), generator=gen, device=device)[: src.numel() // 100].sort().values
-        deleted = {"edges": int(g.delete_edges(ids)), "sampler": "general path (k_count_general / k_write_general)"}
+        deleted = {"edges": int(g.delete_edges(ids)), "sampler": "post-deletion path: k_sample_fused_del (lane per query, validity-checked selection)"}
     roots, rts = roots_for_rank(src, dst, ts, R, rank)
     key_base = rank * R
 

@@ -578,6 +578,7 @@ static int64_t sample_one_faithful(const or_graph* g, int64_t node, int64_t t_st
 /* General-path uniform selection (graphs with deletions): see sample_one_fast */
 #define OR_GEN_EXACT 64
 #define OR_KREJ 32
+#define OR_KFLOYD 16 /* KMAX: fanouts served by the fused kernels */
 #define OR_REJ_TAG (1ull << 40)
 
 /* Early-exit path, same output: position-indexed view of the node list. */
@@ -656,8 +657,23 @@ static int64_t sample_one_fast(const or_graph* g, int64_t node, int64_t t_start,
    * fanout keeps -- a uniform k-subset of the valid candidates (the CUDA general path,
    * gf_sample.cu k_count_general, makes the same decisions in the same draw order).  After
    * 8 * fanout + 32 draws without fanout keeps, the exact path below runs. */
+  /* First (fanouts up to OR_KFLOYD, the CUDA fused kernel k_sample_fused_del): Floyd's k distinct
+   * positions of the window -- the draws of the no-deletion path -- and the valid ones are kept in
+   * draw order (a query no deletion touches keeps its pre-deletion sample).  They are a uniform
+   * subset of the valid candidates of a uniform size; the draws below top them up with uniform new
+   * valid candidates, so the result stays a uniform k-subset. */
   if (policy != OR_RECENT && hi - lo > OR_GEN_EXACT && fanout <= OR_KREJ) {
     int64_t npos = hi - lo, dmax = 8 * fanout + 32, acc = 0;
+    if (fanout <= OR_KFLOYD) {
+      int64_t fl[OR_KFLOYD];
+      floyd_select(npos, fanout, seed, qkey, fl);
+      for (int64_t i = 0; i < fanout; i++) {
+        int64_t h, j;
+        nv_at(g, nv, lo + fl[i], &h, &j);
+        const or_edges* e = &g->edges[h];
+        if (e->valid[j] && g->node_valid[e->nbr[j]]) sel[acc++] = lo + fl[i];
+      }
+    }
     for (int64_t d = 0; d < dmax && acc < fanout; d++) {
       int64_t p = lo + (int64_t)bounded(rand64(seed, qkey, OR_REJ_TAG + (uint64_t)d), (uint64_t)npos);
       int64_t h, j;

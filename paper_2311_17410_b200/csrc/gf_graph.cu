@@ -291,6 +291,11 @@ gf_status ensure_slots(gf_graph* g, int64_t need, cudaStream_t s) {
   GF_TRY(grow_array(g->fts32, (g->slots_used + FENCE32 - 1) / FENCE32, nc / FENCE32 + 16, s));  // chunk loads read up to 7 past
   // unused capacity slots must read as invalid (delete scans the whole pool)
   GF_CUDA(cudaMemsetAsync(g->slots + old, 0, sizeof(Slot) * (size_t)(nc - old), s));
+  if (g->okbits) {
+    const int64_t w_old = (old + 31) / 32, w_new = (nc + 31) / 32 + 4;  // padded: 64-bit runs read 3 words
+    GF_TRY(grow_array(g->okbits, w_old, w_new, s));
+    GF_CUDA(cudaMemsetAsync(g->okbits + w_old, 0, sizeof(uint32_t) * (size_t)(w_new - w_old), s));
+  }
   g->slot_cap = nc;
   return GF_OK;
 }
@@ -703,6 +708,8 @@ struct SlotArrays {
   Slot* slots;
   int64_t *sts, *fts;
   int32_t *sts32, *fts32;
+  uint32_t* okbits;          // candidate bitmap, NULL before the first deletion
+  const uint8_t* node_valid;
 };
 
 // one slot record plus its timestamp copies and fences
@@ -720,6 +727,11 @@ __device__ __forceinline__ void write_slot(const SlotArrays& SA, int64_t pos, in
   const int32_t t32 = (int32_t)max(min(ts, (int64_t)INT32_MAX), (int64_t)INT32_MIN);  // exact while ts32
   SA.sts32[pos] = t32;
   if ((pos & (FENCE32 - 1)) == 0) SA.fts32[pos / FENCE32] = t32;
+  if (SA.okbits) {  // a new edge is a candidate unless its neighbour was deleted
+    const uint32_t bit = 1u << (pos & 31);
+    if (SA.node_valid[nbr]) atomicOr(SA.okbits + (pos >> 5), bit);
+    else atomicAnd(SA.okbits + (pos >> 5), ~bit);
+  }
 }
 
 // The commit: one THREAD per segment writes its new blocks (handle and slot base from the trigger
@@ -1637,7 +1649,7 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
                  g->nflags, g->nrec};
     BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
     DirArrays D{g->dir};
-    SlotArrays SA{g->slots, g->sts, g->fts, g->sts32, g->fts32};
+    SlotArrays SA{g->slots, g->sts, g->fts, g->sts32, g->fts32, g->okbits, g->node_valid};
     const IngestScalars* a_S = ds;
     int64_t a_n = n, a_cap = g->node_cap, a_tau = g->tau, a_param = g->sizing_param;
     int a_dir = dir, a_bits = bits_for(E + 1), a_kind = g->sizing_kind;
@@ -1862,7 +1874,7 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
       GF_LAUNCH_PDL(k_commit, grid_for(E, T, G), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan, ce_ev, rec, dir,
                 old_tail, N, B, D, g->sizing_kind);
       GF_LAUNCH_PDL(k_commit_slots, grid_for(E, T, 16 * num_sms()), T, 0, s, dc, ds, keys, seg_start, P, off4, R, tscan,
-                ce_ev, ce_seg, rec, dir, old_tail, g->bbase, SlotArrays{g->slots, g->sts, g->fts, g->sts32, g->fts32});
+                ce_ev, ce_seg, rec, dir, old_tail, g->bbase, SlotArrays{g->slots, g->sts, g->fts, g->sts32, g->fts32, g->okbits, g->node_valid});
       GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
       return GF_OK;
     };
@@ -1924,6 +1936,36 @@ gf_status add_edges_fast(gf_graph* g, const int64_t* src_in, const int64_t* dst_
 }
 
 // ---- deletes (storage.py:479-512) ------------------------------------------
+// candidate bitmap word i: slots 32i .. 32i+31 (valid edge and valid neighbour, sampling.py:178)
+__global__ void k_okbits_build(const Slot* __restrict__ slots, int64_t nslots, const uint8_t* __restrict__ node_valid,
+                               int64_t num_nodes, uint32_t* okbits) {
+  const int64_t nw = (nslots + 31) / 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw * 32; i += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = false;
+    if (i < nslots) {
+      const Slot sl = slots[i];
+      ok = sl.valid && sl.nbr >= 0 && sl.nbr < num_nodes && node_valid[sl.nbr];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if ((threadIdx.x & 31) == 0) okbits[i >> 5] = m;
+  }
+}
+
+// after a deletion: (re)build the candidate bitmap over the whole pool; its first allocation changes
+// the ingest kernels' arguments, so the captured ingest graph is invalidated
+gf_status okbits_rebuild(gf_graph* g, cudaStream_t s) {
+  if (!g->okbits) {
+    const size_t words = (size_t)(g->slot_cap + 31) / 32 + 4;  // padded: 64-bit runs read 3 words
+    GF_CUDA(cudaMallocAsync(&g->okbits, sizeof(uint32_t) * words, s));
+    GF_CUDA(cudaMemsetAsync(g->okbits, 0, sizeof(uint32_t) * words, s));
+    g->gen++;
+  }
+  if (g->slots_used > 0)
+    GF_LAUNCH(k_okbits_build, grid_for(g->slots_used, 256, 16 * num_sms()), 256, 0, s, g->slots, g->slots_used,
+              g->node_valid, g->num_nodes, g->okbits);
+  return GF_OK;
+}
+
 __global__ void k_delete_scan(Slot* slots, int64_t nslots, const int64_t* __restrict__ wanted, int64_t nw, int64_t* degree,
                               uint8_t* hit) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1967,7 +2009,7 @@ __global__ void k_gather_slots(const Slot* slots, const int64_t* __restrict__ bb
 void free_graph(gf_graph* g) {
   void* ps[] = {g->head, g->tail, g->num_blocks, g->degree, g->node_valid, g->nslots, g->dir_off, g->dir_cap,
                 g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase, g->dir,
-                g->slots, g->sts, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf,
+                g->slots, g->sts, g->fts, g->sts32, g->fts32, g->nflags, g->nrec, g->ing_buf, g->okbits,
                 g->co_buf, g->co_ncnt, g->co_nseg};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -2078,7 +2120,11 @@ gf_status gf_graph_delete_edges(gf_graph* g, const int64_t* d_eids, int64_t n, i
   long long h = 0;
   GF_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
   GF_CUDA(cudaStreamSynchronize(s));
-  if (h > 0) g->any_deleted = 1;
+  if (h > 0) {
+    g->any_deleted = 1;
+    GF_TRY(okbits_rebuild(g, s));
+    GF_CUDA(cudaStreamSynchronize(s));
+  }
   if (h_out_deleted) *h_out_deleted = h;
   return GF_OK;
 }
@@ -2095,8 +2141,9 @@ gf_status gf_graph_delete_node(gf_graph* g, int64_t node, int* h_out_deleted, vo
   if (!v) return GF_OK;
   GF_CUDA(cudaMemsetAsync(g->node_valid + node, 0, 1, s));
   GF_LAUNCH(k_noderec_invalidate, 1, 1, 0, s, g->nrec, node);
-  GF_CUDA(cudaStreamSynchronize(s));
   g->any_deleted = 1;
+  GF_TRY(okbits_rebuild(g, s));  // every edge into the node stops being a candidate
+  GF_CUDA(cudaStreamSynchronize(s));
   if (h_out_deleted) *h_out_deleted = 1;
   return GF_OK;
 }

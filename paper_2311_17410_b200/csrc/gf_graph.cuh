@@ -19,6 +19,9 @@
 //                                              29 MB at GDELT scale, and the 32-slot window it leaves
 //                                              is ONE aligned line of sts32
 //   nflags     (u8 per node)                   bit 0: block list not on the sizing law's closed form
+//   okbits     (1 bit per slot, after the      slot is a candidate: valid edge and valid neighbour
+//               first deletion)                (23 MB at GDELT scale: the post-deletion sampler's
+//                                              validity checks stay in L2)
 #pragma once
 
 #include <atomic>
@@ -59,6 +62,9 @@ struct gf_graph {
   int32_t* sts32 = nullptr;  // 32-bit slot timestamps (valid while ts32)
   int32_t* fts32 = nullptr;  // 32-bit fence every 32 slots (valid while ts32)
   int ts32 = 1;              // every timestamp ingested so far fits in int32
+  // candidate bitmap, one bit per pool slot: valid edge and valid neighbour (sampling.py:178).
+  // Allocated by the first deletion, rebuilt by every delete call, kept current by ingest.
+  uint32_t* okbits = nullptr;
   // persistent ingest scratch (sync-free path), sized for the largest batch seen
   void* ing_buf = nullptr;
   size_t ing_bytes = 0;
@@ -144,6 +150,7 @@ struct GraphView {
   const int32_t* fts32;
   const uint8_t* nflags;
   const int64_t* nrec;
+  const uint32_t* okbits;  // NULL until the first deletion
   int64_t num_nodes;
   int any_deleted;
   int ts32;
@@ -153,7 +160,7 @@ struct GraphView {
 inline GraphView view_of(const gf_graph* g) {
   return GraphView{g->node_valid, g->num_blocks, g->nslots, g->dir_off,   g->dir,
                    g->slots,      g->sts,        g->fts,       g->sts32,     g->fts32,     g->nflags,
-                   g->nrec,       g->num_nodes,  g->any_deleted, g->ts32,
+                   g->nrec,       g->okbits,    g->num_nodes,  g->any_deleted, g->ts32,
                    sizing_law(g->sizing_kind, g->tau, g->sizing_param)};
 }
 

@@ -897,14 +897,14 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
         s_inb[EARLY ? w : 0][lane] = (uint16_t)min(inblk, (int64_t)KMAX);
         if (k > inblk) {  // the run crosses into earlier blocks (short lists)
           s_xhi[EARLY ? w : 0][lane] = hi;
-          s_xd0[EARLY ? w : 0][lane] = d0 | nb << 40;
+          s_xd0[EARLY ? w : 0][lane] = d0 | nb << 40 | (irregular ? 1ll << 62 : 0ll);
         }
       } else {
 #pragma unroll
         for (int r = 0; r < KMAX; r++) {
           if (r < k)
             s_sel[EARLY ? 0 : w][lane][(r + lane) & (KMAX - 1)] =
-                (r < inblk) ? (uint32_t)(slot_hi - r) : pool_slot_of(GV, true, d0, nb, hi - 1 - r);
+                (r < inblk) ? (uint32_t)(slot_hi - r) : pool_slot_of(GV, irregular, d0, nb, hi - 1 - r);
         }
       }
     } else {
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
       const int ww = EARLY ? w : 0;
       if (i < s_inb[ww][j]) return s_hi[ww][j] - (uint32_t)i;
       const int64_t xd = s_xd0[ww][j];
-      return pool_slot_of(GV, true, xd & ((1ll << 40) - 1), xd >> 40, s_xhi[ww][j] - 1 - i);
+      return pool_slot_of(GV, (xd >> 62) & 1, xd & ((1ll << 40) - 1), (xd >> 40) & ((1ll << 22) - 1), s_xhi[ww][j] - 1 - i);
     }
     return s_sel[EARLY ? 0 : w][j][(i + j) & (KMAX - 1)];
   };
@@ -1253,6 +1253,476 @@ __global__ void __launch_bounds__(THREADS) k_write_general(GraphView GV, QueryIn
   }
 }
 
+// ===================== fused path after deletions (lane per query) ===================
+// The general path's decisions (k_count_general / k_write_general, oracle/gf_oracle.c) in the fused
+// kernel's shape: the window search of the fast path (deletions are soft, so the list layout and
+// its timestamps are unchanged), then a per-lane selection that reads candidate validity
+// (valid edge and valid neighbour, sampling.py:178) from the 1-bit-per-slot candidate bitmap:
+//   recent             newest first, up to fanout valid, scanning back at most DEL_SCAN positions;
+//   uniform / window   more than GEN_EXACT positions: the fast path's Floyd positions, the valid
+//                      ones kept; then rejection draws (REJ_TAG + d), 4 in flight, kept in draw
+//                      order when valid and new, up to rej_max draws;
+//                      at most GEN_EXACT positions: a validity mask of the window, then newest
+//                      first (every valid candidate fits) or Floyd over the valid ranks.
+// A query a lane cannot finish within those bounds (a recent run past DEL_SCAN, rejection draws
+// exhausted) is taken over by its whole warp, 32 positions per step, as the general kernels do.
+// Selected pool slots go to the per-query pick array; tile scan, decoupled look-back and the
+// cooperative gather/store are those of k_sample_fused.
+#ifndef GF_DEL_THREADS
+#define GF_DEL_THREADS 256
+#endif
+#ifndef GF_DEL_MINB
+#define GF_DEL_MINB 4  // 64 registers (A/B: 2 and 3 CTAs per SM of 256 are 1.4x / 1.15x slower)
+#endif
+
+constexpr int DEL_SCAN = 64;
+#if GF_DEL_STATS
+__device__ unsigned long long g_del_stats[8];  // A/B instrumentation only (GF_DEL_STATS builds)
+#define DEL_STAT(i, v) atomicAdd(&g_del_stats[i], (unsigned long long)(v))
+#else
+#define DEL_STAT(i, v) ((void)0)
+#endif
+
+// Floyd's k distinct indices of [0, nv) (k < nv, k <= KMAX), exactly as k_sample_fused draws them:
+// t_i in [0, nv-k+i] from Philox block i/2 keyed by (seed, key) (two draws per block, = rand64),
+// a duplicate replaced by nv-k+i
+__device__ __forceinline__ void floyd_positions(uint64_t seed, uint64_t qkey, int64_t nv, int k, int32_t (&pick)[KMAX]) {
+#pragma unroll
+  for (int i = 0; i < KMAX; i += 2) {
+    if (i < k) {
+      uint32_t c[4] = {(uint32_t)(i >> 1), (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+      philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+      const int64_t t0 = (int64_t)bounded64((uint64_t)c[0] | ((uint64_t)c[1] << 32), (uint64_t)(nv - k + i + 1));
+      bool dup0 = false;
+#pragma unroll
+      for (int j = 0; j < KMAX; j++) dup0 |= (j < i) && pick[j] == (int32_t)t0;
+      pick[i] = dup0 ? (int32_t)(nv - k + i) : (int32_t)t0;
+      if (i + 1 < k) {
+        const int64_t t1 = (int64_t)bounded64((uint64_t)c[2] | ((uint64_t)c[3] << 32), (uint64_t)(nv - k + i + 2));
+        bool dup1 = false;
+#pragma unroll
+        for (int j = 0; j < KMAX; j++) dup1 |= (j < i + 1) && pick[j] == (int32_t)t1;
+        pick[i + 1] = dup1 ? (int32_t)(nv - k + i + 1) : (int32_t)t1;
+      }
+    }
+  }
+}
+
+// pool slot sl is a candidate (valid edge, valid neighbour): one bit of the 1-bit-per-slot bitmap the
+// deletions maintain (gf_graph.cuh okbits), L2-resident, instead of the slot's own record
+__device__ __forceinline__ bool cand_ok(const GraphView& GV, uint32_t sl) {
+#if GF_AB_DEL_NOBITS
+  return sl != 0xffffffffu;  // A/B timing only: every candidate valid, no bitmap read
+#else
+  return (__ldg(GV.okbits + (sl >> 5)) >> (sl & 31)) & 1u;
+#endif
+}
+
+__device__ __forceinline__ int nth_set_bit64(uint64_t m, int r) {  // 0-based position of the r-th set bit
+  const unsigned lo = (unsigned)m;
+  const int c = __popc(lo);
+  return r < c ? nth_set_bit(lo, r) : 32 + nth_set_bit((unsigned)(m >> 32), r - c);
+}
+
+// a query's window, as the lane found it: positions [lo, hi); positions >= cum lie in the boundary
+// block (slot of hi-1 = slot_hi), earlier ones are mapped through the sizing law or the directory
+struct DelWin {
+  int64_t lo, hi, cum, slot_hi, d0, nb;
+  bool irregular;
+};
+__device__ __forceinline__ uint32_t del_slot(const GraphView& GV, const DelWin& W, int64_t p) {
+  return p >= W.cum ? (uint32_t)(W.slot_hi - (W.hi - 1 - p)) : pool_slot_of(GV, W.irregular, W.d0, W.nb, p);
+}
+
+// bits [s, s + len) of the candidate bitmap (len <= 64; the bitmap is padded past its end)
+__device__ __forceinline__ uint64_t run_bits(const GraphView& GV, int64_t s, int len) {
+  const int64_t w = s >> 5;
+  const int sh = (int)(s & 31);
+  const uint64_t a = (uint64_t)__ldg(GV.okbits + w) | ((uint64_t)__ldg(GV.okbits + w + 1) << 32);
+  const uint64_t b = (len + sh > 64) ? (uint64_t)__ldg(GV.okbits + w + 2) : 0;
+  const uint64_t v = (a >> sh) | (sh ? (b << (64 - sh)) : 0);
+  return len >= 64 ? v : (v & ((1ull << len) - 1));
+}
+
+// candidate mask of a window of at most 64 positions, bit i = position lo + i: the boundary block's
+// part is one contiguous run of slots; each earlier block's run comes from its directory entry
+__device__ __forceinline__ uint64_t window_mask(const GraphView& GV, const DelWin& W) {
+  const int64_t p0 = max(W.lo, W.cum);
+  uint64_t m = run_bits(GV, W.slot_hi - (W.hi - 1 - p0), (int)(W.hi - p0)) << (p0 - W.lo);
+  if (W.lo < W.cum) {
+    const int64_t* d = GV.dir + W.d0 * DIRW;
+    const int64_t b0 = W.irregular ? dir_block_of(GV, W.d0, W.nb, W.lo) : law_block(GV.law, W.lo);
+    const int64_t b1 = W.irregular ? dir_block_of(GV, W.d0, W.nb, W.cum - 1) : law_block(GV.law, W.cum - 1);
+#pragma unroll 4
+    for (int64_t b = b0; b <= b1; b++) {
+      const int64_t cb = W.irregular ? __ldg(d + b * DIRW + 1) : law_cum(GV.law, b);
+      const int64_t ce = (b == b1) ? W.cum : (W.irregular ? __ldg(d + (b + 1) * DIRW + 1) : law_cum(GV.law, b + 1));
+      const int64_t ps = max(W.lo, cb);
+      m |= run_bits(GV, __ldg(d + b * DIRW + 2) + (ps - cb), (int)(ce - ps)) << (ps - W.lo);
+    }
+  }
+  return m;
+}
+
+// the whole warp selects for one query (uniform after failed draws / recent past DEL_SCAN): the
+// general kernels' algorithm; picks go to sel[(i + owner) % KMAX]; returns the count
+__device__ __forceinline__ int warp_select_general(const GraphView& GV, const QueryIn& Q, const DelWin& W, uint64_t qkey,
+                                   uint32_t* sel, int owner) {
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  auto put = [&](int i, uint32_t sl) { sel[(i + owner) & (KMAX - 1)] = sl; };
+  auto ok_at = [&](int64_t p, uint32_t& sl) {
+    sl = del_slot(GV, W, p);
+    return cand_ok(GV, sl);
+  };
+  const bool recent = Q.policy == GF_POLICY_RECENT;
+  int64_t nv = 0;
+  if (!recent) {  // every valid candidate counts
+    for (int64_t p0 = W.lo; p0 < W.hi; p0 += 32) {
+      const int64_t p = p0 + lane;
+      uint32_t sl;
+      nv += __popc(__ballot_sync(0xffffffffu, p < W.hi && ok_at(p, sl)));
+    }
+  }
+  const int kmax = (int)min((int64_t)Q.fanout, recent ? (int64_t)Q.fanout : nv);
+  if (recent || kmax == nv) {  // newest first
+    int done = 0;
+    for (int64_t p0 = W.hi - 1; p0 >= W.lo && done < kmax; p0 -= 32) {
+      const int64_t p = p0 - lane;
+      uint32_t sl = 0;
+      const bool ok = p >= W.lo && ok_at(p, sl);
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      const int r = done + __popc(m & lt);
+      if (ok && r < kmax) put(r, sl);
+      done += __popc(m);
+    }
+    __syncwarp();
+    return min(done, kmax);
+  }
+  // Floyd's k-of-nv over the chronological valid ranks (rand64(seed, key, i)), lane i keeps rank i
+  int64_t want = -1;
+  for (int i = 0; i < kmax; i++) {
+    const int64_t j = nv - kmax + i;
+    const int64_t ti = (int64_t)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
+    const bool dup = __any_sync(0xffffffffu, lane < i && want == ti);
+    if (lane == i) want = dup ? j : ti;
+  }
+  int64_t rank0 = 0;
+  for (int64_t p0 = W.lo; p0 < W.hi; p0 += 32) {
+    const int64_t p = p0 + lane;
+    uint32_t sl;
+    const unsigned m = __ballot_sync(0xffffffffu, p < W.hi && ok_at(p, sl));
+    const int c = __popc(m);
+    if (lane < kmax && want >= rank0 && want < rank0 + c) put(lane, del_slot(GV, W, p0 + nth_set_bit(m, (int)(want - rank0))));
+    rank0 += c;
+  }
+  __syncwarp();
+  return kmax;
+}
+
+// SPLIT (uniform / time-window): the selection ends the kernel -- counts[q] and the picks
+// picks[q * KMAX + i] go to HBM, a scan gives the offsets and k_gather_picks writes the layer.  The
+// selection's validity reads make tile times uneven, and in the fused shape every later tile's
+// look-back waits on them; recent selections are short and stay fused.
+template <bool SPLIT>
+__global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
+    k_sample_fused_del(GraphView GV, QueryIn Q, LayerOut O, TileCtl C, int64_t* counts, uint32_t* picks, int64_t cap_q) {
+  constexpr int FT = GF_DEL_THREADS;
+  constexpr int NW = FT / 32;
+  __shared__ uint32_t s_sel[NW][32][KMAX];
+  __shared__ uint8_t s_owner[NW][32 * KMAX];
+  __shared__ uint64_t s_key[NW][32];
+  __shared__ int32_t s_pre[NW][32];
+  __shared__ int32_t s_wsum[NW];
+  __shared__ unsigned s_tile;
+  __shared__ int64_t s_base;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t tile = blockIdx.x;
+  if (!SPLIT) {
+    if (threadIdx.x == 0) s_tile = (unsigned)atomicAdd(C.ticket, 1ull);
+    __syncthreads();
+    tile = s_tile;
+    if (tile == 0 && threadIdx.x == 0) const_cast<int64_t*>(O.offsets)[0] = 0;
+  }
+  const int64_t n = query_count(Q);
+  if (SPLIT) {  // the scan runs over cap_q counts
+    const int64_t qq = tile * FT + threadIdx.x;
+    if (qq >= n && qq < cap_q) counts[qq] = 0;
+  }
+  if (tile * FT >= n) return;
+  const int64_t q = tile * FT + threadIdx.x;
+
+  // ---- window search (as the fast path) ----
+  DelWin W{0, 0, 0, 0, 0, 0, false};
+  uint64_t qkey = 0;
+  if (q < n) {
+    const int64_t v = Q.src[q];
+    const int64_t te = Q.t_end[q];
+    qkey = Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q;
+    if (v >= 0 && v < GV.num_nodes) {
+      const int64_t* r = GV.nrec + v * NREC;
+      LaneNode N;
+      int64_t w2, w3;
+      ld256(r, N.d0, N.ns, w2, N.first);
+      ld256(r + 4, N.tcum, N.tbase, N.ttmin, N.tmax);
+      ld256(r + 8, N.htmin, w3, w3, w3);
+      N.nb = w2 & 0xffffffffll;
+      N.valid = (w2 & NREC_VALID) != 0;  // cleared by delete_node (sampling.py:153-155)
+      N.irregular = (w2 & NREC_IRREG) != 0;
+      if (N.valid && N.nb > 0) {
+        const int64_t tsr = t_start_of(Q, q, te);
+        const LaneBnd h = lane_list_lower_bound(GV, N, te);
+        const int64_t lo = (tsr == GF_TS_MIN) ? N.first : lane_list_lower_bound(GV, N, tsr).pos;
+        if (h.pos > lo) W = DelWin{lo, h.pos, h.cum, h.base + (h.pos - 1 - h.cum), N.d0, N.nb, N.irregular};
+      }
+    }
+  }
+
+  // ---- selection: validity-checked picks into s_sel ----
+  uint32_t* sel = &s_sel[w][lane][0];
+  int k = 0;
+  bool hard = false;
+  const int fan = (int)Q.fanout;
+  if (W.hi > W.lo) {
+    const int64_t npos = W.hi - W.lo;
+    if (Q.policy == GF_POLICY_RECENT) {
+      // the newest DEL_SCAN positions as one candidate mask; newest first
+      DelWin WS = W;
+      WS.lo = max(W.lo, W.hi - DEL_SCAN);
+      uint64_t mm = window_mask(GV, WS);
+      const int64_t stop = WS.lo;
+      while (mm && k < fan) {
+        const int b = 63 - __clzll(mm);
+        mm &= ~(1ull << b);
+        sel[(k++ + lane) & (KMAX - 1)] = del_slot(GV, W, stop + b);
+      }
+      hard = k < fan && stop > W.lo;  // valid candidates may remain below the lane's bound
+    } else if (npos > GEN_EXACT) {
+      // Floyd first: the fast path's k distinct positions (the same Philox draws); its candidates are
+      // kept (in draw order) -- all of them for every query no deletion touches, which then gets
+      // its pre-deletion sample.  Kept Floyd picks are a uniform subset of the valid candidates of
+      // a uniform size, so topping them up with uniform new valid draws leaves a uniform k-subset.
+      {
+        int32_t pick[KMAX];
+        floyd_positions(Q.seed, qkey, npos, fan, pick);
+        uint32_t sl[KMAX];
+#pragma unroll
+        for (int i = 0; i < KMAX; i++)
+          if (i < fan) sl[i] = del_slot(GV, W, W.lo + pick[i]);
+        unsigned okm = 0;  // every bit load in flight together
+#pragma unroll
+        for (int i = 0; i < KMAX; i++)
+          if (i < fan && cand_ok(GV, sl[i])) okm |= 1u << i;
+#pragma unroll
+        for (int i = 0; i < KMAX; i++)
+          if ((okm >> i) & 1) sel[(k++ + lane) & (KMAX - 1)] = sl[i];
+        DEL_STAT(4, k < fan ? 1 : 0);
+      }
+      // then rejection draws over positions (fanout <= KMAX <= KREJ), 4 in flight, kept when valid and new
+      const int64_t dmax = rej_max(Q.fanout);
+      for (int64_t d = 0; k < fan && d < dmax; d += 4) {
+        uint32_t sl[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          ok[u] = false;
+          if (d + u < dmax) {
+            const int64_t p = W.lo + (int64_t)bounded64(rand64(Q.seed, qkey, REJ_TAG + (uint64_t)(d + u)), (uint64_t)npos);
+            sl[u] = del_slot(GV, W, p);
+            ok[u] = cand_ok(GV, sl[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          if (ok[u] && k < fan) {
+            bool dup = false;
+            for (int j = 0; j < k; j++) dup |= sel[(j + lane) & (KMAX - 1)] == sl[u];
+            if (!dup) sel[(k++ + lane) & (KMAX - 1)] = sl[u];
+          }
+        }
+      }
+      if (k < fan) {  // draws exhausted: the exact path, by the warp
+        hard = true;
+        k = 0;
+      }
+    } else {  // exact over at most GEN_EXACT positions: validity mask, bit i = position lo + i
+      const uint64_t m = window_mask(GV, W);
+      const int nv = __popcll(m);
+      k = min(nv, fan);
+      if (k == nv) {  // newest first
+        uint64_t mm = m;
+        for (int i = 0; i < k; i++) {
+          const int b = 63 - __clzll(mm);
+          mm &= ~(1ull << b);
+          sel[(i + lane) & (KMAX - 1)] = del_slot(GV, W, W.lo + b);
+        }
+      } else {  // Floyd's k-of-nv over the chronological valid ranks
+        int t[KMAX];
+#pragma unroll
+        for (int i = 0; i < KMAX; i++) {
+          if (i < k) {
+            const int j = nv - k + i;
+            const int ti = (int)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
+            bool dup = false;
+#pragma unroll
+            for (int c = 0; c < KMAX; c++) dup |= (c < i) && t[c] == ti;
+            t[i] = dup ? j : ti;
+            sel[(i + lane) & (KMAX - 1)] = del_slot(GV, W, W.lo + nth_set_bit64(m, t[i]));
+          }
+        }
+      }
+    }
+  }
+  DEL_STAT(0, 1);
+  DEL_STAT(1, W.hi > W.lo && W.hi - W.lo <= GEN_EXACT ? 1 : 0);
+  DEL_STAT(2, hard ? 1 : 0);
+  DEL_STAT(3, hard ? W.hi - W.lo : 0);
+  // queries the lanes could not finish: their warp takes them one at a time
+  for (unsigned hm = __ballot_sync(0xffffffffu, hard); hm; hm &= hm - 1) {
+    const int L = __ffs(hm) - 1;
+    DelWin WL;
+    WL.lo = __shfl_sync(0xffffffffu, W.lo, L);
+    WL.hi = __shfl_sync(0xffffffffu, W.hi, L);
+    WL.cum = __shfl_sync(0xffffffffu, W.cum, L);
+    WL.slot_hi = __shfl_sync(0xffffffffu, W.slot_hi, L);
+    WL.d0 = __shfl_sync(0xffffffffu, W.d0, L);
+    WL.nb = __shfl_sync(0xffffffffu, W.nb, L);
+    WL.irregular = __shfl_sync(0xffffffffu, (int)W.irregular, L) != 0;
+    const uint64_t kl = __shfl_sync(0xffffffffu, qkey, L);
+    const int kk = warp_select_general(GV, Q, WL, kl, &s_sel[w][L][0], L);
+    if (lane == L) k = kk;
+  }
+
+  if (SPLIT) {
+    __syncwarp();
+    if (q < n) {
+      counts[q] = k;
+      for (int i = 0; i < k; i++) picks[q * KMAX + i] = sel[(i + lane) & (KMAX - 1)];
+    }
+    return;
+  }
+
+  // ---- tile scan, owners, look-back, gather/store (k_sample_fused) ----
+  int incl = 0, wpre = 0, agg = 0;
+  tile_publish<NW>(k, lane, w, s_wsum, C, tile, incl, wpre, agg);
+  const int pre = incl - k;
+  s_pre[w][lane] = pre;
+  s_key[w][lane] = qkey;
+  for (int i = 0; i < k; i++) s_owner[w][pre + i] = (uint8_t)lane;
+  __syncwarp();
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  auto slot_e = [&](int j, int i) { return s_sel[w][j][(i + j) & (KMAX - 1)]; };
+  // the first gather round is issued before the look-back (its loads need no output base)
+  constexpr int GU = GF_GATHER_UNROLL;
+  Slot s0[GU];
+  int j0[GU];
+  int e = lane;
+  const bool round0 = e + 32 * (GU - 1) < total;
+  if (round0) {
+#pragma unroll
+    for (int u = 0; u < GU; u++) {
+      j0[u] = s_owner[w][e + 32 * u];
+      s0[u] = load_slot(GV.slots + slot_e(j0[u], e + 32 * u - s_pre[w][j0[u]]));
+    }
+  }
+  if (w == 0) {
+    int64_t excl = 0;
+    if (tile > 0) {
+      int64_t end = tile - 1;
+      while (true) {
+        const int64_t idx = end - lane;
+        uint64_t st;
+        do {
+          st = idx >= 0 ? ld_relaxed(C.status + idx) : TS_INC;
+        } while (__any_sync(0xffffffffu, (st >> 62) == 0));
+        const unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        const int first = inc ? __ffs(inc) - 1 : 31;
+        int64_t v = lane <= first ? (int64_t)(st & TS_VAL) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+        end -= 32;
+      }
+      if (lane == 0) st_relaxed(C.status + tile, TS_INC | (uint64_t)(excl + agg));
+    }
+    if (lane == 0) s_base = excl;
+  }
+  __syncthreads();
+  const int64_t base = s_base;
+  const int64_t out = base + wpre + pre;
+  if (q < n) {
+    const_cast<int64_t*>(O.offsets)[q + 1] = out + k;
+    if (q == n - 1) *C.total = out + k;
+  }
+  const int64_t out0 = base + wpre;
+  if (round0) {
+#pragma unroll
+    for (int u = 0; u < GU; u++) store_out(O, out0 + e + 32 * u, s0[u], s_key[w][j0[u]], e + 32 * u - s_pre[w][j0[u]]);
+    e += 32 * GU;
+  }
+  for (; e + 32 * (GU - 1) < total; e += 32 * GU) {
+    Slot sv[GU];
+    int jv[GU];
+#pragma unroll
+    for (int u = 0; u < GU; u++) {
+      jv[u] = s_owner[w][e + 32 * u];
+      sv[u] = load_slot(GV.slots + slot_e(jv[u], e + 32 * u - s_pre[w][jv[u]]));
+    }
+#pragma unroll
+    for (int u = 0; u < GU; u++) store_out(O, out0 + e + 32 * u, sv[u], s_key[w][jv[u]], e + 32 * u - s_pre[w][jv[u]]);
+  }
+  for (; e < total; e += 32) {
+    const int j = s_owner[w][e];
+    const int i = e - s_pre[w][j];
+    store_out(O, out0 + e, load_slot(GV.slots + slot_e(j, i)), s_key[w][j], i);
+  }
+}
+
+// The layer of a split post-deletion selection: a warp per 32 consecutive queries owns their
+// contiguous output range and moves it with coalesced stores (as k_sample_fused's gather/store)
+__global__ void __launch_bounds__(256) k_gather_picks(GraphView GV, QueryIn Q, LayerOut O, const uint32_t* __restrict__ picks) {
+  __shared__ uint8_t s_owner[8][32 * KMAX];
+  __shared__ int32_t s_pre[8][32];
+  __shared__ uint64_t s_key[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t n = query_count(Q);
+  const int64_t q0 = ((int64_t)blockIdx.x * 8 + w) * 32;
+  if (q0 >= n) return;
+  const int64_t q = q0 + lane;
+  const int64_t base = O.offsets[q0];
+  const int k = q < n ? (int)(O.offsets[q + 1] - O.offsets[q]) : 0;
+  int incl = k;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int pre = incl - k, total = __shfl_sync(0xffffffffu, incl, 31);
+  s_pre[w][lane] = pre;
+  s_key[w][lane] = q < n ? (Q.keys ? Q.keys[q] : Q.key_base + (uint64_t)q) : 0;
+  for (int i = 0; i < k; i++) s_owner[w][pre + i] = (uint8_t)lane;
+  __syncwarp();
+  constexpr int GU = GF_GATHER_UNROLL;
+  int e = lane;
+  for (; e + 32 * (GU - 1) < total; e += 32 * GU) {
+    Slot sv[GU];
+    int jv[GU];
+#pragma unroll
+    for (int u = 0; u < GU; u++) {
+      jv[u] = s_owner[w][e + 32 * u];
+      sv[u] = load_slot(GV.slots + picks[(q0 + jv[u]) * KMAX + (e + 32 * u - s_pre[w][jv[u]])]);
+    }
+#pragma unroll
+    for (int u = 0; u < GU; u++) store_out(O, base + e + 32 * u, sv[u], s_key[w][jv[u]], e + 32 * u - s_pre[w][jv[u]]);
+  }
+  for (; e < total; e += 32) {
+    const int j = s_owner[w][e];
+    const int i = e - s_pre[w][j];
+    store_out(O, base + e, load_slot(GV.slots + picks[(q0 + j) * KMAX + i]), s_key[w][j], i);
+  }
+}
+
 // ============================== host side ====================================
 
 __global__ void k_total(const int64_t* offsets, const int64_t* n_dev, int64_t n, int64_t* total) {
@@ -1291,13 +1761,18 @@ bool fused_enabled() {
 
 // total must already be zero (callers clear their totals once per call): a layer with no
 // queries launches nothing that would write it.
+// after deletions the fused path is k_sample_fused_del; its Floyd-first selection exists only there,
+// so GF_NO_FUSED (the unfused A/B kernels) applies to graphs without deletions
 bool uses_fused(const gf_graph* g, int64_t fanout) {
-  return !g->any_deleted && fanout <= KMAX && g->slot_cap < (1ll << 32) && fused_enabled();
+  return fanout <= KMAX && g->slot_cap < (1ll << 32) && (fused_enabled() || g->any_deleted);
 }
 
-int tile_threads(int policy) { return policy == GF_POLICY_RECENT ? fused_threads<true>() : fused_threads<false>(); }
-int64_t tile_words(int64_t cap_q, int policy) {  // status words + ticket
-  return (cap_q + tile_threads(policy) - 1) / tile_threads(policy) + 1;
+int tile_threads(const gf_graph* g, int policy) {
+  if (g->any_deleted) return GF_DEL_THREADS;
+  return policy == GF_POLICY_RECENT ? fused_threads<true>() : fused_threads<false>();
+}
+int64_t tile_words(const gf_graph* g, int64_t cap_q, int policy) {  // status words + ticket
+  return (cap_q + tile_threads(g, policy) - 1) / tile_threads(g, policy) + 1;
 }
 
 // tile_state: (tiles + 1) zeroed words for the fused kernel, or NULL to allocate them here
@@ -1307,7 +1782,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
   const bool fast = !g->any_deleted;
   if (uses_fused(g, Q.fanout) && cap_q > 0) {
     // offsets[0] is written by tile 0, which always runs
-    const int ft = tile_threads(Q.policy);
+    const int ft = tile_threads(g, Q.policy);
     const int64_t tiles = (cap_q + ft - 1) / ft;
     Scratch sb(s);
     if (!tile_state) {
@@ -1316,7 +1791,20 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
       GF_CUDA(cudaMemsetAsync(tile_state, 0, sizeof(uint64_t) * (tiles + 1), s));
     }
     TileCtl C{tile_state, reinterpret_cast<unsigned long long*>(tile_state + tiles), total};
-    if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, ft, 0, s, GV, Q, O, C);
+    if (g->any_deleted && Q.policy != GF_POLICY_RECENT) {  // split: select, scan, gather
+      Scratch ps(s);
+      GF_TRY(ps.alloc(sizeof(int64_t) * (size_t)cap_q + sizeof(uint32_t) * KMAX * (size_t)cap_q + 256));
+      int64_t* counts = ps.as<int64_t>();
+      uint32_t* picks = reinterpret_cast<uint32_t*>(counts + cap_q);
+      GF_LAUNCH(k_sample_fused_del<true>, tiles, ft, 0, s, GV, Q, O, C, counts, picks, cap_q);
+      GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
+      GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
+      GF_LAUNCH(k_total, 1, 1, 0, s, d_offsets, Q.n_dev, Q.n, total);
+      GF_LAUNCH(k_gather_picks, (cap_q + 255) / 256, 256, 0, s, GV, Q, O, picks);
+      return GF_OK;
+    }
+    if (g->any_deleted) GF_LAUNCH(k_sample_fused_del<false>, tiles, ft, 0, s, GV, Q, O, C, nullptr, nullptr, cap_q);
+    else if (Q.policy == GF_POLICY_RECENT) GF_LAUNCH(k_sample_fused<true>, tiles, ft, 0, s, GV, Q, O, C);
     else GF_LAUNCH(k_sample_fused<false>, tiles, ft, 0, s, GV, Q, O, C);
     return GF_OK;
   }
@@ -1352,6 +1840,12 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
 
 extern "C" {
 
+#if GF_DEL_STATS
+__attribute__((visibility("default"))) int gf_ab_del_stats(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(host, g_del_stats, sizeof(unsigned long long) * 8);
+}
+#endif
 #if GF_AB_TRACE
 // measurement-only export of the A/B trace variant (not in include/gfb200.h)
 __attribute__((visibility("default"))) int gf_ab_trace_dump(unsigned long long* host, int tiles) {
@@ -1415,7 +1909,7 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
     const int64_t cq = (h == 0) ? n_roots : h_caps[h - 1];
     if (uses_fused(g, h_fanouts[h]) && cq > 0) {
       tile_off[h] = zero_words;
-      zero_words += tile_words(cq, policy);
+      zero_words += tile_words(g, cq, policy);
     }
   }
   const size_t bytes = sizeof(int64_t) * (size_t)zero_words + 256 + 2 * sizeof(uint64_t) * (size_t)key_cap + 512;

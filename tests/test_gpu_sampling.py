@@ -106,6 +106,45 @@ def test_layer_bitwise_vs_oracle(cuda_device, policy, deletions):
                 np.testing.assert_array_equal(getattr(lay, nm), w, err_msg=f"case {case} f{f} {nm}")
 
 
+@pytest.mark.parametrize("policy", ["recent", "uniform", "time_window"])
+def test_ingest_after_deletions_bitwise_vs_oracle(cuda_device, policy):
+    """Deletions, then more batches (some edges into the deleted nodes), then sampling: the candidate
+    bitmap the post-deletion sampler reads is kept current by ingest and rebuilt by every delete."""
+    import paper_2311_17410_b200 as gf
+    from oracle import OracleGraph
+
+    rng = np.random.default_rng(77)
+    for case in range(4):
+        directed = bool(case % 2)
+        tau = int(rng.choice([1, 4, 48, 512]))
+        n_nodes, m = int(rng.integers(20, 300)), int(rng.integers(2000, 8000))
+        g = gf.DynamicGraph(directed=directed, tau=tau)
+        o = OracleGraph(directed, tau)
+        src = rng.integers(0, n_nodes, m); dst = rng.integers(0, n_nodes, m)
+        ts = np.sort(rng.integers(0, 5 * m, m))
+        cut = [0, m // 3, 2 * m // 3, m]
+        for b in range(3):
+            sl = slice(cut[b], cut[b + 1])
+            g.add_edges_arrays(src[sl], dst[sl], ts[sl])
+            o.add_edges(src[sl], dst[sl], ts[sl])
+            if b < 2:  # delete between batches: later batches append behind the deletions
+                dels = rng.choice(cut[b + 1], size=cut[b + 1] // 9, replace=False)
+                assert g.delete_edges(dels) == o.delete_edges(dels)
+                v = int(rng.integers(0, n_nodes))
+                assert g.delete_node(v) == o.delete_node(v)
+        nq = 4000
+        q = rng.integers(0, g.num_nodes, nq)
+        t1 = rng.integers(0, int(ts[-1]) + 10, nq)
+        t0 = np.where(rng.random(nq) < 0.5, TS_MIN, t1 - rng.integers(0, int(ts[-1]) + 1, nq))
+        delta = max(1, int(ts[-1]) // 5)
+        pol = gf.SamplingPolicy(policy, delta if policy == "time_window" else 0)
+        for f in (1, 7, 10, 16):
+            lay = gf.sample_layer(g, q, t0, t1, f, pol, seed=99 + f)
+            want = o.sample_layer(q, t0, t1, f, policy, delta, seed=99 + f)
+            for nm, w in zip(("offsets", "neighbors", "edge_ids", "timestamps"), want):
+                np.testing.assert_array_equal(getattr(lay, nm), w, err_msg=f"case {case} f{f} {nm}")
+
+
 @pytest.mark.parametrize("policy", ["recent", "uniform"])
 def test_khop_bitwise_vs_oracle_and_sharding_invariance(cuda_device, policy):
     import torch
