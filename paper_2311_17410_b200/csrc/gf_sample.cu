@@ -246,18 +246,31 @@ __device__ __forceinline__ int64_t pick32(int64_t w0, int64_t w1, int64_t w2, in
   return (int64_t)(int32_t)((i & 1) ? (uint64_t)w >> 32 : (uint64_t)w);
 }
 
+// Callers start with the virtual bracket lo = -1, hi = n (the run length).  Inside the run the values
+// ascend and run[lo] < x <= run[hi], so a chunk's count is the entries before the run (virtual, < x)
+// plus the run entries < x: one 8-bit compare mask masked to the run, no per-entry bracket tests.
 __device__ __forceinline__ void bracket_search32(const int32_t* __restrict__ run, int mis, int& lo, int& hi, int64_t& tl,
                                                  int64_t& th, int64_t x) {
+  const int n = hi;
+  // every stored timestamp fits int32 here (ts32): v < x is all-true above INT32_MAX, all-false below
+  const unsigned all = x > (int64_t)INT32_MAX ? 0xffu : 0u;
+  const bool cmp = x > (int64_t)INT32_MIN && x <= (int64_t)INT32_MAX;
+  const int32_t x32 = (int32_t)x;
   for (int step = 0; hi - lo > 1; step++) {
     const int g0 = ((probe_rel(lo, hi, x, tl, th, step) + mis) & ~7) - mis;
     int64_t w0, w1, w2, w3;
     ld256(run + g0, w0, w1, w2, w3);
-    int k = 0;
+    const int32_t v[8] = {(int32_t)w0, (int32_t)(w0 >> 32), (int32_t)w1, (int32_t)(w1 >> 32),
+                          (int32_t)w2, (int32_t)(w2 >> 32), (int32_t)w3, (int32_t)(w3 >> 32)};
+    unsigned mv = all;
+    if (cmp) {
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-      const int idx = g0 + i;
-      k += (idx <= lo || (idx < hi && pick32(w0, w1, w2, w3, i) < x)) ? 1 : 0;
+      for (int i = 0; i < 8; i++) mv |= (v[i] < x32) ? (1u << i) : 0u;
     }
+    const int neg = min(max(-g0, 0), 8);      // chunk entries before the run
+    const int inr = min(max(n - g0, 0), 8);   // chunk entries before the run's end
+    const unsigned mr = ((1u << inr) - 1u) & ~((1u << neg) - 1u);
+    const int k = neg + __popc(mv & mr);
     if (k > 0 && g0 + k - 1 > lo) {
       lo = g0 + k - 1;
       tl = pick32(w0, w1, w2, w3, k - 1);
