@@ -175,20 +175,35 @@ def dist_setup(args):
 
         if args.gpus not in (1, world) and rank == 0:
             print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} ranks", file=sys.stderr)
-        # the NCCL communicator-init lines (rank count, NVLink/NVLS transport) go to stderr
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if _backend() == "gloo":
+            # GF_BENCH_BACKEND=gloo: exercise the multi-rank path with several ranks sharing the GPUs
+            # of a smaller box (ranks map to devices round-robin; host-staged collectives)
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            # the NCCL communicator-init lines (rank count, NVLink/NVLS transport) go to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         # one tiny collective so the communicator (and its INIT log) exists before any timing
-        t = torch.ones(1, device="cuda")
+        t = torch.ones(1, device=_coll_device())
         dist.all_reduce(t)
         if rank == 0:
-            print(f"bench: NCCL communicator up, {int(t.item())} ranks", file=sys.stderr, flush=True)
+            print(f"bench: {_backend()} communicator up, {int(t.item())} ranks", file=sys.stderr, flush=True)
     else:
         if torch.cuda.is_available():
             torch.cuda.set_device(0)
     return world, rank, local
+
+
+def _backend() -> str:
+    return os.environ.get("GF_BENCH_BACKEND", "nccl")
+
+
+def _coll_device() -> str:
+    return "cpu" if _backend() == "gloo" else "cuda"
 
 
 def barrier(world):
@@ -204,7 +219,7 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -215,7 +230,7 @@ def sum_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
