@@ -964,9 +964,11 @@ __device__ __forceinline__ int64_t ev_node(const int64_t* rec, uint32_t e, int d
 }
 
 __global__ void __launch_bounds__(CO_T, 1)
-    k_ingest_coop(const IngestScalars* S, IngestCounters* c, int64_t* rec, int64_t n, int directed, int64_t node_cap,
-                  int sort_bits, CoopBufs CB, NodeArrays N, BlockArrays B, DirArrays D, SlotArrays SA, int kind,
-                  int64_t tau, int64_t param) {
+    k_ingest_coop(const __grid_constant__ IngestScalars S_, IngestCounters* c, int64_t* rec, int64_t n, int directed,
+                  int64_t node_cap, int sort_bits, CoopBufs CB, NodeArrays N, BlockArrays B, DirArrays D, SlotArrays SA,
+                  int kind, int64_t tau, int64_t param) {
+  // the per-call scalars arrive as a kernel parameter (no H2D copy ahead of the launch)
+  const IngestScalars* S = &S_;
   cg::grid_group grid = cg::this_grid();
   typedef cub::BlockRadixSort<uint32_t, CO_T, CO_ITEMS> BSortK;
   constexpr int HC = 2 * CO_T;  // per-CTA node hash: at most CO_T distinct nodes per sub-chunk
@@ -1643,14 +1645,14 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     memset(hci, 0, sizeof(IngestCounters));
     hci->minv = hci->tsmin = LLONG_MAX;
     hci->maxv = hci->tsmax = hci->max_eid = LLONG_MIN;
-    GF_CUDA(cudaMemcpyAsync(ds, hs, sizeof(IngestScalars), cudaMemcpyHostToDevice, s));
     GF_CUDA(cudaMemcpyAsync(dc, hci, sizeof(IngestCounters), cudaMemcpyHostToDevice, s));
+    (void)ds;
     NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
                  g->nflags, g->nrec};
     BlockArrays B{g->bcap, g->bsize, g->btmin, g->btmax, g->bprev, g->bnext, g->bbase};
     DirArrays D{g->dir};
     SlotArrays SA{g->slots, g->sts, g->fts, g->sts32, g->fts32, g->okbits, g->node_valid};
-    const IngestScalars* a_S = ds;
+    const IngestScalars a_S = *hs;
     int64_t a_n = n, a_cap = g->node_cap, a_tau = g->tau, a_param = g->sizing_param;
     int a_dir = dir, a_bits = bits_for(E + 1), a_kind = g->sizing_kind;
     void* args[] = {(void*)&a_S, (void*)&dc, (void*)&rec, (void*)&a_n, (void*)&a_dir, (void*)&a_cap, (void*)&a_bits,
