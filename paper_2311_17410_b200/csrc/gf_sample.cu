@@ -1434,7 +1434,8 @@ __device__ __forceinline__ int warp_select_general(const GraphView& GV, const Qu
 }
 
 // SPLIT (uniform / time-window): the selection ends the kernel -- counts[q] and the picks
-// picks[q * KMAX + i] go to HBM, a scan gives the offsets and k_gather_picks writes the layer.  The
+// picks[i * cap_q + q] (pick-major: a warp's stores of pick i are one line) go to HBM, a scan gives the
+// offsets and k_gather_picks writes the layer.  The
 // selection's validity reads make tile times uneven, and in the fused shape every later tile's
 // look-back waits on them; recent selections are short and stay fused.
 template <bool SPLIT>
@@ -1610,7 +1611,7 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
     __syncwarp();
     if (q < n) {
       counts[q] = k;
-      for (int i = 0; i < k; i++) picks[q * KMAX + i] = sel[(i + lane) & (KMAX - 1)];
+      for (int i = 0; i < k; i++) picks[i * cap_q + q] = sel[(i + lane) & (KMAX - 1)];
     }
     return;
   }
@@ -1694,7 +1695,8 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
 
 // The layer of a split post-deletion selection: a warp per 32 consecutive queries owns their
 // contiguous output range and moves it with coalesced stores (as k_sample_fused's gather/store)
-__global__ void __launch_bounds__(256) k_gather_picks(GraphView GV, QueryIn Q, LayerOut O, const uint32_t* __restrict__ picks) {
+__global__ void __launch_bounds__(256) k_gather_picks(GraphView GV, QueryIn Q, LayerOut O, const uint32_t* __restrict__ picks,
+                                                      int64_t cap_q) {
   __shared__ uint8_t s_owner[8][32 * KMAX];
   __shared__ int32_t s_pre[8][32];
   __shared__ uint64_t s_key[8][32];
@@ -1724,7 +1726,7 @@ __global__ void __launch_bounds__(256) k_gather_picks(GraphView GV, QueryIn Q, L
 #pragma unroll
     for (int u = 0; u < GU; u++) {
       jv[u] = s_owner[w][e + 32 * u];
-      sv[u] = load_slot(GV.slots + picks[(q0 + jv[u]) * KMAX + (e + 32 * u - s_pre[w][jv[u]])]);
+      sv[u] = load_slot(GV.slots + picks[(e + 32 * u - s_pre[w][jv[u]]) * cap_q + q0 + jv[u]]);
     }
 #pragma unroll
     for (int u = 0; u < GU; u++) store_out(O, base + e + 32 * u, sv[u], s_key[w][jv[u]], e + 32 * u - s_pre[w][jv[u]]);
@@ -1732,7 +1734,7 @@ __global__ void __launch_bounds__(256) k_gather_picks(GraphView GV, QueryIn Q, L
   for (; e < total; e += 32) {
     const int j = s_owner[w][e];
     const int i = e - s_pre[w][j];
-    store_out(O, base + e, load_slot(GV.slots + picks[(q0 + j) * KMAX + i]), s_key[w][j], i);
+    store_out(O, base + e, load_slot(GV.slots + picks[i * cap_q + q0 + j]), s_key[w][j], i);
   }
 }
 
@@ -1813,7 +1815,7 @@ gf_status layer_launch(gf_graph* g, const QueryIn& Q, int64_t cap_q, int64_t* d_
       GF_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), s));
       GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, counts, d_offsets + 1, cap_q, s); }, s));
       GF_LAUNCH(k_total, 1, 1, 0, s, d_offsets, Q.n_dev, Q.n, total);
-      GF_LAUNCH(k_gather_picks, (cap_q + 255) / 256, 256, 0, s, GV, Q, O, picks);
+      GF_LAUNCH(k_gather_picks, (cap_q + 255) / 256, 256, 0, s, GV, Q, O, picks, cap_q);
       return GF_OK;
     }
     if (g->any_deleted) GF_LAUNCH(k_sample_fused_del<false>, tiles, ft, 0, s, GV, Q, O, C, nullptr, nullptr, cap_q);
