@@ -1282,10 +1282,10 @@ __global__ void __launch_bounds__(THREADS) k_write_general(GraphView GV, QueryIn
 // Selected pool slots go to the per-query pick array; tile scan, decoupled look-back and the
 // cooperative gather/store are those of k_sample_fused.
 #ifndef GF_DEL_THREADS
-#define GF_DEL_THREADS 256
+#define GF_DEL_THREADS 512  // A/B: 128 / 256-query tiles 1.3x / 1.12x slower uniform selection
 #endif
 #ifndef GF_DEL_MINB
-#define GF_DEL_MINB 4  // 64 registers (A/B: 2 and 3 CTAs per SM of 256 are 1.4x / 1.15x slower)
+#define GF_DEL_MINB 2  // 64 registers (A/B at 256 threads: 2 and 3 CTAs per SM 1.4x / 1.15x slower than 4)
 #endif
 
 constexpr int DEL_SCAN = 64;
