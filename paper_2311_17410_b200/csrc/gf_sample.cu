@@ -174,10 +174,14 @@ __device__ __forceinline__ void store_out(const LayerOut& O, int64_t at, const S
   if (O.keys) __stcs((long long*)O.keys + at, (long long)child_key(qkey, (uint64_t)i));
 }
 
+// 64-bit division out of line: a power-of-two law shifts, and the division's inline expansion at
+// every pick site of the unrolled selection loops bloated the kernels past the instruction cache
+__device__ __noinline__ int64_t div64_ol(int64_t a, int64_t b) { return a / b; }
+
 // closed-form block index of a list position for regular lists (SizingLaw)
 __device__ __forceinline__ int64_t law_block(const SizingLaw& L, int64_t p) {
-  if (L.kind == GF_SIZING_FIXED) return L.size_shift >= 0 ? (p >> L.size_shift) : p / L.size;
-  if (p >= L.cum_m) return L.m + (L.tau_shift >= 0 ? ((p - L.cum_m) >> L.tau_shift) : (p - L.cum_m) / L.tau);
+  if (L.kind == GF_SIZING_FIXED) return L.size_shift >= 0 ? (p >> L.size_shift) : div64_ol(p, L.size);
+  if (p >= L.cum_m) return L.m + (L.tau_shift >= 0 ? ((p - L.cum_m) >> L.tau_shift) : div64_ol(p - L.cum_m, L.tau));
   return p == 0 ? 0 : 64 - __clzll(p);
 }
 
@@ -721,13 +725,24 @@ struct TileCtl {
   int64_t* total;               // layer total (written by the tile holding the last query)
 };
 
+// pool slot of list position p of an irregular list: the directory's binary search, out of line
+__device__ __noinline__ int64_t dir_slot_ol(const int64_t* __restrict__ dd, int64_t nb, int64_t p) {
+  int64_t lo = 0, hi = nb;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (__ldg(dd + m * DIRW + 1) <= p) lo = m + 1;
+    else hi = m;
+  }
+  const int64_t b = lo - 1;
+  return __ldg(dd + b * DIRW + 2) + (p - __ldg(dd + b * DIRW + 1));
+}
+
 // list position -> pool slot for a selected position (regular lists: closed form; else directory)
 __device__ __forceinline__ int64_t pool_slot_of64(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
   const int64_t* dd = GV.dir + d0 * DIRW;
   int64_t b, cum;
   if (irregular) {
-    b = dir_block_of(GV, d0, nb, p);
-    cum = __ldg(dd + b * DIRW + 1);
+    return dir_slot_ol(dd, nb, p);
   } else {
     b = law_block(GV.law, p);
     cum = law_cum(GV.law, b);
@@ -1060,9 +1075,17 @@ __device__ __forceinline__ bool node_ok(const GraphView& G_, int64_t v) {
 
 __device__ __forceinline__ bool slot_ok(const GraphView& G_, const Slot& s) { return s.valid && G_.node_valid[s.nbr]; }
 
-__device__ __forceinline__ int nth_set_bit(unsigned m, int n) {  // 0-based
-  for (int i = 0; i < n; i++) m &= m - 1;
-  return __ffs(m) - 1;
+__device__ __forceinline__ int nth_set_bit(unsigned m, int n) {  // 0-based: popcount bisection, no loop
+  int pos = 0, c;
+  c = __popc(m & 0xffffu);
+  if (n >= c) { n -= c; m >>= 16; pos += 16; }
+  c = __popc(m & 0xffu);
+  if (n >= c) { n -= c; m >>= 8; pos += 8; }
+  c = __popc(m & 0xfu);
+  if (n >= c) { n -= c; m >>= 4; pos += 4; }
+  c = __popc(m & 0x3u);
+  if (n >= c) { n -= c; m >>= 2; pos += 2; }
+  return pos + ((n >= (int)(m & 1u)) ? 1 : 0);
 }
 
 // timestamps < x in the block whose slots are sts[base, base + size)
@@ -1321,6 +1344,24 @@ __device__ __forceinline__ void floyd_positions(uint64_t seed, uint64_t qkey, in
   }
 }
 
+// rand64 as one out-of-line copy of Philox4x32-10 for the post-deletion kernels: their ~20 draw sites
+// inlined made the selection kernel larger than the instruction cache
+__device__ __noinline__ uint64_t rand64_ol(uint64_t seed, uint64_t qkey, uint64_t d) { return rand64(seed, qkey, d); }
+
+// floyd_positions with the out-of-line draws (the same values: draw i = rand64(seed, key, 2 blk0 + i))
+__device__ __forceinline__ void floyd_positions_ol(uint64_t seed, uint64_t qkey, int64_t nv, int k, int32_t (&pick)[KMAX]) {
+#pragma unroll
+  for (int i = 0; i < KMAX; i++) {
+    if (i < k) {
+      const int64_t t = (int64_t)bounded64(rand64_ol(seed, qkey, (uint64_t)i), (uint64_t)(nv - k + i + 1));
+      bool dup = false;
+#pragma unroll
+      for (int j = 0; j < KMAX; j++) dup |= (j < i) && pick[j] == (int32_t)t;
+      pick[i] = dup ? (int32_t)(nv - k + i) : (int32_t)t;
+    }
+  }
+}
+
 // pool slot sl is a candidate (valid edge, valid neighbour): one bit of the 1-bit-per-slot bitmap the
 // deletions maintain (gf_graph.cuh okbits), L2-resident, instead of the slot's own record
 __device__ __forceinline__ bool cand_ok(const GraphView& GV, uint32_t sl) {
@@ -1343,8 +1384,17 @@ struct DelWin {
   int64_t lo, hi, cum, slot_hi, d0, nb;
   bool irregular;
 };
+// a position before the boundary block, out of line: the post-deletion kernel maps positions at ~40
+// sites, and their inline closed-form/directory code overflowed the instruction cache
+__device__ __noinline__ uint32_t del_slot_ol(const SizingLaw* __restrict__ L, const int64_t* __restrict__ dir,
+                                             int64_t d0, int64_t nb, bool irregular, int64_t p) {
+  const int64_t* dd = dir + d0 * DIRW;
+  if (irregular) return (uint32_t)dir_slot_ol(dd, nb, p);
+  const int64_t b = law_block(*L, p);
+  return (uint32_t)(__ldg(dd + b * DIRW + 2) + (p - law_cum(*L, b)));
+}
 __device__ __forceinline__ uint32_t del_slot(const GraphView& GV, const DelWin& W, int64_t p) {
-  return p >= W.cum ? (uint32_t)(W.slot_hi - (W.hi - 1 - p)) : pool_slot_of(GV, W.irregular, W.d0, W.nb, p);
+  return p >= W.cum ? (uint32_t)(W.slot_hi - (W.hi - 1 - p)) : del_slot_ol(&GV.law, GV.dir, W.d0, W.nb, W.irregular, p);
 }
 
 // bits [s, s + len) of the candidate bitmap (len <= 64; the bitmap is padded past its end)
@@ -1379,6 +1429,7 @@ __device__ __forceinline__ uint64_t window_mask(const GraphView& GV, const DelWi
 
 // the whole warp selects for one query (uniform after failed draws / recent past DEL_SCAN): the
 // general kernels' algorithm; picks go to sel[(i + owner) % KMAX]; returns the count
+template <bool RECENT>
 __device__ __forceinline__ int warp_select_general(const GraphView& GV, const QueryIn& Q, const DelWin& W, uint64_t qkey,
                                    uint32_t* sel, int owner) {
   const int lane = lane_id();
@@ -1388,7 +1439,7 @@ __device__ __forceinline__ int warp_select_general(const GraphView& GV, const Qu
     sl = del_slot(GV, W, p);
     return cand_ok(GV, sl);
   };
-  const bool recent = Q.policy == GF_POLICY_RECENT;
+  constexpr bool recent = RECENT;
   int64_t nv = 0;
   if (!recent) {  // every valid candidate counts
     for (int64_t p0 = W.lo; p0 < W.hi; p0 += 32) {
@@ -1416,7 +1467,7 @@ __device__ __forceinline__ int warp_select_general(const GraphView& GV, const Qu
   int64_t want = -1;
   for (int i = 0; i < kmax; i++) {
     const int64_t j = nv - kmax + i;
-    const int64_t ti = (int64_t)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
+    const int64_t ti = (int64_t)bounded64(rand64_ol(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
     const bool dup = __any_sync(0xffffffffu, lane < i && want == ti);
     if (lane == i) want = dup ? j : ti;
   }
@@ -1440,7 +1491,8 @@ __device__ __forceinline__ int warp_select_general(const GraphView& GV, const Qu
 // look-back waits on them; recent selections are short and stay fused.
 template <bool SPLIT>
 __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
-    k_sample_fused_del(GraphView GV, QueryIn Q, LayerOut O, TileCtl C, int64_t* counts, uint32_t* picks, int64_t cap_q) {
+    k_sample_fused_del(const __grid_constant__ GraphView GV, QueryIn Q, LayerOut O, TileCtl C, int64_t* counts,
+                       uint32_t* picks, int64_t cap_q) {
   constexpr int FT = GF_DEL_THREADS;
   constexpr int NW = FT / 32;
   __shared__ uint32_t s_sel[NW][32][KMAX];
@@ -1499,7 +1551,10 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
   const int fan = (int)Q.fanout;
   if (W.hi > W.lo) {
     const int64_t npos = W.hi - W.lo;
-    if (Q.policy == GF_POLICY_RECENT) {
+    // each instantiation carries only its policy's branches (the host launches SPLIT for uniform /
+    // time-window and the fused form for recent): one kernel with all of them ran out of the
+    // instruction cache (half of its warp stalls were no-instruction)
+    if (!SPLIT) {
       // the newest DEL_SCAN positions as one candidate mask; newest first
       DelWin WS = W;
       WS.lo = max(W.lo, W.hi - DEL_SCAN);
@@ -1511,14 +1566,14 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
         sel[(k++ + lane) & (KMAX - 1)] = del_slot(GV, W, stop + b);
       }
       hard = k < fan && stop > W.lo;  // valid candidates may remain below the lane's bound
-    } else if (npos > GEN_EXACT) {
+    } else if (npos > GEN_EXACT) {  // SPLIT
       // Floyd first: the fast path's k distinct positions (the same Philox draws); its candidates are
       // kept (in draw order) -- all of them for every query no deletion touches, which then gets
       // its pre-deletion sample.  Kept Floyd picks are a uniform subset of the valid candidates of
       // a uniform size, so topping them up with uniform new valid draws leaves a uniform k-subset.
       {
         int32_t pick[KMAX];
-        floyd_positions(Q.seed, qkey, npos, fan, pick);
+        floyd_positions_ol(Q.seed, qkey, npos, fan, pick);
         uint32_t sl[KMAX];
 #pragma unroll
         for (int i = 0; i < KMAX; i++)
@@ -1541,7 +1596,7 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
         for (int u = 0; u < 4; u++) {
           ok[u] = false;
           if (d + u < dmax) {
-            const int64_t p = W.lo + (int64_t)bounded64(rand64(Q.seed, qkey, REJ_TAG + (uint64_t)(d + u)), (uint64_t)npos);
+            const int64_t p = W.lo + (int64_t)bounded64(rand64_ol(Q.seed, qkey, REJ_TAG + (uint64_t)(d + u)), (uint64_t)npos);
             sl[u] = del_slot(GV, W, p);
             ok[u] = cand_ok(GV, sl[u]);
           }
@@ -1576,7 +1631,7 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
         for (int i = 0; i < KMAX; i++) {
           if (i < k) {
             const int j = nv - k + i;
-            const int ti = (int)bounded64(rand64(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
+            const int ti = (int)bounded64(rand64_ol(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
             bool dup = false;
 #pragma unroll
             for (int c = 0; c < KMAX; c++) dup |= (c < i) && t[c] == ti;
@@ -1603,7 +1658,7 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
     WL.nb = __shfl_sync(0xffffffffu, W.nb, L);
     WL.irregular = __shfl_sync(0xffffffffu, (int)W.irregular, L) != 0;
     const uint64_t kl = __shfl_sync(0xffffffffu, qkey, L);
-    const int kk = warp_select_general(GV, Q, WL, kl, &s_sel[w][L][0], L);
+    const int kk = warp_select_general<!SPLIT>(GV, Q, WL, kl, &s_sel[w][L][0], L);
     if (lane == L) k = kk;
   }
 
