@@ -753,6 +753,15 @@ __device__ __forceinline__ int64_t pool_slot_of64(const GraphView& GV, bool irre
 __device__ __forceinline__ uint32_t pool_slot_of(const GraphView& GV, bool irregular, int64_t d0, int64_t nb, int64_t p) {
   return (uint32_t)pool_slot_of64(GV, irregular, d0, nb, p);
 }
+// the same out of line, for the selection loops: inlined at every unrolled pick site the closed-form /
+// directory code overflowed the instruction cache (L: the kernel's __grid_constant__ law)
+__device__ __noinline__ uint32_t pool_slot_ol(const SizingLaw* __restrict__ L, const int64_t* __restrict__ dir,
+                                              int64_t d0, int64_t nb, bool irregular, int64_t p) {
+  const int64_t* dd = dir + d0 * DIRW;
+  if (irregular) return (uint32_t)dir_slot_ol(dd, nb, p);
+  const int64_t b = law_block(*L, p);
+  return (uint32_t)(__ldg(dd + b * DIRW + 2) + (p - law_cum(*L, b)));
+}
 
 #ifndef GF_FUSED_MINB
 #define GF_FUSED_MINB 4
@@ -807,7 +816,7 @@ template <bool EARLY>
 #endif
 __global__ void __launch_bounds__(fused_threads<EARLY>(),
                                   EARLY ? GF_FUSED_MINB_RECENT : GF_FUSED_MINB * 256 / fused_threads<EARLY>())
-    k_sample_fused(GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
+    k_sample_fused(const __grid_constant__ GraphView GV, QueryIn Q, LayerOut O, TileCtl C) {
   constexpr int FT = fused_threads<EARLY>();
   constexpr int NW = FT / 32;
   constexpr int GU = EARLY ? GF_GATHER_UNROLL_RECENT : GF_GATHER_UNROLL;  // record loads in flight per lane
@@ -932,7 +941,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
         for (int r = 0; r < KMAX; r++) {
           if (r < k)
             s_sel[EARLY ? 0 : w][lane][(r + lane) & (KMAX - 1)] =
-                (r < inblk) ? (uint32_t)(slot_hi - r) : pool_slot_of(GV, irregular, d0, nb, hi - 1 - r);
+                (r < inblk) ? (uint32_t)(slot_hi - r) : pool_slot_ol(&GV.law, GV.dir, d0, nb, irregular, hi - 1 - r);
         }
       }
     } else {
@@ -960,7 +969,7 @@ __global__ void __launch_bounds__(fused_threads<EARLY>(),
       }
 #pragma unroll
       for (int i = 0; i < KMAX; i++)
-        if (i < k) s_sel[EARLY ? 0 : w][lane][(i + lane) & (KMAX - 1)] = pool_slot_of(GV, irregular, d0, nb, lo + pick[i]);
+        if (i < k) s_sel[EARLY ? 0 : w][lane][(i + lane) & (KMAX - 1)] = pool_slot_ol(&GV.law, GV.dir, d0, nb, irregular, lo + pick[i]);
     }
   }
 
@@ -1384,17 +1393,8 @@ struct DelWin {
   int64_t lo, hi, cum, slot_hi, d0, nb;
   bool irregular;
 };
-// a position before the boundary block, out of line: the post-deletion kernel maps positions at ~40
-// sites, and their inline closed-form/directory code overflowed the instruction cache
-__device__ __noinline__ uint32_t del_slot_ol(const SizingLaw* __restrict__ L, const int64_t* __restrict__ dir,
-                                             int64_t d0, int64_t nb, bool irregular, int64_t p) {
-  const int64_t* dd = dir + d0 * DIRW;
-  if (irregular) return (uint32_t)dir_slot_ol(dd, nb, p);
-  const int64_t b = law_block(*L, p);
-  return (uint32_t)(__ldg(dd + b * DIRW + 2) + (p - law_cum(*L, b)));
-}
 __device__ __forceinline__ uint32_t del_slot(const GraphView& GV, const DelWin& W, int64_t p) {
-  return p >= W.cum ? (uint32_t)(W.slot_hi - (W.hi - 1 - p)) : del_slot_ol(&GV.law, GV.dir, W.d0, W.nb, W.irregular, p);
+  return p >= W.cum ? (uint32_t)(W.slot_hi - (W.hi - 1 - p)) : pool_slot_ol(&GV.law, GV.dir, W.d0, W.nb, W.irregular, p);
 }
 
 // bits [s, s + len) of the candidate bitmap (len <= 64; the bitmap is padded past its end)
