@@ -1357,16 +1357,31 @@ __device__ __forceinline__ void floyd_positions(uint64_t seed, uint64_t qkey, in
 // inlined made the selection kernel larger than the instruction cache
 __device__ __noinline__ uint64_t rand64_ol(uint64_t seed, uint64_t qkey, uint64_t d) { return rand64(seed, qkey, d); }
 
-// floyd_positions with the out-of-line draws (the same values: draw i = rand64(seed, key, 2 blk0 + i))
+// Philox block `blk` of the stream keyed by (seed, key), out of line: draws 2 blk and 2 blk + 1
+__device__ __noinline__ uint4 philox_block_ol(uint64_t seed, uint64_t qkey, uint32_t blk) {
+  uint32_t c[4] = {blk, (uint32_t)qkey, (uint32_t)(qkey >> 32), GF_PHILOX_TAG};
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  return make_uint4(c[0], c[1], c[2], c[3]);
+}
+
+// floyd_positions with the out-of-line Philox, two draws per block (the same values)
 __device__ __forceinline__ void floyd_positions_ol(uint64_t seed, uint64_t qkey, int64_t nv, int k, int32_t (&pick)[KMAX]) {
 #pragma unroll
-  for (int i = 0; i < KMAX; i++) {
+  for (int i = 0; i < KMAX; i += 2) {
     if (i < k) {
-      const int64_t t = (int64_t)bounded64(rand64_ol(seed, qkey, (uint64_t)i), (uint64_t)(nv - k + i + 1));
-      bool dup = false;
+      const uint4 c = philox_block_ol(seed, qkey, (uint32_t)(i >> 1));
+      const int64_t t0 = (int64_t)bounded64((uint64_t)c.x | ((uint64_t)c.y << 32), (uint64_t)(nv - k + i + 1));
+      bool dup0 = false;
 #pragma unroll
-      for (int j = 0; j < KMAX; j++) dup |= (j < i) && pick[j] == (int32_t)t;
-      pick[i] = dup ? (int32_t)(nv - k + i) : (int32_t)t;
+      for (int j = 0; j < KMAX; j++) dup0 |= (j < i) && pick[j] == (int32_t)t0;
+      pick[i] = dup0 ? (int32_t)(nv - k + i) : (int32_t)t0;
+      if (i + 1 < k) {
+        const int64_t t1 = (int64_t)bounded64((uint64_t)c.z | ((uint64_t)c.w << 32), (uint64_t)(nv - k + i + 2));
+        bool dup1 = false;
+#pragma unroll
+        for (int j = 0; j < KMAX; j++) dup1 |= (j < i + 1) && pick[j] == (int32_t)t1;
+        pick[i + 1] = dup1 ? (int32_t)(nv - k + i + 1) : (int32_t)t1;
+      }
     }
   }
 }
