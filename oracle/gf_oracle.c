@@ -579,7 +579,7 @@ static int64_t sample_one_faithful(const or_graph* g, int64_t node, int64_t t_st
 #define OR_GEN_EXACT 64
 #define OR_KREJ 32
 #define OR_KFLOYD 16 /* KMAX: fanouts served by the fused kernels */
-#define OR_REJ_TAG (1ull << 40)
+#define OR_REJ_TAG (1ull << 31) /* Philox block 2^30 + d/2: disjoint from the Floyd draws */
 
 /* Early-exit path, same output: position-indexed view of the node list. */
 typedef struct {

@@ -106,7 +106,9 @@ struct QState {
 // The oracle (oracle/gf_oracle.c) makes the same decisions.
 constexpr int64_t GEN_EXACT = 64;
 constexpr int KREJ = 32;  // the rejection path serves fanouts up to 32
-constexpr uint64_t REJ_TAG = 1ull << 40;
+// draw index offset of the rejection draws: Philox block 2^30 + d/2, disjoint from the Floyd draws
+// (blocks 0..15); rand64 keys the block with the low 32 bits of d/2, so 2^40 aliased block d/2
+constexpr uint64_t REJ_TAG = 1ull << 31;
 __host__ __device__ constexpr int64_t rej_max(int64_t fanout) { return 8 * fanout + 32; }
 
 struct LayerOut {
@@ -1607,11 +1609,16 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
       for (int64_t d = 0; k < fan && d < dmax; d += 4) {
         uint32_t sl[4];
         bool ok[4];
+        // draws REJ_TAG + d .. + 3: two Philox blocks (d is even, REJ_TAG too)
+        const uint32_t blk = (uint32_t)((REJ_TAG + (uint64_t)d) >> 1);
+        const uint4 ca = philox_block_ol(Q.seed, qkey, blk), cb = philox_block_ol(Q.seed, qkey, blk + 1);
+        const uint64_t r4[4] = {(uint64_t)ca.x | ((uint64_t)ca.y << 32), (uint64_t)ca.z | ((uint64_t)ca.w << 32),
+                                (uint64_t)cb.x | ((uint64_t)cb.y << 32), (uint64_t)cb.z | ((uint64_t)cb.w << 32)};
 #pragma unroll
         for (int u = 0; u < 4; u++) {
           ok[u] = false;
           if (d + u < dmax) {
-            const int64_t p = W.lo + (int64_t)bounded64(rand64_ol(Q.seed, qkey, REJ_TAG + (uint64_t)(d + u)), (uint64_t)npos);
+            const int64_t p = W.lo + (int64_t)bounded64(r4[u], (uint64_t)npos);
             sl[u] = del_slot(GV, W, p);
             ok[u] = cand_ok(GV, sl[u]);
           }
@@ -1640,20 +1647,12 @@ __global__ void __launch_bounds__(GF_DEL_THREADS, GF_DEL_MINB)
           mm &= ~(1ull << b);
           sel[(i + lane) & (KMAX - 1)] = del_slot(GV, W, W.lo + b);
         }
-      } else {  // Floyd's k-of-nv over the chronological valid ranks
-        int t[KMAX];
+      } else {  // Floyd's k-of-nv over the chronological valid ranks (draws rand64 i)
+        int32_t t[KMAX];
+        floyd_positions_ol(Q.seed, qkey, nv, k, t);
 #pragma unroll
-        for (int i = 0; i < KMAX; i++) {
-          if (i < k) {
-            const int j = nv - k + i;
-            const int ti = (int)bounded64(rand64_ol(Q.seed, qkey, (uint64_t)i), (uint64_t)(j + 1));
-            bool dup = false;
-#pragma unroll
-            for (int c = 0; c < KMAX; c++) dup |= (c < i) && t[c] == ti;
-            t[i] = dup ? j : ti;
-            sel[(i + lane) & (KMAX - 1)] = del_slot(GV, W, W.lo + nth_set_bit64(m, t[i]));
-          }
-        }
+        for (int i = 0; i < KMAX; i++)
+          if (i < k) sel[(i + lane) & (KMAX - 1)] = del_slot(GV, W, W.lo + nth_set_bit64(m, t[i]));
       }
     }
   }
