@@ -384,11 +384,18 @@ def launch_key(name: str) -> str:
 
 
 def bench_ours(args, cfg, world, rank, local):
+    import gc
+
     import torch
 
     import paper_2311_17410_b200 as gf
     from paper_2311_17410_b200 import _lib
 
+    # as timeit does: no collector pauses inside timed regions (every sampling / ingest / fetch call
+    # synchronises with the host once, so a pause would show up as device idle time; single fetch
+    # passes measured up to 5x slower with the collector on)
+    gc.collect()
+    gc.disable()
     device = torch.device("cuda", local)
     R = cfg["roots"] if args.roots is None else args.roots
     if args.strong:  # fixed total root count (R = 2^23 split over the ranks)
@@ -682,10 +689,6 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50, world: int = 1,
     rows = sum(nk.numel() + ek.numel() for nk, ek in mb[2:])
     byts = sum(nk.numel() * (9 + 8 * FETCH_DV) + ek.numel() * (9 + 8 * FETCH_DE) for nk, ek in mb[2:])
     passes, hit_rates = [], []
-    import gc
-
-    gc.collect()
-    gc.disable()  # no collector pause inside a pass (the block synchronises with the host once per call)
     for _ in range(5):
         nsnap.restore_into(ncache)
         esnap.restore_into(ecache)
@@ -700,7 +703,6 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50, world: int = 1,
         torch.cuda.synchronize()
         passes.append(a.elapsed_time(b))
         hit_rates.append((ncache.stats()["hit_rate"], ecache.stats()["hit_rate"]))
-    gc.enable()
     ms = statistics.median(passes)
     _lib.profile_enable(True)
     for nk, ek in mb[2:6]:
