@@ -506,6 +506,9 @@ def bench_ours(args, cfg, world, rank, local):
         barrier(world)
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e2e_edges = 0
+        # results go back on a copy stream, so one policy's D2H overlaps the next policy's sampling
+        # (the D2H over PCIe is ~20x the sampling time)
+        copy_stream = torch.cuda.Stream(device=device)
         a0.record(stream)
         for _ in range(args.steps):
             bi = bo = 0
@@ -515,13 +518,17 @@ def bench_ours(args, cfg, world, rank, local):
                 t_d = rts_h.to(device, non_blocking=True)
                 bi += 2 * roots_h.numel() * 8
                 s = sampler[p].sample(r_d, t_d, root_key_base=key_base)
-                for lay in s.layers:
-                    e2e_edges += int(lay.neighbors.numel())
-                    for t in (lay.offsets, lay.neighbors, lay.edge_ids, lay.timestamps):
-                        hb = host_bufs[k]
-                        k += 1
-                        hb[: t.numel()].copy_(t, non_blocking=True)
-                        bo += t.numel() * 8
+                copy_stream.wait_stream(stream)
+                with torch.cuda.stream(copy_stream):
+                    for lay in s.layers:
+                        e2e_edges += int(lay.neighbors.numel())
+                        for t in (lay.offsets, lay.neighbors, lay.edge_ids, lay.timestamps):
+                            t.record_stream(copy_stream)  # the allocator keeps it until the copy is done
+                            hb = host_bufs[k]
+                            k += 1
+                            hb[: t.numel()].copy_(t, non_blocking=True)
+                            bo += t.numel() * 8
+        stream.wait_stream(copy_stream)
         a1.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -689,6 +696,8 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50, world: int = 1,
     rows = sum(nk.numel() + ek.numel() for nk, ek in mb[2:])
     byts = sum(nk.numel() * (9 + 8 * FETCH_DV) + ek.numel() * (9 + 8 * FETCH_DE) for nk, ek in mb[2:])
     passes, hit_rates = [], []
+    diag = os.environ.get("GF_FETCH_DIAG") is not None  # per-call host times to stderr (diagnostics only)
+    diag_rows = []
     for _ in range(5):
         nsnap.restore_into(ncache)
         esnap.restore_into(ecache)
@@ -697,13 +706,22 @@ def fetch_bench(g, src, dst, ts, cfg, device, batches: int = 50, world: int = 1,
         torch.cuda.synchronize()
         a.record()
         for nk, ek in mb[2:]:
+            t0 = time.perf_counter() if diag else 0.0
             gf.fetch_features(ncache, ntab, nk)
+            t1 = time.perf_counter() if diag else 0.0
             fetch_features_sharded(ecache, eshard, ek)
+            if diag:
+                t2 = time.perf_counter()
+                diag_rows.append((round((t1 - t0) * 1e3, 3), round((t2 - t1) * 1e3, 3)))
         b.record()
         torch.cuda.synchronize()
         passes.append(a.elapsed_time(b))
         hit_rates.append((ncache.stats()["hit_rate"], ecache.stats()["hit_rate"]))
     ms = statistics.median(passes)
+    if diag:
+        worst = sorted(range(len(diag_rows)), key=lambda i: -sum(diag_rows[i]))[:8]
+        print("fetch diag: passes", passes, "slowest calls (index, node ms, edge ms):",
+              [(i, diag_rows[i]) for i in worst], file=sys.stderr)
     _lib.profile_enable(True)
     for nk, ek in mb[2:6]:
         gf.fetch_features(ncache, ntab, nk)

@@ -1809,6 +1809,12 @@ __global__ void __launch_bounds__(256) k_gather_picks(GraphView GV, QueryIn Q, L
 
 // ============================== host side ====================================
 
+// the layer totals into pinned host memory (mapped under unified addressing)
+__global__ void k_totals_to_host(const int64_t* __restrict__ totals, int n, int64_t* host) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) host[i] = totals[i];
+  __threadfence_system();
+}
+
 __global__ void k_total(const int64_t* offsets, const int64_t* n_dev, int64_t n, int64_t* total) {
   *total = offsets[n_dev ? *n_dev : n];
 }
@@ -2056,7 +2062,13 @@ gf_status gf_sample_khop(gf_graph* g, const int64_t* d_roots, const int64_t* d_t
     in_keys = out_keys;
   }
   int64_t* h = hbuf;
-  GF_CUDA(cudaMemcpyAsync(h, totals, sizeof(int64_t) * (n_hops + 1), cudaMemcpyDeviceToHost, s));
+  if (h == g->smp_host) {
+    // the pinned totals are written by a kernel (zero-copy): a DMA copy would queue behind the
+    // caller's own D2H of earlier results on the copy engine and stall this return
+    GF_LAUNCH(k_totals_to_host, 1, 32, 0, s, totals, n_hops + 1, h);
+  } else {
+    GF_CUDA(cudaMemcpyAsync(h, totals, sizeof(int64_t) * (n_hops + 1), cudaMemcpyDeviceToHost, s));
+  }
   GF_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < n_hops; i++) h_totals[i] = h[i];
   if ((int)h[n_hops]) return fail(GF_ERANGE, "output buffer too small");
