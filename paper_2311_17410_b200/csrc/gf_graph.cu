@@ -48,7 +48,16 @@ struct IngestCounters {
   long long num_big;      // cooperative path: segments with more than 32 events
   long long num_moves;    // cooperative path: directories that move to a larger region
   long long phase_ns[12]; // cooperative path: globaltimer at each phase start (GF_INGEST_TIMING)
+  long long done;         // cooperative path: CTAs finished (the last one publishes and re-arms)
 };
+
+// the values every call starts from
+__host__ __device__ inline void counters_arm(IngestCounters* c) {
+  long long* w = reinterpret_cast<long long*>(c);
+  for (size_t i = 0; i < sizeof(IngestCounters) / sizeof(long long); i++) w[i] = 0;
+  c->minv = c->tsmin = LLONG_MAX;
+  c->maxv = c->tsmax = c->max_eid = LLONG_MIN;
+}
 // ABORT_SLOW (cooperative path only): the batch needs the general launch sequence -- an endpoint
 // may see a decreasing timestamp (possible rejection), or a segment exceeds what one CTA sorts
 constexpr long long ABORT_NODES = 1, ABORT_CAP = 2, ABORT_SLOW = 4;
@@ -909,14 +918,18 @@ __device__ __forceinline__ void grid_scan(cg::grid_group& grid, int64_t n, V1 va
   const int64_t G = gridDim.x, b = blockIdx.x;
   const int64_t chunk = ((n + G - 1) / G + CO_T - 1) / CO_T * CO_T;
   const int64_t lo = min(n, b * chunk), hi = min(n, lo + chunk);
-  int64_t part[K];
+  int64_t part[K], x1[K];  // x1: the item of a chunk of one round, kept for the scan pass
 #pragma unroll
-  for (int f = 0; f < K; f++) part[f] = 0;
+  for (int f = 0; f < K; f++) part[f] = x1[f] = 0;
+  const bool one_round = hi - lo <= CO_T;
   for (int64_t i = lo + threadIdx.x; i < hi; i += CO_T) {
     int64_t x[K];
     val1(i, x);
 #pragma unroll
-    for (int f = 0; f < K; f++) part[f] += x[f];
+    for (int f = 0; f < K; f++) {
+      part[f] += x[f];
+      x1[f] = x[f];
+    }
   }
   int64_t ex[K], t[K];
   cta_scan<K>(part, ex, t, sm);
@@ -942,7 +955,10 @@ __device__ __forceinline__ void grid_scan(cg::grid_group& grid, int64_t n, V1 va
   for (int64_t i0 = lo; i0 < hi; i0 += CO_T) {
     const int64_t i = i0 + threadIdx.x;
     int64_t x[K];
-    if (i < hi) val2(i, x);
+    if (i < hi && one_round)
+#pragma unroll
+      for (int f = 0; f < K; f++) x[f] = x1[f];
+    else if (i < hi) val2(i, x);
     else
 #pragma unroll
       for (int f = 0; f < K; f++) x[f] = 0;
@@ -966,9 +982,24 @@ __device__ __forceinline__ int64_t ev_node(const int64_t* rec, uint32_t e, int d
 __global__ void __launch_bounds__(CO_T, 1)
     k_ingest_coop(const __grid_constant__ IngestScalars S_, IngestCounters* c, int64_t* rec, int64_t n, int directed,
                   int64_t node_cap, int sort_bits, CoopBufs CB, NodeArrays N, BlockArrays B, DirArrays D, SlotArrays SA,
-                  int kind, int64_t tau, int64_t param) {
-  // the per-call scalars arrive as a kernel parameter (no H2D copy ahead of the launch)
+                  int kind, int64_t tau, int64_t param, IngestCounters* hout) {
+  // the per-call scalars arrive as a kernel parameter (no H2D copy ahead of the launch); the counters
+  // go back the other way without a copy either: the last CTA to finish writes them to the pinned
+  // host struct `hout` and re-arms `c` for the next call
   const IngestScalars* S = &S_;
+  auto finish = [&]() {  // every CTA, on every exit
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd((unsigned long long*)&c->done, 1ull) == gridDim.x - 1) {
+        __threadfence();
+        const long long* w = reinterpret_cast<const long long*>(c);
+        long long* o = reinterpret_cast<long long*>(hout);
+        for (size_t i = 0; i < sizeof(IngestCounters) / sizeof(long long); i++) o[i] = __ldcg(w + i);
+        counters_arm(c);
+      }
+    }
+  };
   cg::grid_group grid = cg::this_grid();
   typedef cub::BlockRadixSort<uint32_t, CO_T, CO_ITEMS> BSortK;
   constexpr int HC = 2 * CO_T;  // per-CTA node hash: at most CO_T distinct nodes per sub-chunk
@@ -1068,6 +1099,28 @@ __global__ void __launch_bounds__(CO_T, 1)
     }
     __syncthreads();
     // one counter atomic per (sub-chunk, node); the first to count a node lists it (one segment)
+#ifndef GF_AB_SEG_WARP
+    {  // the sub-chunk's fresh nodes take one range of the segment list: one list atomic per CTA
+      int32_t kk[HC / CO_T];
+      bool fr[HC / CO_T];
+      int64_t nf[1] = {0}, ex[1], tt[1];
+#pragma unroll
+      for (int q = 0; q < HC / CO_T; q++) {
+        const int i = q * CO_T + threadIdx.x;
+        kk[q] = sm.h.key[i];
+        fr[q] = kk[q] >= 0 && atomicAdd(&CB.ncnt[kk[q]], sm.h.cnt[i]) == 0;
+        nf[0] += fr[q] ? 1 : 0;
+      }
+      cta_scan<1>(nf, ex, tt, reinterpret_cast<int64_t(*)[1]>(s_scan));
+      __shared__ unsigned long long s_segbase;
+      if (threadIdx.x == 0) s_segbase = tt[0] ? atomicAdd((unsigned long long*)&c->num_segs, (unsigned long long)tt[0]) : 0ull;
+      __syncthreads();
+      int64_t pos = (int64_t)s_segbase + ex[0];
+#pragma unroll
+      for (int q = 0; q < HC / CO_T; q++)
+        if (fr[q]) CB.touched[pos++] = kk[q];
+    }
+#else
     for (int i0 = 0; i0 < HC; i0 += CO_T) {
       const int i = i0 + threadIdx.x;
       const int32_t k = sm.h.key[i];
@@ -1078,6 +1131,7 @@ __global__ void __launch_bounds__(CO_T, 1)
       base = __shfl_sync(0xffffffffu, base, fm ? __ffs(fm) - 1 : 0);
       if (fresh) CB.touched[base + __popc(fm & ((1u << lane) - 1))] = k;
     }
+#endif
   }
   grid.sync();
 
@@ -1085,6 +1139,7 @@ __global__ void __launch_bounds__(CO_T, 1)
   const int64_t nseg = ldl2(&c->num_segs);
   if (ldl2(&c->abort) & ABORT_NODES) {  // node ids beyond the table (or negative): undo the counts
     for (int64_t i = gtid; i < nseg; i += gstride) CB.ncnt[ldl2(&CB.touched[i])] = 0;
+    finish();
     return;
   }
   // ---- C: rows of new nodes; segment starts ----
@@ -1153,7 +1208,10 @@ __global__ void __launch_bounds__(CO_T, 1)
     }
   }
   grid.sync();
-  if (ldl2(&c->abort)) return;  // a segment beyond one CTA's sort
+  if (ldl2(&c->abort)) {  // a segment beyond one CTA's sort
+    finish();
+    return;
+  }
 
   COOP_MARK(3);
   // ---- E: each segment in append order ----
@@ -1310,7 +1368,10 @@ __global__ void __launch_bounds__(CO_T, 1)
       [&](int64_t i, int64_t (&o)[3]) { CB.off4[i] = make_longlong4(o[0], o[1], o[2], 0); },
       CB.ctot, reinterpret_cast<int64_t(*)[3]>(s_scan), tot3);
   COOP_MARK(9);
-  if (ldl2(&c->abort)) return;  // a possible rejection: the general sequence resolves the batch
+  if (ldl2(&c->abort)) {  // a possible rejection: the general sequence resolves the batch
+    finish();
+    return;
+  }
   if (tot3[1] > S->slots_free || tot3[2] > S->dir_free || tot3[0] - S->nfree > S->blocks_free) {
     if (gtid == 0) {
       c->new_blocks = tot3[0];
@@ -1318,6 +1379,7 @@ __global__ void __launch_bounds__(CO_T, 1)
       c->dir_need = tot3[2];
       c->abort |= ABORT_CAP;
     }
+    finish();
     return;  // every CTA holds the same totals
   }
   if (gtid == 0) {
@@ -1486,6 +1548,7 @@ __global__ void __launch_bounds__(CO_T, 1)
   for (int64_t j = gtid; j < n; j += gstride) S->out_eids[j] = has_eids ? rec[ER * j + ER_EID] : next_id + j;
   __syncthreads();
   COOP_MARK(6);
+  finish();
 }
 
 // node capacity only (rows are initialised on the device by k_grow_nodes)
@@ -1609,6 +1672,13 @@ gf_status ensure_coop(gf_graph* g, int64_t n, int64_t grid, cudaStream_t s) {
     const size_t want = probe.off + 4096 + (probe.off + 4096) / 4;
     GF_CUDA(cudaMallocAsync(&g->co_buf, want, s));
     g->co_bytes = want;
+    // the counters sit at a fixed offset of the buffer; armed once here, then by every launch's last CTA
+    Arena A;
+    A.base = (char*)g->co_buf;
+    IngestCounters* dc = std::get<1>(coop_layout(A, g, n, grid, CB));
+    IngestCounters armed;
+    counters_arm(&armed);
+    GF_CUDA(cudaMemcpyAsync(dc, &armed, sizeof(armed), cudaMemcpyHostToDevice, s));  // pageable: staged before return
   }
   return GF_OK;
 }
@@ -1630,7 +1700,6 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
   GF_TRY(stage_free_handles(g, s));
   const int64_t nfree = (int64_t)g->free_handles.size();
   IngestScalars* hs = (IngestScalars*)g->ing_host;
-  IngestCounters* hci = (IngestCounters*)((char*)g->ing_host + 1024);
   IngestCounters* hcp = (IngestCounters*)((char*)g->ing_host + 2048);
   IngestCounters hc;
   for (int attempt = 0;; attempt++) {
@@ -1642,10 +1711,6 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     *hs = IngestScalars{src_in, dst_in, ts_in, eids_user, out_user, g->num_nodes, g->blk_used, g->slots_used,
                         g->dir_used, g->next_edge_id, g->slot_cap - g->slots_used, g->dir_cap_total - g->dir_used,
                         g->free_dev, nfree, g->blk_cap - g->blk_used};
-    memset(hci, 0, sizeof(IngestCounters));
-    hci->minv = hci->tsmin = LLONG_MAX;
-    hci->maxv = hci->tsmax = hci->max_eid = LLONG_MIN;
-    GF_CUDA(cudaMemcpyAsync(dc, hci, sizeof(IngestCounters), cudaMemcpyHostToDevice, s));
     (void)ds;
     NodeArrays N{g->head, g->tail, g->num_blocks, g->degree, g->nslots, g->dir_off, g->dir_cap, g->node_valid,
                  g->nflags, g->nrec};
@@ -1657,13 +1722,12 @@ gf_status add_edges_coop(gf_graph* g, const int64_t* src_in, const int64_t* dst_
     int a_dir = dir, a_bits = bits_for(E + 1), a_kind = g->sizing_kind;
     void* args[] = {(void*)&a_S, (void*)&dc, (void*)&rec, (void*)&a_n, (void*)&a_dir, (void*)&a_cap, (void*)&a_bits,
                     (void*)&CB, (void*)&N, (void*)&B, (void*)&D, (void*)&SA, (void*)&a_kind, (void*)&a_tau,
-                    (void*)&a_param};
+                    (void*)&a_param, (void*)&hcp};
     cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
     GF_CUDA(cudaLaunchCooperativeKernel((const void*)k_ingest_coop, dim3((unsigned)grid), dim3(CO_T), args, 0, s));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e0) prof_stop("k_ingest_coop", s, e0);
-    GF_CUDA(cudaMemcpyAsync(hcp, dc, sizeof(IngestCounters), cudaMemcpyDeviceToHost, s));
-    GF_CUDA(cudaStreamSynchronize(s));
+    GF_CUDA(cudaStreamSynchronize(s));  // the kernel's last CTA wrote the counters to hcp
     hc = *hcp;
     static const bool timing = getenv("GF_INGEST_TIMING") != nullptr;
     if (timing && !hc.abort) {  // per-phase device time of the cooperative launch (CTA 0's view)
