@@ -350,14 +350,12 @@ __global__ void k_fifo_slots(int64_t head, int64_t cap, int64_t na, int64_t* asl
     aslot[j] = (head + j) % cap;
 }
 
-// free-slot flags, slot identities for the victim sort, and the score range of the occupied slots
-__global__ void k_free_flags(const int64_t* keys, const int64_t* scores, int64_t cap, int64_t* flag, uint32_t* iota,
-                             long long* mm) {
+// free-slot flags and the score range of the occupied slots
+__global__ void k_free_flags(const int64_t* keys, const int64_t* scores, int64_t cap, int64_t* flag, long long* mm) {
   long long lo = LLONG_MAX, hi = LLONG_MIN;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x) {
     const bool empty = keys[s] == GF_EMPTY_KEY;
     flag[s] = empty;
-    iota[s] = (uint32_t)s;
     if (!empty) {
       lo = min(lo, (long long)scores[s]);
       hi = max(hi, (long long)scores[s]);
@@ -377,16 +375,13 @@ __global__ void k_free_scatter(const int64_t* flag, const int64_t* pos, int64_t 
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x)
     if (flag[s]) free_slots[pos[s]] = s;
 }
-// order-preserving int64 -> uint64 for the (score, slot) radix sort
-__global__ void k_iota(uint32_t* iota, int64_t cap) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x)
-    iota[s] = (uint32_t)s;
-}
-
-// score - lo: order-preserving and narrow, so the victim sort runs over only the bits the range needs
-__global__ void k_score_keys(const int64_t* scores, int64_t cap, int64_t lo, uint64_t* out) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x)
+// score - lo: order-preserving and narrow, so the victim sort runs over only the bits the range needs;
+// the sort's values (slot ids) are written in the same pass
+__global__ void k_score_keys(const int64_t* scores, int64_t cap, int64_t lo, uint64_t* out, uint32_t* iota) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < cap; s += (int64_t)gridDim.x * blockDim.x) {
     out[s] = (uint64_t)(scores[s] - lo);
+    iota[s] = (uint32_t)s;
+  }
 }
 __global__ void k_victims(const uint32_t* sorted_slots, int64_t r, int64_t* aslot) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < r; j += (int64_t)gridDim.x * blockDim.x)
@@ -467,12 +462,11 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
       nfree = pre->nfree;
       hmm[0] = pre->lo;
       hmm[1] = pre->hi;
-      GF_LAUNCH(k_iota, grid_for(cap, 256, G), 256, 0, s, iota, cap);
     } else {
       long long* mm = reinterpret_cast<long long*>(F.take<int64_t>(2));
       const long long mm0[2] = {LLONG_MAX, LLONG_MIN};
       GF_CUDA(cudaMemcpyAsync(mm, mm0, sizeof(mm0), cudaMemcpyHostToDevice, s));
-      GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, iota, mm);
+      GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, mm);
       GF_TRY(cub_call([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, ff, fpos, (int)(cap + 1), s); }, s));
       GF_LAUNCH(k_free_scatter, grid_for(cap, 256, G), 256, 0, s, ff, fpos, cap, free_slots);
       GF_CUDA(cudaMemcpyAsync(&nfree, fpos + cap, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -493,7 +487,7 @@ gf_status place_impl(gf_cache* c, const int64_t* ukeys, const int64_t* usrc, int
       const long long lo = std::min<long long>(hmm[0], new_score), hi = std::max<long long>(hmm[1], new_score);
       int bits = 1;
       while (bits < 64 && ((unsigned long long)(hi - lo) >> bits) != 0) bits++;
-      GF_LAUNCH(k_score_keys, grid_for(cap, 256, G), 256, 0, s, c->scores, cap, (int64_t)lo, skeys);
+      GF_LAUNCH(k_score_keys, grid_for(cap, 256, G), 256, 0, s, c->scores, cap, (int64_t)lo, skeys, iota);
       cudaEvent_t e0 = g_profile.load(std::memory_order_relaxed) ? prof_start(s) : nullptr;
       GF_TRY(cub_call([&](void* t, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(t, b, skeys, skeys_sorted, iota, sorted_slots, (int)cap, 0, bits, s);
@@ -1074,7 +1068,6 @@ gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, in
   long long *smin, *mm = nullptr, *counts;
   uint8_t* found;
   longlong2 *flag2, *pos2;
-  uint32_t* iota_unused = nullptr;
   void *scan_tmp, *free_tmp = nullptr;
   float* values = d_values;
   auto carve = [&](Arena& a) {
@@ -1093,7 +1086,6 @@ gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, in
       ff = a.take<int64_t>(cap + 1);
       fpos = a.take<int64_t>(cap + 1);
       free_slots = a.take<int64_t>(cap + 1);
-      iota_unused = a.take<uint32_t>(cap);
       mm = a.take<long long>(2);
       free_tmp = a.take<char>((int64_t)free_bytes);
     }
@@ -1125,7 +1117,7 @@ gf_status gf_fetch_features(gf_cache* c, gf_ftable* t, const int64_t* d_keys, in
   // free slots and the occupied score range, ahead of the placement (the fetch changes no key)
   if (lru_lfu) {
     GF_LAUNCH(k_mm_init, 1, 1, 0, s, mm);
-    GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, iota_unused, mm);
+    GF_LAUNCH(k_free_flags, grid_for(cap, 256, G), 256, 0, s, c->keys, c->scores, cap, ff, mm);
     size_t fb = free_bytes;
     GF_CUDA(cub::DeviceScan::ExclusiveSum(free_tmp, fb, ff, fpos, (int)(cap + 1), s));
     GF_LAUNCH(k_free_scatter, grid_for(cap, 256, G), 256, 0, s, ff, fpos, cap, free_slots);

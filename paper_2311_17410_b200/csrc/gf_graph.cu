@@ -1086,6 +1086,10 @@ __global__ void __launch_bounds__(CO_T, 1)
     }
     if (has_eids && lane == 0 && ex != LLONG_MIN) atomicMax(&c->max_eid, ex);
   }
+  // a chunk of one sub-chunk (E <= grid x CO_T, the common case) keeps its hash in shared memory and
+  // each event's slot and rank in registers for phase D, which then skips rebuilding the hash
+  const bool one_sub = c_hi - c_lo <= CO_T;
+  int a_slot = 0, a_lr = 0;
   for (int64_t s0 = c_lo; s0 < c_hi; s0 += CO_T) {
     __syncthreads();
     h_clear();
@@ -1093,9 +1097,8 @@ __global__ void __launch_bounds__(CO_T, 1)
     const int64_t e = s0 + threadIdx.x;
     if (e < c_hi) {
       const int64_t v = node_in(e);
-      int slot;
       if (v < 0 || v >= node_cap) atomicOr((unsigned long long*)&c->abort, (unsigned long long)ABORT_NODES);
-      else h_insert((int32_t)v, slot);
+      else a_lr = h_insert((int32_t)v, a_slot);
     }
     __syncthreads();
     // one counter atomic per (sub-chunk, node); the first to count a node lists it (one segment)
@@ -1183,13 +1186,18 @@ __global__ void __launch_bounds__(CO_T, 1)
   COOP_MARK(2);
   // ---- D: scatter, one counter atomic per (sub-chunk, node); the counters count back to zero ----
   for (int64_t s0 = c_lo; s0 < c_hi; s0 += CO_T) {
-    __syncthreads();
-    h_clear();
-    __syncthreads();
     const int64_t e = s0 + threadIdx.x;
-    int slot = 0, lr = 0;
-    if (e < c_hi) lr = h_insert((int32_t)node_in(e), slot);
-    __syncthreads();
+    int slot = a_slot, lr = a_lr;
+#ifndef GF_AB_NO_HASH_REUSE
+    if (!one_sub)
+#endif
+    {
+      __syncthreads();
+      h_clear();
+      __syncthreads();
+      if (e < c_hi) lr = h_insert((int32_t)node_in(e), slot);
+      __syncthreads();
+    }
     for (int i = threadIdx.x; i < HC; i += CO_T) {
       const int32_t k = sm.h.key[i];
       if (k >= 0) {
