@@ -987,6 +987,13 @@ __global__ void __launch_bounds__(CO_T, 1)
   // go back the other way without a copy either: the last CTA to finish writes them to the pinned
   // host struct `hout` and re-arms `c` for the next call
   const IngestScalars* S = &S_;
+  __shared__ long long s_abort;
+  auto cta_abort = [&]() -> long long {  // c->abort as one value for the whole CTA
+    __syncthreads();
+    if (threadIdx.x == 0) s_abort = __ldcg(&c->abort);
+    __syncthreads();
+    return s_abort;
+  };
   auto finish = [&]() {  // every CTA, on every exit
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1140,7 +1147,7 @@ __global__ void __launch_bounds__(CO_T, 1)
 
   COOP_MARK(1);
   const int64_t nseg = ldl2(&c->num_segs);
-  if (ldl2(&c->abort) & ABORT_NODES) {  // node ids beyond the table (or negative): undo the counts
+  if (cta_abort() & ABORT_NODES) {  // node ids beyond the table (or negative): undo the counts
     for (int64_t i = gtid; i < nseg; i += gstride) CB.ncnt[ldl2(&CB.touched[i])] = 0;
     finish();
     return;
@@ -1216,7 +1223,7 @@ __global__ void __launch_bounds__(CO_T, 1)
     }
   }
   grid.sync();
-  if (ldl2(&c->abort)) {  // a segment beyond one CTA's sort
+  if (cta_abort()) {  // a segment beyond one CTA's sort
     finish();
     return;
   }
@@ -1376,7 +1383,9 @@ __global__ void __launch_bounds__(CO_T, 1)
       [&](int64_t i, int64_t (&o)[3]) { CB.off4[i] = make_longlong4(o[0], o[1], o[2], 0); },
       CB.ctot, reinterpret_cast<int64_t(*)[3]>(s_scan), tot3);
   COOP_MARK(9);
-  if (ldl2(&c->abort)) {  // a possible rejection: the general sequence resolves the batch
+  // abort is read once per CTA: CTA 0 may set ABORT_CAP below while another CTA (or a lagging warp)
+  // is still at this check, and every thread of a CTA must leave through the same finish()
+  if (cta_abort()) {  // a possible rejection: the general sequence resolves the batch
     finish();
     return;
   }

@@ -186,8 +186,9 @@ def _as_device_i64(x, device):
     import torch
 
     if isinstance(x, torch.Tensor):
-        t = x.to(device=device, dtype=torch.int64)
-        return t.contiguous()
+        if x.dtype is torch.int64 and x.device == device and x.is_contiguous():
+            return x  # the common case (device-resident int64 batches): no dispatch at all
+        return x.to(device=device, dtype=torch.int64).contiguous()
     a = np.ascontiguousarray(np.asarray(x, dtype=np.int64))
     return torch.from_numpy(a).to(device)
 
@@ -213,6 +214,7 @@ class DynamicGraph:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
         self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.device = torch.device(self.device.type, self._dev_index)  # "cuda" -> "cuda:k": tensors compare equal
         h = ctypes.c_void_p()
         check(load().gf_graph_create(int(bool(directed)), int(tau), _lib.SIZING_CODE[sizing.kind],
                                      int(sizing.param), self._dev_index, ctypes.byref(h)))
