@@ -23,6 +23,7 @@ on a bounded root sample of the same workload, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import re
@@ -185,8 +186,13 @@ def dist_setup(args):
             # the NCCL communicator-init lines (rank count, NVLink/NVLS transport) go to stderr
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            # failure propagation: the process group's watchdog polls
+            # ncclCommGetAsyncError; on an asynchronous NCCL error or a collective past the timeout
+            # it aborts the communicator and the waiting ranks raise instead of hanging
+            os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
             torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                    timeout=datetime.timedelta(seconds=float(os.environ.get("GF_NCCL_TIMEOUT_S", "600"))))
         # one tiny collective so the communicator (and its INIT log) exists before any timing
         t = torch.ones(1, device=_coll_device())
         dist.all_reduce(t)

@@ -230,6 +230,9 @@ class PartitionedGraph:
         self.P, self.rank = transport.P, transport.rank
         self.directed = directed
         self.next_edge_id = 0
+        # cluster.py:88,97-98: a failed worker answers requests with ErrorMsg(1, "worker failed")
+        self.failed = False
+        self._next_request_id = 0
 
     @property
     def device(self):
@@ -285,6 +288,16 @@ class PartitionedGraph:
     def _merge(self, perm, cnt_sorted, arrays):
         return X.csr_merge(perm, cnt_sorted, arrays)
 
+    @staticmethod
+    def _raise_failed(rid0, sent, cnt_recv):
+        """RemoteRequestError for the first owner whose count chunk does not match the request
+        (cluster.py:264-265): the request to owner d carries id rid0 + d."""
+        for d, (ns, c) in enumerate(zip(sent, cnt_recv)):
+            if int(c.shape[-1]) != int(ns):
+                from .cluster import RemoteRequestError
+
+                raise RemoteRequestError(rid0 + d, "worker failed")
+
     def sample_layer(self, src, tend, keys, fanout: int, policy: SamplingPolicy, seed_h: int):
         import torch
 
@@ -296,9 +309,24 @@ class PartitionedGraph:
         for c in owner_counts:
             chunks.append(qs[:, pos:pos + c])
             pos += c
+        # one request id per (hop, owner), as the reference's origin numbers its requests
+        # (cluster.py:251-252); every rank numbers them the same way
+        rid0 = self._next_request_id
+        self._next_request_id += self.P
         recv = self.t.exchange(chunks)
         q = torch.cat(recv, dim=1)
         per_src = [int(c.shape[1]) for c in recv]
+        if self.failed:
+            # cluster.py:97-98: a failed owner serves nothing.  It still takes part in both answer
+            # exchanges (the collectives stay matched on every rank) and signals the failure through
+            # the split sizes the all-to-all already moves to the host: a count chunk one longer than
+            # the origin's request.  Every origin therefore sees it, fails over the same hop and raises
+            # -- fail-stop, instead of the ranks that sent no request to it hanging in the next hop.
+            back_counts = [torch.full((1, nq + 1), -1, dtype=torch.int64, device=dev) for nq in per_src]
+            back_edges = [torch.zeros((4, 0), dtype=torch.int64, device=dev) for _ in per_src]
+            cnt_recv = self.t.exchange(back_counts)
+            self.t.exchange(back_edges)
+            self._raise_failed(rid0, owner_counts, cnt_recv)
         if q.shape[1]:
             offs, nbr, eid, ts, okeys = self.e.sample(q[0].contiguous(), q[1].contiguous(), q[2].contiguous(), fanout,
                                                       policy, seed_h)
@@ -318,6 +346,7 @@ class PartitionedGraph:
         back_edges = [edges[:, eb[i]:eb[i + 1]] for i in range(len(per_src))]
         cnt_recv = self.t.exchange(back_counts)
         edge_recv = self.t.exchange(back_edges)
+        self._raise_failed(rid0, owner_counts, cnt_recv)
         # merge into the original query order (send order -> request order, one kernel)
         cnt_sorted = torch.cat([c.reshape(-1) for c in cnt_recv])
         edges_sorted = torch.cat(edge_recv, dim=1)

@@ -117,3 +117,45 @@ def test_peer_feature_fetch_threads(cuda_device):
     for r in range(P):
         np.testing.assert_array_equal(out[r][-1][0], ref_cache.keys)
         np.testing.assert_array_equal(out[r][-1][1], ref_cache.scores)
+
+
+def test_partitioned_failed_owner_raises_on_every_rank(cuda_device):
+    """cluster.py:97-98,264-265 on libgfb200 (3 thread ranks, one GPU): a failed owner makes every
+    rank raise RemoteRequestError with the same request id in the same hop; the group recovers."""
+    import paper_2311_17410_b200 as gf
+    from paper_2311_17410_b200.distributed import shard_range
+    from paper_2311_17410_b200.partitioned import GpuEngine, PartitionedGraph, ThreadTransport
+
+    P = 3
+    src, dst, ts = gf.generate_synthetic_arrays(500, 40_000, 2.2, 20_000, seed=2, src_skew=2.2)
+    transports = ThreadTransport.group(P)
+    got = [None] * P
+    errors = []
+
+    def rank_main(r):
+        try:
+            pg = PartitionedGraph(transports[r], GpuEngine(tau=32), directed=False)
+            a, b = shard_range(len(src), P, r)
+            pg.add_edges(src[a:b], dst[a:b], ts[a:b])
+            roots, rts = src[-30:][r::P], ts[-30:][r::P]
+            pg.failed = r == 2
+            rid = None
+            try:
+                pg.sample_khop(roots, rts, [5, 5], gf.SamplingPolicy("uniform"), seed=1)
+            except gf.RemoteRequestError as e:
+                rid = e.request_id
+            pg.failed = False
+            s = pg.sample_khop(roots, rts, [5], gf.SamplingPolicy("recent"), seed=1)
+            got[r] = (rid, int(s.layers[0].offsets[-1]))
+        except Exception as e:  # surface thread failures
+            errors.append(e)
+            transports[r].shared.barrier.abort()
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(P)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert [g[0] for g in got] == [2] * P  # hop 0, owner 2
+    assert all(g[1] > 0 for g in got)

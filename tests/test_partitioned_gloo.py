@@ -150,3 +150,46 @@ def test_partitioned_two_ranks_equal_unpartitioned_directed(tmp_path):
 def test_partitioned_two_ranks_equal_unpartitioned_undirected(tmp_path):
     mp.spawn(_worker, args=(2, _port(), str(tmp_path), False), nprocs=2, join=True)
     _check(tmp_path, False)
+
+
+def _failed_worker(rank, world, port, out_dir):
+    """cluster.py:97-98,264-265 (tests/test_cluster.py:101-108): a failed owner surfaces as a
+    RemoteRequestError carrying the request id -- here on every rank of the SPMD group, in the
+    same hop, so no rank is left waiting in the next exchange."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2311_17410_b200 import RemoteRequestError, SamplingPolicy
+        from paper_2311_17410_b200.distributed import shard_range
+        from paper_2311_17410_b200.partitioned import DistTransport
+
+        pg = _host_partitioned_graph()(DistTransport(), OracleEngine(32), directed=False)
+        src, dst, ts = _stream()
+        a, b = shard_range(len(src), world, rank)
+        pg.add_edges(torch.from_numpy(src[a:b]), torch.from_numpy(dst[a:b]), torch.from_numpy(ts[a:b]))
+        roots = torch.tensor([1, 2, 3], dtype=torch.int64)
+        rts = torch.full((3,), int(ts[-1]), dtype=torch.int64)
+        # healthy group first: the layer completes on both ranks
+        pg.sample_khop(roots, rts, [4], SamplingPolicy("recent"), seed=0)
+        pg.failed = rank == 1
+        got = -1
+        try:
+            pg.sample_khop(roots, rts, [4, 3], SamplingPolicy("recent"), seed=0)
+        except RemoteRequestError as err:
+            got = err.request_id
+        # the group is still usable afterwards: the exchanges stayed matched
+        pg.failed = False
+        ok = pg.sample_khop(roots, rts, [4], SamplingPolicy("recent"), seed=0)
+        np.save(os.path.join(out_dir, f"fail{rank}.npy"),
+                np.array([got, int(ok.layers[0].offsets[-1])], dtype=np.int64))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partitioned_failed_owner_raises_request_id(tmp_path):
+    mp.spawn(_failed_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    a, b = (np.load(tmp_path / f"fail{r}.npy") for r in range(2))
+    # hop 0 of the second sample_khop call (ids 2P..3P-1 after the first call's one hop); owner 1
+    assert a[0] == b[0] == 2 + 1
+    assert a[1] > 0 and b[1] > 0
